@@ -1,0 +1,156 @@
+/* pf_gpu.h — C-ABI of the B200-native per-step grid update (pedflow-b200).
+ *
+ * Drop-in boundary for the reference's hot path: the C++ class
+ * pedflow::StepEngine (/root/reference/proj/include/pedflow/engine.hpp:48-66)
+ * and its setup call new_environment (include/pedflow/state.hpp:37). The
+ * reference has no FFI; this header is what a binding to that path needs:
+ * plain pointers and sizes, no exceptions, no C++ or torch types. The C++
+ * shim include/pedflow_gpu.hpp re-exposes it as pedflow::gpu::StepEngine.
+ *
+ * Status codes mirror the reference's error classes (inc/errors.hpp:9-11,
+ * tools/pedflow.cpp:253-258): PF_ERR_CONFIG is ConfigError; PF_ERR_STATE is
+ * the std::logic_error("state corrupt: ...") of check_consistency
+ * (src/state.cpp:77-110). pf_last_error() gives the message (thread-local).
+ */
+#ifndef PF_GPU_H
+#define PF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_CONFIG 2 /* ConfigError: invalid scenario parameters */
+#define PF_ERR_CUDA 3   /* CUDA runtime failure (no device, OOM, launch error) */
+#define PF_ERR_COMM 4   /* halo exchange failure */
+#define PF_ERR_STATE 5  /* state corrupt: inconsistent planes passed to pf_load_state */
+#define PF_ERR_ARG 6    /* bad argument (null pointer, replica out of range) */
+
+#define PF_MODEL_LEM 0
+#define PF_MODEL_ACO 1
+
+#define PF_KERNEL_FUSED 0    /* one kernel per step (default) */
+#define PF_KERNEL_PIPELINE 1 /* propose / resolve / commit, three kernels per step */
+
+/* Number of ghost rows kept above and below a row shard: one step's
+ * dependency radius. */
+#define PF_GHOST_ROWS 3
+
+/* ScenarioConfig numerics (inc/config.hpp:20-58) + the GPU's additions.
+ * replaces: pedflow::ScenarioConfig + EngineOptions::from_config
+ * (src/engine.cpp:35-46). */
+typedef struct pf_config {
+    int32_t width, height, agents_per_side, model;
+    uint64_t seed; /* replica i runs seed + i (tools/pedflow.cpp:135 repeat schedule) */
+    double d0, sel_mu, sel_sigma, alpha, beta, rho, tau0, q;
+    int32_t replicas;  /* >= 1 independent scenarios stepped by one launch */
+    int32_t row_begin; /* owned global rows [row_begin, row_end) of a row shard; */
+    int32_t row_end;   /* row_end == 0 means the whole grid */
+    int32_t device;    /* CUDA device ordinal */
+    int32_t kernel;    /* PF_KERNEL_FUSED or PF_KERNEL_PIPELINE */
+} pf_config;
+
+/* Byte-identical to pedflow::AgentRecord (inc/grid.hpp:84-93), 40 bytes. */
+typedef struct pf_agent {
+    uint32_t index; /* 1-based id */
+    uint8_t group;  /* 1 Top, 2 Bottom */
+    int32_t row, col, future_row, future_col;
+    double tour_length;
+    uint8_t crossed;
+} pf_agent;
+
+/* Byte-identical to pedflow::StepReport (inc/engine.hpp:16-21). */
+typedef struct pf_step_report {
+    uint32_t step, moved, newly_crossed_top, newly_crossed_bottom;
+} pf_step_report;
+
+typedef struct pf_ctx pf_ctx;
+
+/* Ghost/boundary rows of one replica's current planes, for the halo
+ * exchange of a row shard. All three are contiguous device ranges. */
+typedef struct pf_halo_rows {
+    void* cells; size_t cell_bytes; /* PF_GHOST_ROWS rows of u32 cell words */
+    void* tau;   size_t tau_bytes;  /* PF_GHOST_ROWS rows of {f64 top, f64 bottom} (ACO) */
+    void* tour;  size_t tour_bytes; /* 1 row of f64 tour lengths (ACO) */
+} pf_halo_rows;
+
+const char* pf_last_error(void);
+const char* pf_version(void);
+
+/* validate() (src/config.cpp:101-124) plus the GPU preconditions:
+ * W*H < 2^32, 2n < 2^29, shard rows >= PF_GHOST_ROWS. */
+int pf_validate(const pf_config* cfg);
+
+/* band_height (src/metrics.cpp:8-11). */
+int32_t pf_band_height(int32_t agents_per_side, int32_t width);
+
+/* new_environment (src/state.cpp:54-75) on the host, into caller-owned
+ * planes: occ[H*W], index[H*W], agents[2n], tau_top/tau_bot[H*W] (ACO; may
+ * be NULL for LEM). */
+int pf_new_environment(const pf_config* cfg, uint64_t seed, uint8_t* occ, uint32_t* index, pf_agent* agents,
+                       double* tau_top, double* tau_bot);
+
+/* replaces: StepEngine::StepEngine(EngineOptions) (inc/engine.hpp:51). */
+int pf_create(const pf_config* cfg, pf_ctx** out);
+int pf_destroy(pf_ctx* ctx);
+
+/* new_environment for every replica (seed + i), built on the host and
+ * uploaded; for a shard only the owned rows and ghost rows travel. */
+int pf_init_environment(pf_ctx* ctx);
+
+/* Upload / download one replica's SimState (inc/state.hpp:16-31) as the
+ * reference's planes over the GLOBAL grid. A shard reads rows
+ * [row_begin-3, row_end+3) and writes back only its owned rows (agents living
+ * there). n_agents must be 2*agents_per_side. */
+int pf_load_state(pf_ctx* ctx, int32_t replica, const uint8_t* occ, const uint32_t* index, const pf_agent* agents,
+                  uint32_t n_agents, const double* tau_top, const double* tau_bot, uint32_t step);
+int pf_store_state(pf_ctx* ctx, int32_t replica, uint8_t* occ, uint32_t* index, pf_agent* agents, uint32_t n_agents,
+                   double* tau_top, double* tau_bot, uint32_t* step);
+
+/* replaces: StepEngine::step(SimState&) x n (src/engine.cpp:53-62).
+ * Runs n full steps on every replica; out (may be NULL) receives
+ * [replicas][n] reports. Synchronous. */
+int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out);
+
+/* Asynchronous variant: enqueue n steps on the context's stream; reports
+ * stay on the device until pf_read_reports (which synchronizes). */
+int pf_step_async(pf_ctx* ctx, uint32_t n);
+int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n);
+int pf_synchronize(pf_ctx* ctx);
+
+/* Device-timed step loop: enqueue n steps bracketed by CUDA events on the
+ * context stream. *total_ms = step loop; *kernel_ms = mean duration of the
+ * dominant (step) kernel measured with per-launch events in a second pass
+ * when kernel_ms is non-NULL (state advances by 2n steps in that case). */
+int pf_time_steps(pf_ctx* ctx, uint32_t n, float* total_ms, float* kernel_ms);
+
+uint32_t pf_current_step(const pf_ctx* ctx);
+void* pf_stream(pf_ctx* ctx); /* cudaStream_t */
+
+/* Count of CUDA kernel launches issued by this context since creation. */
+uint64_t pf_launch_count(const pf_ctx* ctx);
+
+/* Halo exchange support for row shards: side 0 = the rows toward row 0,
+ * side 1 = toward row H-1; recv 0 = this shard's boundary rows to send,
+ * recv 1 = its ghost rows to fill. Valid for the current step parity. */
+int pf_halo(pf_ctx* ctx, int32_t replica, int32_t side, int32_t recv, pf_halo_rows* out);
+
+/* Device-to-device halo exchange between two vertically adjacent shards
+ * (upper owns the rows just above lower) on the same or peer devices. */
+int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower);
+
+/* Device self-test of the keyed generator (src/rng.cpp:43-59,152-156): for
+ * n keys computes random_bits, uniform and normal(mu, sigma) ON THE DEVICE
+ * (the same device functions the step kernels use). Pins the device RNG and
+ * AS241 quantile against the oracle. Outputs may be NULL. */
+int pf_selftest_rng(int32_t device, uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                    const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits_out,
+                    double* uniform_out, double* normal_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,224 @@
+"""ctypes binding of the C-ABI in include/pf_gpu.h (libpedflow_b200.so).
+
+There is no fallback: if the shared library is missing, importing this module
+raises; if no CUDA device is present, creating a context raises. Every call
+that fails raises the Python mirror of the reference's exception class
+(ConfigError for PF_ERR_CONFIG, StateCorrupt for PF_ERR_STATE, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpedflow_b200.so")
+
+PF_OK, PF_ERR_CONFIG, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, 2, 3, 4, 5, 6
+PF_MODEL_LEM, PF_MODEL_ACO = 0, 1
+PF_KERNEL_FUSED, PF_KERNEL_PIPELINE = 0, 1
+PF_GHOST_ROWS = 3
+
+# pedflow::AgentRecord (inc/grid.hpp:84-93) == pf_agent, 40 bytes.
+AGENT_DTYPE = np.dtype(
+    {
+        "names": ["index", "group", "row", "col", "future_row", "future_col", "tour_length", "crossed"],
+        "formats": ["<u4", "u1", "<i4", "<i4", "<i4", "<i4", "<f8", "u1"],
+        "offsets": [0, 4, 8, 12, 16, 20, 24, 32],
+        "itemsize": 40,
+    }
+)
+# pedflow::StepReport (inc/engine.hpp:16-21) == pf_step_report.
+REPORT_DTYPE = np.dtype(
+    [("step", "<u4"), ("moved", "<u4"), ("newly_crossed_top", "<u4"), ("newly_crossed_bottom", "<u4")]
+)
+
+
+class ConfigError(ValueError):
+    """pedflow::ConfigError (inc/errors.hpp:9-11)."""
+
+
+class StateCorrupt(RuntimeError):
+    """The std::logic_error("state corrupt: ...") of check_consistency (src/state.cpp:77-110)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure inside the library (no device, out of memory, launch error)."""
+
+
+class CommError(RuntimeError):
+    """Halo-exchange failure between row shards."""
+
+
+class PfConfig(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32), ("height", C.c_int32), ("agents_per_side", C.c_int32), ("model", C.c_int32),
+        ("seed", C.c_uint64),
+        ("d0", C.c_double), ("sel_mu", C.c_double), ("sel_sigma", C.c_double), ("alpha", C.c_double),
+        ("beta", C.c_double), ("rho", C.c_double), ("tau0", C.c_double), ("q", C.c_double),
+        ("replicas", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32), ("device", C.c_int32),
+        ("kernel", C.c_int32),
+    ]
+
+
+class PfHalo(C.Structure):
+    _fields_ = [
+        ("cells", C.c_void_p), ("cell_bytes", C.c_size_t),
+        ("tau", C.c_void_p), ("tau_bytes", C.c_size_t),
+        ("tour", C.c_void_p), ("tour_bytes", C.c_size_t),
+    ]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA library first "
+        "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback."
+    )
+
+lib = C.CDLL(LIB_PATH)
+_vp, _i32, _u32, _u64 = C.c_void_p, C.c_int32, C.c_uint32, C.c_uint64
+_sigs = {
+    "pf_last_error": (C.c_char_p, []),
+    "pf_version": (C.c_char_p, []),
+    "pf_validate": (C.c_int, [C.POINTER(PfConfig)]),
+    "pf_band_height": (_i32, [_i32, _i32]),
+    "pf_new_environment": (C.c_int, [C.POINTER(PfConfig), _u64, _vp, _vp, _vp, _vp, _vp]),
+    "pf_create": (C.c_int, [C.POINTER(PfConfig), C.POINTER(_vp)]),
+    "pf_destroy": (C.c_int, [_vp]),
+    "pf_init_environment": (C.c_int, [_vp]),
+    "pf_load_state": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _u32, _vp, _vp, _u32]),
+    "pf_store_state": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _u32, _vp, _vp, C.POINTER(_u32)]),
+    "pf_step": (C.c_int, [_vp, _u32, _vp]),
+    "pf_step_async": (C.c_int, [_vp, _u32]),
+    "pf_read_reports": (C.c_int, [_vp, _vp, _u32]),
+    "pf_synchronize": (C.c_int, [_vp]),
+    "pf_time_steps": (C.c_int, [_vp, _u32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "pf_current_step": (_u32, [_vp]),
+    "pf_stream": (_vp, [_vp]),
+    "pf_launch_count": (_u64, [_vp]),
+    "pf_halo": (C.c_int, [_vp, _i32, _i32, _i32, C.POINTER(PfHalo)]),
+    "pf_exchange_pair": (C.c_int, [_vp, _vp]),
+    "pf_selftest_rng": (C.c_int, [_i32, _u32, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double, _vp, _vp, _vp]),
+}
+for _name, (_res, _args) in _sigs.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED_SYMBOLS = tuple(_sigs)
+
+
+def check(rc: int) -> None:
+    if rc == PF_OK:
+        return
+    msg = lib.pf_last_error().decode(errors="replace")
+    if rc == PF_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == PF_ERR_STATE:
+        raise StateCorrupt(msg)
+    if rc == PF_ERR_CUDA:
+        raise DeviceError(msg)
+    if rc == PF_ERR_COMM:
+        raise CommError(msg)
+    raise ValueError(f"pedflow-b200 error {rc}: {msg}")
+
+
+def ptr(a) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+class Context:
+    """Owns one pf_ctx: R replicas of one grid (or one row shard of it) on one device."""
+
+    def __init__(self, cfg: PfConfig):
+        self.cfg = cfg
+        h = C.c_void_p()
+        check(lib.pf_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.pf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def replicas(self) -> int:
+        return self.cfg.replicas
+
+    @property
+    def aco(self) -> bool:
+        return self.cfg.model == PF_MODEL_ACO
+
+    def init_environment(self):
+        check(lib.pf_init_environment(self.h))
+
+    def load(self, replica, occ, index, agents, tau_top, tau_bot, step):
+        check(lib.pf_load_state(self.h, replica, ptr(occ), ptr(index), ptr(agents) if len(agents) else None,
+                                len(agents), ptr(tau_top), ptr(tau_bot), step))
+
+    def store(self, replica, occ, index, agents, tau_top, tau_bot) -> int:
+        step = C.c_uint32(0)
+        check(lib.pf_store_state(self.h, replica, ptr(occ), ptr(index), ptr(agents) if len(agents) else None,
+                                 len(agents), ptr(tau_top), ptr(tau_bot), C.byref(step)))
+        return step.value
+
+    def step(self, n: int, want_reports: bool = True) -> np.ndarray | None:
+        out = np.zeros((self.replicas, n), REPORT_DTYPE) if want_reports and n else None
+        check(lib.pf_step(self.h, n, ptr(out)))
+        return out
+
+    def step_async(self, n: int):
+        check(lib.pf_step_async(self.h, n))
+
+    def read_reports(self, n: int) -> np.ndarray:
+        out = np.zeros((self.replicas, n), REPORT_DTYPE)
+        check(lib.pf_read_reports(self.h, ptr(out), n))
+        return out
+
+    def synchronize(self):
+        check(lib.pf_synchronize(self.h))
+
+    def time_steps(self, n: int, kernel: bool = False) -> tuple[float, float | None]:
+        tot, ker = C.c_float(0), C.c_float(0)
+        check(lib.pf_time_steps(self.h, n, C.byref(tot), C.byref(ker) if kernel else None))
+        return tot.value, (ker.value if kernel else None)
+
+    @property
+    def current_step(self) -> int:
+        return lib.pf_current_step(self.h)
+
+    @property
+    def launches(self) -> int:
+        return lib.pf_launch_count(self.h)
+
+    def stream(self) -> int:
+        return lib.pf_stream(self.h)
+
+    def halo(self, replica: int, side: int, recv: bool) -> PfHalo:
+        h = PfHalo()
+        check(lib.pf_halo(self.h, replica, side, 1 if recv else 0, C.byref(h)))
+        return h
+
+
+def exchange_pair(upper: Context, lower: Context) -> None:
+    check(lib.pf_exchange_pair(upper.h, lower.h))
+
+
+def selftest_rng(seed, step, phase, entity, counter, mu=0.0, sigma=1.0, device=0):
+    """Device random_bits / uniform / normal for arrays of keys (pf_selftest_rng)."""
+    seed = np.ascontiguousarray(seed, np.uint64)
+    n = len(seed)
+    step = np.ascontiguousarray(np.broadcast_to(step, n), np.uint32)
+    phase = np.ascontiguousarray(np.broadcast_to(phase, n), np.uint32)
+    entity = np.ascontiguousarray(np.broadcast_to(entity, n), np.uint64)
+    counter = np.ascontiguousarray(np.broadcast_to(counter, n), np.uint32)
+    bits = np.zeros(n, np.uint64)
+    uni = np.zeros(n, np.float64)
+    nrm = np.zeros(n, np.float64)
+    check(lib.pf_selftest_rng(device, n, ptr(seed), ptr(step), ptr(phase), ptr(entity), ptr(counter), mu, sigma,
+                              ptr(bits), ptr(uni), ptr(nrm)))
+    return bits, uni, nrm

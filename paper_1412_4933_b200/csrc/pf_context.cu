@@ -1,0 +1,636 @@
+// C-ABI of pedflow-b200 (include/pf_gpu.h): context lifetime, state
+// upload/download, the step loop (CUDA-graph batched), halo support.
+#include "../../include/pf_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "pf_internal.h"
+#include "pf_setup.h"
+
+using pfdev::kWall;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define PF_CUDA(call)                                                                             \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) return fail(PF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int kBatchCap = 256;  // steps per captured graph / report slab
+
+}  // namespace
+
+struct pf_ctx {
+    pf_config cfg{};
+    pfk::StepArgs args{};
+    int rows_owned = 0, rows_buf = 0, row_begin = 0;
+    int parity = 0;                 // buffer holding the current state
+    uint32_t step = 0;              // host mirror of the device step counter
+    uint32_t* d_step = nullptr;
+    uint32_t* d_reports = nullptr;  // [replicas][kBatchCap][4]
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
+    std::vector<void*> allocs;
+    bool aco() const { return cfg.model == PF_MODEL_ACO; }
+    size_t plane() const { return size_t(rows_buf) * size_t(cfg.width); }
+    size_t total() const { return plane() * size_t(cfg.replicas); }
+};
+
+extern "C" {
+
+const char* pf_last_error(void) { return g_err.c_str(); }
+const char* pf_version(void) { return "pedflow-b200 0.1 (sm_100a)"; }
+
+int32_t pf_band_height(int32_t n, int32_t w) { return pfhost::band_height(n, w); }
+
+int pf_validate(const pf_config* c) {
+    if (!c) return fail(PF_ERR_ARG, "null config");
+    // validate() (src/config.cpp:101-124)
+    if (c->width < 16 || c->width % 16 != 0) return fail(PF_ERR_CONFIG, "width must be a multiple of 16 and >= 16");
+    if (c->height < 16 || c->height % 16 != 0) return fail(PF_ERR_CONFIG, "height must be a multiple of 16 and >= 16");
+    if (c->agents_per_side < 0) return fail(PF_ERR_CONFIG, "agents_per_side must be >= 0");
+    if (c->model != PF_MODEL_LEM && c->model != PF_MODEL_ACO) return fail(PF_ERR_CONFIG, "malformed value for key 'model'");
+    if (!(c->d0 > 1.0)) return fail(PF_ERR_CONFIG, "d0 must be > 1");
+    if (!(c->sel_sigma >= 0.0)) return fail(PF_ERR_CONFIG, "sel_sigma must be >= 0");
+    if (!(c->alpha >= 0.0)) return fail(PF_ERR_CONFIG, "alpha must be >= 0");
+    if (!(c->beta >= 0.0)) return fail(PF_ERR_CONFIG, "beta must be >= 0");
+    if (!(c->rho > 0.0 && c->rho <= 1.0)) return fail(PF_ERR_CONFIG, "rho must be in (0, 1]");
+    if (!(c->tau0 > 0.0)) return fail(PF_ERR_CONFIG, "tau0 must be > 0");
+    if (!(c->q > 0.0)) return fail(PF_ERR_CONFIG, "q must be > 0");
+    const int64_t cells = int64_t(c->width) * c->height;
+    if (2 * int64_t(c->agents_per_side) > cells)
+        return fail(PF_ERR_CONFIG, "agents_per_side exceeds grid capacity (width * height / 2)");
+    const int band = pfhost::band_height(c->agents_per_side, c->width);
+    if (2 * band > c->height)
+        return fail(PF_ERR_CONFIG, "agents_per_side needs more placement rows than the grid height allows");
+    // GPU preconditions
+    if (cells >= (int64_t(1) << 32)) return fail(PF_ERR_CONFIG, "width * height must be < 2^32");
+    if (2 * int64_t(c->agents_per_side) >= (int64_t(1) << 29)) return fail(PF_ERR_CONFIG, "2 * agents_per_side must be < 2^29");
+    if (c->replicas < 1) return fail(PF_ERR_CONFIG, "replicas must be >= 1");
+    if (c->replicas > 65535) return fail(PF_ERR_CONFIG, "replicas must be <= 65535");
+    if (c->kernel != PF_KERNEL_FUSED && c->kernel != PF_KERNEL_PIPELINE) return fail(PF_ERR_CONFIG, "unknown kernel");
+    if (c->row_end != 0) {
+        if (c->row_begin < 0 || c->row_end > c->height || c->row_begin >= c->row_end)
+            return fail(PF_ERR_CONFIG, "shard rows must satisfy 0 <= row_begin < row_end <= height");
+        if (c->row_end - c->row_begin < PF_GHOST_ROWS)
+            return fail(PF_ERR_CONFIG, "a row shard must own at least PF_GHOST_ROWS rows");
+    }
+    return PF_OK;
+}
+
+int pf_new_environment(const pf_config* c, uint64_t seed, uint8_t* occ, uint32_t* index, pf_agent* agents,
+                       double* tau_top, double* tau_bot) {
+    pf_config v = *c;
+    v.replicas = 1;
+    v.row_begin = v.row_end = 0;
+    if (int rc = pf_validate(&v)) return rc;
+    if (!occ || !index || (!agents && c->agents_per_side > 0)) return fail(PF_ERR_ARG, "null plane");
+    const size_t cells = size_t(c->width) * size_t(c->height);
+    std::memset(occ, 0, cells);
+    std::memset(index, 0, cells * 4);
+    if (c->agents_per_side > 0) std::memset(agents, 0, sizeof(pf_agent) * 2 * size_t(c->agents_per_side));
+    if (c->model == PF_MODEL_ACO && tau_top && tau_bot) {
+        std::fill(tau_top, tau_top + cells, c->tau0);
+        std::fill(tau_bot, tau_bot + cells, c->tau0);
+    }
+    const uint32_t W = uint32_t(c->width);
+    pfhost::place_all(c->width, c->height, c->agents_per_side, seed, [&](uint32_t cell, uint32_t id, uint32_t g) {
+        occ[cell] = uint8_t(g);
+        index[cell] = id;
+        pf_agent& a = agents[id - 1];
+        a.index = id;
+        a.group = uint8_t(g);
+        a.row = a.future_row = int32_t(cell / W);
+        a.col = a.future_col = int32_t(cell % W);
+        a.tour_length = 0.0;
+        a.crossed = 0;
+    });
+    return PF_OK;
+}
+
+int pf_destroy(pf_ctx* ctx) {
+    if (!ctx) return PF_OK;
+    cudaSetDevice(ctx->cfg.device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    for (void* p : ctx->allocs) cudaFree(p);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return PF_OK;
+}
+
+static int fill_consts(pf_ctx* ctx) {
+    const pf_config& c = ctx->cfg;
+    pfdev::StepConsts& k = ctx->args.k;
+    // distance_table (src/grid.cpp:10-27) and the host-side factors the
+    // reference computes once: dmin/d_i (src/lem.cpp:11-16), (1/d_i)^beta
+    // (src/aco.cpp:24), 1 - rho (src/engine.cpp:126), sqrt(2) (src/aco.cpp:11).
+    const int f[8] = {+1, +1, +1, 0, 0, -1, -1, -1};
+    const int l[8] = {0, 1, 1, 1, 1, 0, 1, 1};
+    double d[8];
+    for (int i = 0; i < 8; ++i) d[i] = std::sqrt((c.d0 - f[i]) * (c.d0 - f[i]) + double(l[i] * l[i]));
+    for (int i = 0; i < 8; ++i) {
+        k.lem_score[i] = d[0] / d[i];
+        k.eta[i] = std::pow(1.0 / d[i], c.beta);
+    }
+    k.sel_mu = c.sel_mu;
+    k.sel_sigma = c.sel_sigma;
+    k.alpha = c.alpha;
+    k.alpha_mode = c.alpha == 1.0 ? 0 : (c.alpha == 0.0 ? 1 : 2);
+    k.factor = 1.0 - c.rho;
+    k.q = c.q;
+    k.diag = std::sqrt(2.0);
+    k.model = c.model;
+    k.W = c.width;
+    k.H = c.height;
+    k.band = pfhost::band_height(c.agents_per_side, c.width);
+    return PF_OK;
+}
+
+int pf_create(const pf_config* cfg, pf_ctx** out) {
+    if (!out) return fail(PF_ERR_ARG, "null out");
+    *out = nullptr;
+    if (int rc = pf_validate(cfg)) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PF_ERR_CUDA, "no CUDA device available");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(PF_ERR_CONFIG, "device ordinal out of range");
+    auto* ctx = new pf_ctx();
+    ctx->cfg = *cfg;
+    ctx->row_begin = cfg->row_end ? cfg->row_begin : 0;
+    ctx->rows_owned = cfg->row_end ? cfg->row_end - cfg->row_begin : cfg->height;
+    ctx->rows_buf = ctx->rows_owned + 2 * pfk::kGhost;
+    fill_consts(ctx);
+    auto cleanup = [&](int rc) {
+        pf_destroy(ctx);
+        return rc;
+    };
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "cudaSetDevice failed"));
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(PF_ERR_CUDA, "cudaStreamCreate failed"));
+    auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+        ctx->allocs.push_back(p);
+        return p;
+    };
+    const size_t n = ctx->total();
+    pfk::Planes& P = ctx->args.p;
+    P.plane = ctx->plane();
+    P.cell[0] = static_cast<uint32_t*>(alloc(n * 4));
+    P.cell[1] = static_cast<uint32_t*>(alloc(n * 4));
+    bool ok = P.cell[0] && P.cell[1];
+    if (ctx->aco()) {
+        P.tau[0] = static_cast<double2*>(alloc(n * 16));
+        P.tau[1] = static_cast<double2*>(alloc(n * 16));
+        P.tour = static_cast<double*>(alloc(n * 8));
+        ok = ok && P.tau[0] && P.tau[1] && P.tour;
+    }
+    if (cfg->kernel == PF_KERNEL_PIPELINE) {
+        P.intent = static_cast<uint8_t*>(alloc(n));
+        P.win = static_cast<uint8_t*>(alloc(n));
+        ok = ok && P.intent && P.win;
+    }
+    ctx->d_step = static_cast<uint32_t*>(alloc(4));
+    auto* kc = static_cast<pfdev::StepConsts*>(alloc(sizeof(pfdev::StepConsts)));
+    ok = ok && kc && cudaMemcpy(kc, &ctx->args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice) == cudaSuccess;
+    ctx->args.kc = kc;
+    ctx->d_reports = static_cast<uint32_t*>(alloc(size_t(cfg->replicas) * kBatchCap * 16));
+    if (!ok || !ctx->d_step || !ctx->d_reports) {
+        cudaGetLastError();
+        return cleanup(fail(PF_ERR_CUDA, "device allocation failed (out of memory?)"));
+    }
+    if (cudaMemsetAsync(P.cell[0], 0, n * 4, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(P.cell[1], 0, n * 4, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(ctx->d_step, 0, 4, ctx->stream) != cudaSuccess)
+        return cleanup(fail(PF_ERR_CUDA, "cudaMemset failed"));
+    if (P.intent) {
+        ctx->launches += pfk::launch_fill_u8(P.intent, n, pfdev::kNone, ctx->stream);
+        ctx->launches += pfk::launch_fill_u8(P.win, n, pfdev::kNone, ctx->stream);
+    }
+    ctx->args.seed_base = cfg->seed;
+    ctx->args.d_step = ctx->d_step;
+    ctx->args.reports = ctx->d_reports;
+    ctx->args.batch_cap = kBatchCap;
+    ctx->args.row_begin = ctx->row_begin;
+    ctx->args.rows_owned = ctx->rows_owned;
+    ctx->args.rows_buf = ctx->rows_buf;
+    ctx->args.replicas = cfg->replicas;
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "init failed"));
+    *out = ctx;
+    return PF_OK;
+}
+
+// Global row of buffer row b.
+static inline int64_t grow_of(const pf_ctx* ctx, int b) { return int64_t(ctx->row_begin) - pfk::kGhost + b; }
+
+// Upload one replica's buffer-row planes (cells + tour) and set the step.
+static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& words, const std::vector<double>* tour,
+                          const std::vector<double2>* tau) {
+    const size_t off = size_t(rep) * ctx->plane();
+    pfk::Planes& P = ctx->args.p;
+    PF_CUDA(cudaMemcpyAsync(P.cell[0] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->aco()) {
+        if (tour) PF_CUDA(cudaMemcpyAsync(P.tour + off, tour->data(), ctx->plane() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
+        if (tau) {
+            PF_CUDA(cudaMemcpyAsync(P.tau[0] + off, tau->data(), ctx->plane() * 16, cudaMemcpyHostToDevice, ctx->stream));
+            PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, tau->data(), ctx->plane() * 16, cudaMemcpyHostToDevice, ctx->stream));
+        } else {
+            ctx->launches += pfk::launch_fill_tau(P.tau[0] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
+            ctx->launches += pfk::launch_fill_tau(P.tau[1] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
+        }
+    }
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PF_OK;
+}
+
+static void set_step(pf_ctx* ctx, uint32_t step) {
+    ctx->step = step;
+    cudaMemcpyAsync(ctx->d_step, &ctx->step, 4, cudaMemcpyHostToDevice, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+}
+
+int pf_init_environment(pf_ctx* ctx) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    const pf_config& c = ctx->cfg;
+    const uint32_t W = uint32_t(c.width);
+    // Placement is host work; replicas are independent, so build them on
+    // worker threads and upload in order.
+    const int R = c.replicas;
+    const int nthreads = std::max(1, std::min<int>(R, int(std::thread::hardware_concurrency())));
+    std::vector<std::vector<uint32_t>> words(std::min(R, nthreads));
+    for (int r0 = 0; r0 < R; r0 += nthreads) {
+        const int nb = std::min(nthreads, R - r0);
+        std::vector<std::thread> ts;
+        for (int t = 0; t < nb; ++t) {
+            ts.emplace_back([&, t] {
+                std::vector<uint32_t>& w = words[size_t(t)];
+                w.assign(ctx->plane(), 0u);
+                for (int b = 0; b < ctx->rows_buf; ++b) {
+                    const int64_t g = grow_of(ctx, b);
+                    if (g < 0 || g >= c.height) std::fill(w.begin() + size_t(b) * W, w.begin() + size_t(b + 1) * W, kWall);
+                }
+                const int64_t lo = grow_of(ctx, 0), hi = grow_of(ctx, ctx->rows_buf);
+                pfhost::place_all(c.width, c.height, c.agents_per_side, c.seed + uint64_t(r0 + t),
+                                  [&](uint32_t cell, uint32_t id, uint32_t g) {
+                                      const int64_t row = cell / W;
+                                      if (row < lo || row >= hi) return;
+                                      w[size_t(row - lo) * W + cell % W] = id | (g << 30);
+                                  });
+            });
+        }
+        for (auto& t : ts) t.join();
+        for (int t = 0; t < nb; ++t)
+            if (int rc = upload_replica(ctx, r0 + t, words[size_t(t)], nullptr, nullptr)) return rc;
+    }
+    ctx->parity = 0;
+    set_step(ctx, 0);
+    return PF_OK;
+}
+
+int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* index, const pf_agent* agents,
+                  uint32_t n_agents, const double* tau_top, const double* tau_bot, uint32_t step) {
+    if (!ctx || !occ || !index) return fail(PF_ERR_ARG, "null argument");
+    if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
+    const pf_config& c = ctx->cfg;
+    if (n_agents != 2u * uint32_t(c.agents_per_side)) return fail(PF_ERR_STATE, "state corrupt: agent count disagrees with config");
+    if (n_agents && !agents) return fail(PF_ERR_ARG, "null agents");
+    if (ctx->aco() && (!tau_top || !tau_bot)) return fail(PF_ERR_ARG, "ACO state needs both pheromone fields");
+    PF_CUDA(cudaSetDevice(c.device));
+    const size_t W = size_t(c.width);
+    std::vector<uint32_t> words(ctx->plane(), 0u);
+    std::vector<double> tour(ctx->aco() ? ctx->plane() : 0, 0.0);
+    std::vector<double2> tau(ctx->aco() ? ctx->plane() : 0, make_double2(0.0, 0.0));
+    for (int b = 0; b < ctx->rows_buf; ++b) {
+        const int64_t g = grow_of(ctx, b);
+        uint32_t* wrow = words.data() + size_t(b) * W;
+        if (g < 0 || g >= c.height) {
+            std::fill(wrow, wrow + W, kWall);
+            continue;
+        }
+        for (size_t col = 0; col < W; ++col) {
+            const size_t gi = size_t(g) * W + col;
+            const uint32_t id = index[gi];
+            if (ctx->aco()) tau[size_t(b) * W + col] = make_double2(tau_top[gi], tau_bot[gi]);
+            if ((id == 0) != (occ[gi] == 0)) return fail(PF_ERR_STATE, "state corrupt: index/occupancy mismatch");
+            if (id == 0) continue;
+            if (id > n_agents) return fail(PF_ERR_STATE, "state corrupt: index out of agent range");
+            const pf_agent& a = agents[id - 1];
+            if (a.index != id) return fail(PF_ERR_STATE, "state corrupt: agent record id mismatch");
+            if (a.row != g || a.col != int32_t(col)) return fail(PF_ERR_STATE, "state corrupt: agent position disagrees with index grid");
+            if (a.group != occ[gi] || (a.group != 1 && a.group != 2)) return fail(PF_ERR_STATE, "state corrupt: agent group disagrees with occupancy");
+            wrow[col] = id | (a.crossed ? pfdev::kCrossedBit : 0u) | (uint32_t(a.group) << 30);
+            if (ctx->aco()) tour[size_t(b) * W + col] = a.tour_length;
+        }
+    }
+    if (int rc = upload_replica(ctx, rep, words, ctx->aco() ? &tour : nullptr, ctx->aco() ? &tau : nullptr)) return rc;
+    // Both buffers now hold the state; keep the current parity.
+    set_step(ctx, step);
+    return PF_OK;
+}
+
+int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_agent* agents, uint32_t n_agents,
+                   double* tau_top, double* tau_bot, uint32_t* step) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
+    const pf_config& c = ctx->cfg;
+    PF_CUDA(cudaSetDevice(c.device));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t W = size_t(c.width);
+    const size_t own = size_t(ctx->rows_owned) * W;
+    const size_t off = size_t(rep) * ctx->plane() + size_t(pfk::kGhost) * W;
+    const pfk::Planes& P = ctx->args.p;
+    std::vector<uint32_t> words(own);
+    PF_CUDA(cudaMemcpy(words.data(), P.cell[ctx->parity] + off, own * 4, cudaMemcpyDeviceToHost));
+    std::vector<double> tour;
+    std::vector<double2> tau;
+    if (ctx->aco()) {
+        tour.resize(own);
+        tau.resize(own);
+        PF_CUDA(cudaMemcpy(tour.data(), P.tour + off, own * 8, cudaMemcpyDeviceToHost));
+        PF_CUDA(cudaMemcpy(tau.data(), P.tau[ctx->parity] + off, own * 16, cudaMemcpyDeviceToHost));
+    }
+    const size_t g0 = size_t(ctx->row_begin) * W;
+    for (size_t i = 0; i < own; ++i) {
+        const uint32_t w = words[i];
+        const size_t gi = g0 + i;
+        if (tau_top && ctx->aco()) tau_top[gi] = tau[i].x;
+        if (tau_bot && ctx->aco()) tau_bot[gi] = tau[i].y;
+        const uint32_t id = w & pfdev::kIdMask;
+        if (occ) occ[gi] = uint8_t(w ? (w >> 30) : 0);
+        if (index) index[gi] = w ? id : 0;
+        if (!w) continue;
+        if (id == 0 || id > n_agents) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
+        if (agents) {
+            pf_agent& a = agents[id - 1];
+            std::memset(&a, 0, sizeof a);
+            a.index = id;
+            a.group = uint8_t(w >> 30);
+            a.row = a.future_row = int32_t(gi / W);
+            a.col = a.future_col = int32_t(gi % W);
+            a.tour_length = ctx->aco() ? tour[i] : 0.0;
+            a.crossed = (w & pfdev::kCrossedBit) ? 1 : 0;
+        }
+    }
+    if (step) *step = ctx->step;
+    return PF_OK;
+}
+
+// Enqueue n <= kBatchCap steps starting at batch slot 0 with current parity.
+static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
+    for (uint32_t i = 0; i < n; ++i) {
+        const int par = (parity + int(i)) & 1;
+        ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED ? pfk::launch_step_fused(ctx->args, int(i), par, ctx->stream)
+                                                            : pfk::launch_step_pipeline(ctx->args, int(i), par, ctx->stream);
+    }
+    ctx->launches += pfk::launch_advance_step(ctx->d_step, n, ctx->stream);
+    return PF_OK;
+}
+
+static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
+    PF_CUDA(cudaMemsetAsync(ctx->d_reports, 0, size_t(ctx->cfg.replicas) * kBatchCap * 16, ctx->stream));
+    const auto key = std::make_pair(n, ctx->parity);
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        const uint64_t before = ctx->launches;
+        PF_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_direct(ctx, n, ctx->parity);
+        PF_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        ctx->launches = before;  // counted when replayed
+        PF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        it = ctx->graphs.emplace(key, ge).first;
+    }
+    PF_CUDA(cudaGraphLaunch(it->second, ctx->stream));
+    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_FUSED ? 1 : 3;
+    ctx->launches += uint64_t(n) * per_step + 1;
+    ctx->parity ^= int(n & 1u);
+    ctx->step += n;
+    PF_CUDA(cudaGetLastError());
+    return PF_OK;
+}
+
+int pf_step_async(pf_ctx* ctx, uint32_t n) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    while (n > 0) {
+        const uint32_t m = std::min<uint32_t>(n, kBatchCap);
+        if (int rc = enqueue_batch(ctx, m)) return rc;
+        n -= m;
+    }
+    return PF_OK;
+}
+
+int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (n > kBatchCap) return fail(PF_ERR_ARG, "at most 256 reports are kept on the device");
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int R = ctx->cfg.replicas;
+    std::vector<uint32_t> buf(size_t(R) * kBatchCap * 4);
+    PF_CUDA(cudaMemcpy(buf.data(), ctx->d_reports, buf.size() * 4, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < R; ++r)
+        std::memcpy(out + size_t(r) * n, buf.data() + size_t(r) * kBatchCap * 4, size_t(n) * 16);
+    return PF_OK;
+}
+
+int pf_synchronize(pf_ctx* ctx) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PF_OK;
+}
+
+int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    const int R = ctx->cfg.replicas;
+    std::vector<pf_step_report> chunk;
+    uint32_t done = 0;
+    while (done < n) {
+        const uint32_t m = std::min<uint32_t>(n - done, kBatchCap);
+        if (int rc = enqueue_batch(ctx, m)) return rc;
+        if (out) {
+            chunk.resize(size_t(R) * m);
+            if (int rc = pf_read_reports(ctx, chunk.data(), m)) return rc;
+            for (int r = 0; r < R; ++r)
+                std::memcpy(out + size_t(r) * n + done, chunk.data() + size_t(r) * m, size_t(m) * 16);
+        }
+        done += m;
+    }
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PF_OK;
+}
+
+int pf_time_steps(pf_ctx* ctx, uint32_t n, float* total_ms, float* kernel_ms) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    cudaEvent_t e0, e1;
+    PF_CUDA(cudaEventCreate(&e0));
+    PF_CUDA(cudaEventCreate(&e1));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    PF_CUDA(cudaEventRecord(e0, ctx->stream));
+    if (int rc = pf_step_async(ctx, n)) return rc;
+    PF_CUDA(cudaEventRecord(e1, ctx->stream));
+    PF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (total_ms) *total_ms = ms;
+    if (kernel_ms) {
+        // Per-launch events around each step's kernel(s), no graph.
+        std::vector<cudaEvent_t> ev(2 * size_t(n));
+        for (auto& e : ev) PF_CUDA(cudaEventCreate(&e));
+        uint32_t done = 0;
+        while (done < n) {
+            const uint32_t m = std::min<uint32_t>(n - done, kBatchCap);
+            PF_CUDA(cudaMemsetAsync(ctx->d_reports, 0, size_t(ctx->cfg.replicas) * kBatchCap * 16, ctx->stream));
+            for (uint32_t i = 0; i < m; ++i) {
+                const int par = (ctx->parity + int(i)) & 1;
+                PF_CUDA(cudaEventRecord(ev[2 * (done + i)], ctx->stream));
+                ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED
+                                     ? pfk::launch_step_fused(ctx->args, int(i), par, ctx->stream)
+                                     : pfk::launch_step_pipeline(ctx->args, int(i), par, ctx->stream);
+                PF_CUDA(cudaEventRecord(ev[2 * (done + i) + 1], ctx->stream));
+            }
+            ctx->launches += pfk::launch_advance_step(ctx->d_step, m, ctx->stream);
+            ctx->parity ^= int(m & 1u);
+            ctx->step += m;
+            done += m;
+        }
+        PF_CUDA(cudaStreamSynchronize(ctx->stream));
+        double sum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) {
+            float t = 0.f;
+            PF_CUDA(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
+            sum += t;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        *kernel_ms = n ? float(sum / n) : 0.f;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return PF_OK;
+}
+
+uint32_t pf_current_step(const pf_ctx* ctx) { return ctx ? ctx->step : 0; }
+void* pf_stream(pf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+uint64_t pf_launch_count(const pf_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pf_halo(pf_ctx* ctx, int32_t rep, int32_t side, int32_t recv, pf_halo_rows* out) {
+    if (!ctx || !out) return fail(PF_ERR_ARG, "null argument");
+    if (rep < 0 || rep >= ctx->cfg.replicas || (side != 0 && side != 1) || (recv != 0 && recv != 1))
+        return fail(PF_ERR_ARG, "bad halo selector");
+    const size_t W = size_t(ctx->cfg.width);
+    const int G = pfk::kGhost;
+    int first, tour_row;
+    if (side == 0) {
+        first = recv ? 0 : G;
+        tour_row = recv ? G - 1 : G;
+    } else {
+        first = recv ? G + ctx->rows_owned : ctx->rows_owned;  // owned rows [rows_owned, rows_owned+G) in buffer = last G owned
+        tour_row = recv ? G + ctx->rows_owned : G + ctx->rows_owned - 1;
+    }
+    const size_t off = size_t(rep) * ctx->plane();
+    const pfk::Planes& P = ctx->args.p;
+    out->cells = P.cell[ctx->parity] + off + size_t(first) * W;
+    out->cell_bytes = size_t(G) * W * 4;
+    if (ctx->aco()) {
+        out->tau = P.tau[ctx->parity] + off + size_t(first) * W;
+        out->tau_bytes = size_t(G) * W * 16;
+        out->tour = P.tour + off + size_t(tour_row) * W;
+        out->tour_bytes = W * 8;
+    } else {
+        out->tau = out->tour = nullptr;
+        out->tau_bytes = out->tour_bytes = 0;
+    }
+    return PF_OK;
+}
+
+int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
+    if (!upper || !lower) return fail(PF_ERR_ARG, "null ctx");
+    if (upper->cfg.replicas != lower->cfg.replicas || upper->cfg.width != lower->cfg.width ||
+        upper->row_begin + upper->rows_owned != lower->row_begin)
+        return fail(PF_ERR_COMM, "shards are not vertically adjacent");
+    PF_CUDA(cudaSetDevice(upper->cfg.device));
+    PF_CUDA(cudaStreamSynchronize(upper->stream));
+    PF_CUDA(cudaSetDevice(lower->cfg.device));
+    PF_CUDA(cudaStreamSynchronize(lower->stream));
+    for (int r = 0; r < upper->cfg.replicas; ++r) {
+        pf_halo_rows us, ur, ls, lr;
+        pf_halo(upper, r, 1, 0, &us);
+        pf_halo(upper, r, 1, 1, &ur);
+        pf_halo(lower, r, 0, 0, &ls);
+        pf_halo(lower, r, 0, 1, &lr);
+        PF_CUDA(cudaMemcpyAsync(lr.cells, us.cells, us.cell_bytes, cudaMemcpyDefault, lower->stream));
+        PF_CUDA(cudaMemcpyAsync(ur.cells, ls.cells, ls.cell_bytes, cudaMemcpyDefault, lower->stream));
+        if (us.tau) {
+            PF_CUDA(cudaMemcpyAsync(lr.tau, us.tau, us.tau_bytes, cudaMemcpyDefault, lower->stream));
+            PF_CUDA(cudaMemcpyAsync(ur.tau, ls.tau, ls.tau_bytes, cudaMemcpyDefault, lower->stream));
+            PF_CUDA(cudaMemcpyAsync(lr.tour, us.tour, us.tour_bytes, cudaMemcpyDefault, lower->stream));
+            PF_CUDA(cudaMemcpyAsync(ur.tour, ls.tour, ls.tour_bytes, cudaMemcpyDefault, lower->stream));
+        }
+    }
+    PF_CUDA(cudaStreamSynchronize(lower->stream));
+    return PF_OK;
+}
+
+int pf_selftest_rng(int32_t device, uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                    const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits_out,
+                    double* uniform_out, double* normal_out) {
+    if (!seed || !step || !phase || !entity || !counter) return fail(PF_ERR_ARG, "null key array");
+    if (n == 0) return PF_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PF_ERR_CUDA, "no CUDA device available");
+    PF_CUDA(cudaSetDevice(device));
+    const size_t in_bytes = size_t(n) * (8 + 4 + 4 + 8 + 4), out_bytes = size_t(n) * 24;
+    char* d = nullptr;
+    PF_CUDA(cudaMalloc(&d, in_bytes + out_bytes));
+    uint64_t* d_seed = reinterpret_cast<uint64_t*>(d);
+    uint64_t* d_ent = d_seed + n;
+    uint64_t* d_bits = d_ent + n;
+    double* d_uni = reinterpret_cast<double*>(d_bits + n);
+    double* d_nrm = d_uni + n;
+    uint32_t* d_step = reinterpret_cast<uint32_t*>(d_nrm + n);
+    uint32_t* d_phase = d_step + n;
+    uint32_t* d_ctr = d_phase + n;
+    auto run = [&]() -> int {
+        PF_CUDA(cudaMemcpy(d_seed, seed, n * 8, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_ent, entity, n * 8, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_step, step, n * 4, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_phase, phase, n * 4, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_ctr, counter, n * 4, cudaMemcpyHostToDevice));
+        pfk::launch_selftest_rng(n, d_seed, d_step, d_phase, d_ent, d_ctr, mu, sigma, d_bits, d_uni, d_nrm, 0);
+        PF_CUDA(cudaGetLastError());
+        PF_CUDA(cudaDeviceSynchronize());
+        if (bits_out) PF_CUDA(cudaMemcpy(bits_out, d_bits, n * 8, cudaMemcpyDeviceToHost));
+        if (uniform_out) PF_CUDA(cudaMemcpy(uniform_out, d_uni, n * 8, cudaMemcpyDeviceToHost));
+        if (normal_out) PF_CUDA(cudaMemcpy(normal_out, d_nrm, n * 8, cudaMemcpyDeviceToHost));
+        return PF_OK;
+    };
+    const int rc = run();
+    cudaFree(d);
+    return rc;
+}
+
+}  // extern "C"

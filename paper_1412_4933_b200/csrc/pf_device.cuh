@@ -1,0 +1,268 @@
+// Device-side building blocks of the per-step update: the keyed Philox
+// stream, the AS241 quantile, and the per-agent move proposal (LEM / ACO).
+//
+// Every floating-point operation uses an explicit round-to-nearest intrinsic
+// (__dmul_rn, __dadd_rn, ...) in the reference's evaluation order, so no FMA
+// contraction can change a bit; the library is additionally built with
+// --fmad=false. The only non-IEEE-exact call is log() in the AS241 tail
+// (CUDA: <= 1 ulp); see DESIGN.md "Bit-exactness".
+#pragma once
+
+#include <cstdint>
+
+namespace pfdev {
+
+// Cell word: agent id in bits 0..28, crossed flag bit 29, group in bits 30..31
+// (1 = Top, 2 = Bottom). 0 = empty; kWall (group 3) = outside the arena.
+constexpr uint32_t kIdMask = 0x1FFFFFFFu;
+constexpr uint32_t kCrossedBit = 1u << 29;
+constexpr uint32_t kWall = 0xFFFFFFFFu;
+constexpr uint8_t kNone = 0xFF;
+
+enum : uint32_t { kPhasePlacement = 0, kPhaseLemSelect = 1, kPhaseAcoSelect = 2, kPhaseResolve = 3, kPhaseTieBreak = 4 };
+
+// Row-major neighbour codes around a cell (the reference's contender scan
+// order, src/engine.cpp:15-24): code j <-> offset (kDR[j], kDC[j]); the
+// opposite direction of code j is 7 - j.
+static __device__ __constant__ const int8_t kDR[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+static __device__ __constant__ const int8_t kDC[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+
+// Goal-relative slot i (F FL FR L R B BL BR, inc/grid.hpp:19-43) -> row-major
+// code, for a Top agent. A Bottom agent's slot is the point reflection
+// (inc/grid.hpp:45-49), whose code is 7 - the Top code.
+static __device__ __constant__ const uint8_t kSlotCodeTop[8] = {6, 5, 7, 3, 4, 1, 0, 2};
+
+struct StepConsts {
+    double lem_score[8]; // d_min / d_i (src/lem.cpp:8-18), host-computed
+    double eta[8];       // (1/d_i)^beta (src/aco.cpp:20-27), host-computed
+    double sel_mu, sel_sigma;
+    double alpha;
+    int alpha_mode;      // 0: tau, 1: 1.0, 2: pow(tau, alpha) (src/aco.cpp:31-35)
+    double factor;       // 1 - rho (src/engine.cpp:126)
+    double q;
+    double diag;         // sqrt(2) (src/aco.cpp:11)
+    int model;           // 0 LEM, 1 ACO
+    int W, H, band;
+};
+
+// ----------------------------------------------------------------- Philox
+
+// Philox4x32-10 with the reference's packing (src/rng.cpp:43-55).
+__device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity,
+                                                uint32_t counter) {
+    uint32_t c0 = uint32_t(entity), c1 = uint32_t(entity >> 32), c2 = step;
+    uint32_t c3 = (phase << 28) | (counter & 0x0FFFFFFFu);
+    uint32_t k0 = uint32_t(seed), k1 = uint32_t(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c1 = lo1;
+        c3 = lo0;
+        c0 = n0;
+        c2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return (uint64_t(c0) << 32) | c1;
+}
+
+// uniform(): (bits >> 11) * 2^-53 (src/rng.cpp:57-59). Exact.
+__device__ __forceinline__ double uniform_from_bits(uint64_t bits) {
+    return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
+}
+
+__device__ __forceinline__ double horner8(const double (&c)[8], double r) {
+    double v = c[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) v = __dadd_rn(__dmul_rn(v, r), c[i]);
+    return v;
+}
+
+// Wichura AS241 PPND16 (src/rng.cpp:61-150), same coefficients and order.
+static __device__ __noinline__ double inverse_normal_cdf(double p) {
+    const double q = __dsub_rn(p, 0.5);
+    if (fabs(q) <= 0.425) {
+        constexpr double num[8] = {2.5090809287301226727e3, 3.3430575583588128105e4, 6.7265770927008700853e4,
+                                   4.5921953931549871457e4, 1.3731693765509461125e4, 1.9715909503065514427e3,
+                                   1.3314166789178437745e2, 3.3871328727963666080e0};
+        constexpr double den[8] = {5.2264952788528545610e3, 2.8729085735721942674e4, 3.9307895800092710610e4,
+                                   2.1213794301586595867e4, 5.3941960214247511077e3, 6.8718700749205790830e2,
+                                   4.2313330701600911252e1, 1.0};
+        const double r = __dsub_rn(0.180625, __dmul_rn(q, q));
+        return __ddiv_rn(__dmul_rn(q, horner8(num, r)), horner8(den, r));
+    }
+    double r = (q < 0.0) ? p : __dsub_rn(1.0, p);
+    r = __dsqrt_rn(-log(r));
+    double val;
+    if (r <= 5.0) {
+        constexpr double num[8] = {7.74545014278341407640e-4, 2.27238449892691845833e-2, 2.41780725177450611770e-1,
+                                   1.27045825245236838258e0,  3.64784832476320460504e0,  5.76949722146069140550e0,
+                                   4.63033784615654529590e0,  1.42343711074968357734e0};
+        constexpr double den[8] = {1.05075007164441684324e-9, 5.47593808499534494600e-4, 1.51986665636164571966e-2,
+                                   1.48103976427480074590e-1, 6.89767334985100004550e-1, 1.67638483018380384940e0,
+                                   2.05319162663775882187e0,  1.0};
+        r = __dsub_rn(r, 1.6);
+        val = __ddiv_rn(horner8(num, r), horner8(den, r));
+    } else {
+        constexpr double num[8] = {2.01033439929228813265e-7, 2.71155556874348757815e-5, 1.24266094738807843860e-3,
+                                   2.65321895265761230930e-2, 2.96560571828504891230e-1, 1.78482653991729133580e0,
+                                   5.46378491116411436990e0,  6.65790464350110377720e0};
+        constexpr double den[8] = {2.04426310338993978564e-15, 1.42151175831644588870e-7, 1.84631831751005468180e-5,
+                                   7.86869131145613259100e-4,  1.48753612908506148525e-2, 1.36929880922735805310e-1,
+                                   5.99832206555887937690e-1,  1.0};
+        r = __dsub_rn(r, 5.0);
+        val = __ddiv_rn(horner8(num, r), horner8(den, r));
+    }
+    return (q < 0.0) ? -val : val;
+}
+
+// ----------------------------------------------------------- proposals
+
+// Slow path of lem_select (src/lem.cpp:28-60): the forward slot is blocked
+// and at least one slot is open. Returns the chosen goal-relative slot.
+static __device__ __noinline__ int lem_choose(const StepConsts* __restrict__ k, uint32_t open, uint64_t seed,
+                                       uint32_t step, uint32_t id) {
+    double cmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double s = (open >> i & 1u) ? __ldg(&k->lem_score[i]) : 0.0;
+        cmax = (cmax < s) ? s : cmax; // std::max
+    }
+    // normal(key, mu_sel*C_max, sigma_sel*C_max) (src/lem.cpp:34, src/rng.cpp:152-156)
+    const uint64_t bits = philox_bits(seed, step, kPhaseLemSelect, id, 0);
+    const double u = __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
+    const double mu = __dmul_rn(__ldg(&k->sel_mu), cmax), sg = __dmul_rn(__ldg(&k->sel_sigma), cmax);
+    double r = __dadd_rn(mu, __dmul_rn(sg, inverse_normal_cdf(u)));
+    r = (r < 0.0) ? 0.0 : ((cmax < r) ? cmax : r); // std::clamp(r, 0, C_max)
+    double best = -1.0;
+    int ntied = 0;
+    uint32_t tied = 0; // slots in canonical order, 3 bits each
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (!(open >> i & 1u)) continue;
+        const double gap = fabs(__dsub_rn(__ldg(&k->lem_score[i]), r));
+        if (ntied == 0 || gap < best) {
+            best = gap;
+            ntied = 1;
+            tied = uint32_t(i);
+        } else if (gap == best) {
+            tied |= uint32_t(i) << (3 * ntied);
+            ++ntied;
+        }
+    }
+    if (ntied > 1) {
+        const double tu = uniform_from_bits(philox_bits(seed, step, kPhaseTieBreak, id, 0));
+        int j = __double2int_rz(__dmul_rn(tu, double(ntied)));
+        j = j < ntied - 1 ? j : ntied - 1;
+        return int(tied >> (3 * j) & 7u);
+    }
+    return int(tied & 7u);
+}
+
+// Slow path of aco_select (src/aco.cpp:64-92) given the numerators of the
+// open slots (aco_numerators, src/aco.cpp:39-51).
+static __device__ __noinline__ int aco_choose(const double (&num)[8], uint32_t open, uint64_t seed, uint32_t step,
+                                       uint32_t id) {
+    double total = 0.0;
+    int k = 0, last = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (!(open >> i & 1u)) continue;
+        total = __dadd_rn(total, num[i]);
+        ++k;
+        last = i;
+    }
+    const double u = uniform_from_bits(philox_bits(seed, step, kPhaseAcoSelect, id, 0));
+    if (total <= 0.0) {
+        int j = __double2int_rz(__dmul_rn(u, double(k)));
+        j = j < k - 1 ? j : k - 1;
+        for (int i = 0; i < 8; ++i) {
+            if (!(open >> i & 1u)) continue;
+            if (j-- == 0) return i;
+        }
+        return last;
+    }
+    const double target = __dmul_rn(u, total);
+    double cum = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (!(open >> i & 1u)) continue;
+        cum = __dadd_rn(cum, num[i]);
+        if (cum > target) return i;
+    }
+    return last;
+}
+
+__device__ __forceinline__ double pheromone_term(const StepConsts* __restrict__ k, double tau) {
+    const int mode = __ldg(&k->alpha_mode);
+    if (mode == 0) return tau;
+    if (mode == 1) return 1.0;
+    return pow(tau, __ldg(&k->alpha)); // alpha not in {0,1}: tolerance-only parity
+}
+
+// Proposal of the agent with cell word `word` (score_phase + intention_phase,
+// src/engine.cpp:64-90). cell_at(dr, dc) returns the step-start word of the
+// neighbour (kWall outside the arena); tau_at(dr, dc, group) returns that
+// neighbour's own-group pheromone. Returns the row-major code of the target
+// cell, or kNone to stay.
+template <class CellAt, class TauAt>
+__device__ __forceinline__ uint8_t propose(const StepConsts* __restrict__ k, int model, uint32_t word, uint64_t seed, uint32_t step,
+                                           CellAt cell_at, TauAt tau_at) {
+    const uint32_t group = word >> 30;
+    const bool bottom = group == 2u;
+    // Forward priority: no draw (src/lem.cpp:23-26, src/aco.cpp:60-63).
+    {
+        const uint8_t cf = bottom ? uint8_t(7 - kSlotCodeTop[0]) : kSlotCodeTop[0];
+        if (cell_at(kDR[cf], kDC[cf]) == 0u) return cf;
+    }
+    uint32_t open = 0;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        const uint8_t c = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
+        open |= uint32_t(cell_at(kDR[c], kDC[c]) == 0u) << i;
+    }
+    if (open == 0u) return kNone; // boxed in: stay
+    const uint32_t id = word & kIdMask;
+    int slot;
+    if (model == 0) {
+        slot = lem_choose(k, open, seed, step, id);
+    } else {
+        double num[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            num[i] = 0.0;
+            if (open >> i & 1u) {
+                const uint8_t c = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
+                num[i] = __dmul_rn(pheromone_term(k, tau_at(kDR[c], kDC[c], bottom)), __ldg(&k->eta[i]));
+            }
+        }
+        slot = aco_choose(num, open, seed, step, id);
+    }
+    return bottom ? uint8_t(7 - kSlotCodeTop[slot]) : kSlotCodeTop[slot];
+}
+
+// Cell-centric conflict resolution for one destination whose claim mask has
+// bit j set when the neighbour at row-major code j targets it (the gather of
+// src/engine.cpp:101-122). Returns the code of the winning source.
+__device__ __forceinline__ uint8_t resolve(uint32_t claims, uint64_t seed, uint32_t step, uint64_t gidx) {
+    const int kc = __popc(claims);
+    if (kc == 1) return uint8_t(__ffs(claims) - 1);
+    const double u = uniform_from_bits(philox_bits(seed, step, kPhaseResolve, gidx, 0));
+    int j = __double2int_rz(__dmul_rn(u, double(kc)));
+    j = j < kc - 1 ? j : kc - 1;
+    uint32_t m = claims;
+    for (int t = 0; t < j; ++t) m &= m - 1u; // drop the j lowest contenders
+    return uint8_t(__ffs(m) - 1);
+}
+
+// crossed() (src/metrics.cpp:13-16) for a mover landing on global row grow.
+__device__ __forceinline__ bool crossed_at(uint32_t group, int grow, int H, int band) {
+    return group == 1u ? grow >= H - band : grow <= band - 1;
+}
+
+__device__ __forceinline__ bool is_diag(int code) { return code == 0 || code == 2 || code == 5 || code == 7; }
+
+} // namespace pfdev

@@ -1,0 +1,55 @@
+// Internal interface between the C-ABI/context code (pf_context.cu) and the
+// kernels (pf_kernels.cu). Not part of the public boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "pf_device.cuh"
+
+namespace pfk {
+
+constexpr int kGhost = 3;  // == PF_GHOST_ROWS
+
+// Device planes of one context. Every plane is replica-major:
+// plane[replica][buffer row][column]; buffer row b <-> global row
+// row_begin - kGhost + b.
+struct Planes {
+    uint32_t* cell[2];  // ping-pong cell words
+    double2* tau[2];    // ping-pong {top, bottom} pheromone (ACO)
+    double* tour;       // cell-resident tour length, updated in place (ACO)
+    uint8_t* intent;    // pipeline-kernel scratch
+    uint8_t* win;       // pipeline-kernel scratch
+    size_t plane;       // elements per replica plane = rows_buf * W
+};
+
+struct StepArgs {
+    pfdev::StepConsts k;              // by value: hot scalars read from param space
+    const pfdev::StepConsts* kc;      // device copy: tables read by the slow paths
+    Planes p;
+    uint64_t seed_base;     // replica r uses seed_base + r
+    const uint32_t* d_step; // device step counter: step of batch slot 0
+    uint32_t* reports;      // [replicas][batch_cap][4]
+    int batch_cap;
+    int row_begin;          // global row of the first owned row
+    int rows_owned;
+    int rows_buf;           // rows_owned + 2 * kGhost
+    int replicas;
+};
+
+// Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
+// Returns the number of kernel launches issued.
+int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s);
+int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
+// *d_step += n
+int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
+// Fill a tau plane range with {v, v}.
+int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
+int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);
+int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                        const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
+                        double* uni, double* nrm, cudaStream_t s);
+
+}  // namespace pfk

@@ -1,0 +1,374 @@
+// sm_100a kernels of the per-step grid update.
+//
+//   step_fused_kernel   ONE kernel per step (the product path). A CTA owns a
+//                       TH x TW tile; it stages the step-start cell words of
+//                       the tile plus a 3-cell halo in shared memory, proposes
+//                       moves for every agent within 2 cells of the tile,
+//                       scatters claims into per-destination bitmasks
+//                       (shared-memory atomicOr), resolves every destination
+//                       within 1 cell (keyed draw per contested cell), then
+//                       commits the owned cells: cell word, tour, pheromone
+//                       evaporation + deposit, crossing and counters. HBM
+//                       traffic is one read + one write of each plane.
+//   step_pipeline_*     the same semantics as three kernels (propose /
+//                       resolve / commit) through global u8 scratch planes;
+//                       kept as an independent on-device cross-check.
+//
+// Reference semantics: StepEngine::step, src/engine.cpp:53-193.
+#include "pf_internal.h"
+
+namespace pfk {
+
+using namespace pfdev;
+
+namespace {
+
+__device__ __forceinline__ void block_count(uint32_t moved, uint32_t ntop, uint32_t nbot, uint32_t* s_cnt,
+                                            uint32_t* rep_slot, uint32_t step, bool first_block) {
+    moved = __reduce_add_sync(0xFFFFFFFFu, moved);
+    ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);
+    nbot = __reduce_add_sync(0xFFFFFFFFu, nbot);
+    if ((threadIdx.x & 31) == 0 && (moved | ntop | nbot)) {
+        if (moved) atomicAdd(&s_cnt[0], moved);
+        if (ntop) atomicAdd(&s_cnt[1], ntop);
+        if (nbot) atomicAdd(&s_cnt[2], nbot);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (first_block) rep_slot[0] = step;
+        if (s_cnt[0]) atomicAdd(&rep_slot[1], s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&rep_slot[2], s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&rep_slot[3], s_cnt[2]);
+    }
+}
+
+// Commit of one owned cell (the movement-phase commit, src/engine.cpp:137-175,
+// plus evaporation src/engine.cpp:124-131 and deposit src/aco.cpp:119-123).
+// `w` is the step-start word, `win` the winning source code if the cell was
+// empty (kNone otherwise), `vacate` whether the occupant's move was granted,
+// `src_word` the winner's word.
+template <bool ACO>
+__device__ __forceinline__ void commit_cell(const StepConsts& k, uint32_t w, uint8_t win, bool vacate,
+                                            uint32_t src_word, int grow, size_t gi, size_t si,
+                                            uint32_t* __restrict__ cout, const double2* __restrict__ tin,
+                                            double2* __restrict__ tout, double* __restrict__ tour,
+                                            uint32_t& moved, uint32_t& ntop, uint32_t& nbot) {
+    uint32_t nw = w;
+    bool arrived = false;
+    uint32_t group = 0;
+    double tour_new = 0.0;
+    if (w == 0u) {
+        if (win != kNone) {
+            group = src_word >> 30;
+            nw = src_word;
+            if (!(src_word & kCrossedBit) && crossed_at(group, grow, k.H, k.band)) {
+                nw |= kCrossedBit;
+                if (group == 1u) ++ntop; else ++nbot;
+            }
+            ++moved;
+            arrived = true;
+            if (ACO) {
+                tour_new = __dadd_rn(tour[si], is_diag(win) ? k.diag : 1.0);
+                tour[gi] = tour_new;
+            }
+        }
+    } else if (vacate) {
+        nw = 0u;
+    }
+    cout[gi] = nw;
+    if (ACO) {
+        double2 t = tin[gi];
+        t.x = __dmul_rn(t.x, k.factor);
+        t.y = __dmul_rn(t.y, k.factor);
+        if (arrived) {
+            const double dep = __ddiv_rn(k.q, tour_new);
+            if (group == 1u) t.x = __dadd_rn(t.x, dep);
+            else t.y = __dadd_rn(t.y, dep);
+        }
+        tout[gi] = t;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ fused kernel
+
+template <int TH, int TW, bool ACO>
+__global__ void __launch_bounds__(256) step_fused_kernel(const StepArgs a, int slot, int parity) {
+    constexpr int SH = TH + 6, SW = TW + 6; // staged words: tile + 3-cell halo
+    constexpr int RH = TH + 4, RW = TW + 4; // proposal region: tile + 2
+    constexpr int CH = TH + 2, CW = TW + 2; // claim/winner region: tile + 1
+    __shared__ uint32_t s_cell[SH * SW];
+    __shared__ uint32_t s_claim[CH * CW];
+    __shared__ uint8_t s_win[CH * CW];
+    __shared__ uint8_t s_int[TH * TW];
+    __shared__ uint32_t s_cnt[3];
+
+    const StepConsts& k = a.k;
+    const int W = k.W;
+    const int rep = blockIdx.z;
+    const int r0 = blockIdx.y * TH; // owned-local row of the tile origin
+    const int c0 = blockIdx.x * TW;
+    const uint32_t step = *a.d_step + uint32_t(slot);
+    const uint64_t seed = a.seed_base + uint64_t(rep);
+    const size_t base = size_t(rep) * a.p.plane;
+    const uint32_t* __restrict__ cin = a.p.cell[parity] + base;
+    uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + base;
+    const double2* __restrict__ tin = ACO ? a.p.tau[parity] + base : nullptr;
+    double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + base : nullptr;
+    double* __restrict__ tour = ACO ? a.p.tour + base : nullptr;
+
+    // Stage the step-start snapshot (walls outside the arena / buffer).
+    for (int i = threadIdx.x; i < SH * SW; i += blockDim.x) {
+        const int sr = i / SW, sc = i - sr * SW;
+        const int b = kGhost + r0 - 3 + sr;
+        const int c = c0 - 3 + sc;
+        uint32_t w = kWall;
+        if (c >= 0 && c < W && b < a.rows_buf) w = __ldg(cin + size_t(b) * W + c);
+        s_cell[i] = w;
+    }
+    for (int i = threadIdx.x; i < CH * CW; i += blockDim.x) s_claim[i] = 0u;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+
+    // Proposals (score + intention phases) for agents within 2 of the tile;
+    // each granted proposal sets bit (7 - code) in its destination's claim mask.
+    for (int i = threadIdx.x; i < RH * RW; i += blockDim.x) {
+        const int ar = i / RW, ac = i - ar * RW;
+        const int sr = ar + 1, sc = ac + 1;
+        const uint32_t w = s_cell[sr * SW + sc];
+        uint8_t code = kNone;
+        if (w != 0u && w != kWall) {
+            const int b = kGhost + r0 + ar - 2;
+            const int gc = c0 + ac - 2;
+            code = propose(
+                a.kc, ACO ? 1 : 0, w, seed, step, [&](int dr, int dc) { return s_cell[(sr + dr) * SW + sc + dc]; },
+                [&](int dr, int dc, bool bottom) {
+                    const double* t = reinterpret_cast<const double*>(tin + size_t(b + dr) * W + (gc + dc));
+                    return __ldg(t + (bottom ? 1 : 0));
+                });
+            if (code != kNone) {
+                const int tr = ar - 1 + kDR[code], tc = ac - 1 + kDC[code];
+                if (tr >= 0 && tr < CH && tc >= 0 && tc < CW) atomicOr(&s_claim[tr * CW + tc], 1u << (7 - code));
+            }
+        }
+        if (ar >= 2 && ar < TH + 2 && ac >= 2 && ac < TW + 2) s_int[(ar - 2) * TW + (ac - 2)] = code;
+    }
+    __syncthreads();
+
+    // Cell-centric resolution for destinations within 1 of the tile.
+    for (int i = threadIdx.x; i < CH * CW; i += blockDim.x) {
+        const uint32_t m = s_claim[i];
+        uint8_t wv = kNone;
+        if (m) {
+            const int cr = i / CW, cc = i - cr * CW;
+            const int64_t grow = int64_t(a.row_begin) + r0 + cr - 1;
+            wv = resolve(m, seed, step, uint64_t(grow) * uint64_t(W) + uint64_t(c0 + cc - 1));
+        }
+        s_win[i] = wv;
+    }
+    __syncthreads();
+
+    // Commit owned cells.
+    uint32_t moved = 0, ntop = 0, nbot = 0;
+    for (int i = threadIdx.x; i < TH * TW; i += blockDim.x) {
+        const int tr = i / TW, tc = i - tr * TW;
+        const int lr = r0 + tr, gc = c0 + tc;
+        if (lr >= a.rows_owned || gc >= W) continue;
+        const int sr = tr + 3, sc = tc + 3;
+        const uint32_t w = s_cell[sr * SW + sc];
+        const size_t gi = size_t(kGhost + lr) * W + gc;
+        uint8_t win = kNone;
+        bool vacate = false;
+        uint32_t src_word = 0;
+        size_t si = 0;
+        if (w == 0u) {
+            win = s_win[(tr + 1) * CW + tc + 1];
+            if (win != kNone) {
+                src_word = s_cell[(sr + kDR[win]) * SW + sc + kDC[win]];
+                si = size_t(kGhost + lr + kDR[win]) * W + (gc + kDC[win]);
+            }
+        } else {
+            const uint8_t ic = s_int[tr * TW + tc];
+            vacate = ic != kNone && s_win[(tr + 1 + kDR[ic]) * CW + tc + 1 + kDC[ic]] == uint8_t(7 - ic);
+        }
+        commit_cell<ACO>(k, w, win, vacate, src_word, a.row_begin + lr, gi, si, cout, tin, tout, tour, moved,
+                         ntop, nbot);
+    }
+    uint32_t* rep_slot = a.reports + (size_t(rep) * a.batch_cap + slot) * 4;
+    block_count(moved, ntop, nbot, s_cnt, rep_slot, step, blockIdx.x == 0 && blockIdx.y == 0);
+}
+
+constexpr int kTH = 32, kTW = 32;
+
+int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s) {
+    dim3 grid((a.k.W + kTW - 1) / kTW, (a.rows_owned + kTH - 1) / kTH, a.replicas);
+    if (a.k.model == 1) step_fused_kernel<kTH, kTW, true><<<grid, 256, 0, s>>>(a, slot, parity);
+    else step_fused_kernel<kTH, kTW, false><<<grid, 256, 0, s>>>(a, slot, parity);
+    return 1;
+}
+
+// --------------------------------------------------------- pipeline kernels
+
+// K1: proposals for every agent in buffer rows [kGhost-2, kGhost+rows_owned+2).
+__global__ void __launch_bounds__(256) pipeline_propose_kernel(const StepArgs a, int slot, int parity) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = kGhost - 2 + int(blockIdx.y);
+    const int rep = blockIdx.z;
+    const int W = a.k.W;
+    if (c >= W) return;
+    const size_t base = size_t(rep) * a.p.plane;
+    const uint32_t* cin = a.p.cell[parity] + base;
+    const double2* tin = a.k.model == 1 ? a.p.tau[parity] + base : nullptr;
+    const uint32_t w = cin[size_t(b) * W + c];
+    uint8_t code = kNone;
+    if (w != 0u && w != kWall) {
+        const uint32_t step = *a.d_step + uint32_t(slot);
+        code = propose(
+            a.kc, a.k.model, w, a.seed_base + uint64_t(rep), step,
+            [&](int dr, int dc) {
+                const int cc = c + dc;
+                if (cc < 0 || cc >= W) return kWall;
+                return cin[size_t(b + dr) * W + cc];
+            },
+            [&](int dr, int dc, bool bottom) {
+                const double* t = reinterpret_cast<const double*>(tin + size_t(b + dr) * W + (c + dc));
+                return t[bottom ? 1 : 0];
+            });
+    }
+    a.p.intent[base + size_t(b) * W + c] = code;
+}
+
+// K2: winners for every empty cell in buffer rows [kGhost-1, kGhost+rows_owned+1).
+__global__ void __launch_bounds__(256) pipeline_resolve_kernel(const StepArgs a, int slot, int parity) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = kGhost - 1 + int(blockIdx.y);
+    const int rep = blockIdx.z;
+    const int W = a.k.W;
+    if (c >= W) return;
+    const size_t base = size_t(rep) * a.p.plane;
+    const uint32_t* cin = a.p.cell[parity] + base;
+    const uint8_t* intent = a.p.intent + base;
+    uint8_t wv = kNone;
+    if (cin[size_t(b) * W + c] == 0u) {
+        uint32_t claims = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int cc = c + kDC[j];
+            if (cc < 0 || cc >= W) continue;
+            claims |= uint32_t(intent[size_t(b + kDR[j]) * W + cc] == uint8_t(7 - j)) << j;
+        }
+        if (claims) {
+            const uint32_t step = *a.d_step + uint32_t(slot);
+            const int64_t grow = int64_t(a.row_begin) + (b - kGhost);
+            wv = resolve(claims, a.seed_base + uint64_t(rep), step, uint64_t(grow) * uint64_t(W) + uint64_t(c));
+        }
+    }
+    a.p.win[base + size_t(b) * W + c] = wv;
+}
+
+// K3: commit owned rows.
+template <bool ACO>
+__global__ void __launch_bounds__(256) pipeline_commit_kernel(const StepArgs a, int slot, int parity) {
+    __shared__ uint32_t s_cnt[3];
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lr = int(blockIdx.y);
+    const int rep = blockIdx.z;
+    const int W = a.k.W;
+    const size_t base = size_t(rep) * a.p.plane;
+    const uint32_t step = *a.d_step + uint32_t(slot);
+    uint32_t moved = 0, ntop = 0, nbot = 0;
+    if (c < W) {
+        const uint32_t* cin = a.p.cell[parity] + base;
+        const uint8_t* intent = a.p.intent + base;
+        const uint8_t* winp = a.p.win + base;
+        const int b = kGhost + lr;
+        const size_t gi = size_t(b) * W + c;
+        const uint32_t w = cin[gi];
+        uint8_t win = kNone;
+        bool vacate = false;
+        uint32_t src_word = 0;
+        size_t si = 0;
+        if (w == 0u) {
+            win = winp[gi];
+            if (win != kNone) {
+                si = size_t(b + kDR[win]) * W + (c + kDC[win]);
+                src_word = cin[si];
+            }
+        } else {
+            const uint8_t ic = intent[gi];
+            vacate = ic != kNone && winp[size_t(b + kDR[ic]) * W + (c + kDC[ic])] == uint8_t(7 - ic);
+        }
+        commit_cell<ACO>(a.k, w, win, vacate, src_word, a.row_begin + lr, gi, si, a.p.cell[parity ^ 1] + base,
+                         ACO ? a.p.tau[parity] + base : nullptr, ACO ? a.p.tau[parity ^ 1] + base : nullptr,
+                         ACO ? a.p.tour + base : nullptr, moved, ntop, nbot);
+    }
+    uint32_t* rep_slot = a.reports + (size_t(rep) * a.batch_cap + slot) * 4;
+    block_count(moved, ntop, nbot, s_cnt, rep_slot, step, blockIdx.x == 0 && blockIdx.y == 0);
+}
+
+int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s) {
+    const int bx = (a.k.W + 255) / 256;
+    pipeline_propose_kernel<<<dim3(bx, a.rows_owned + 4, a.replicas), 256, 0, s>>>(a, slot, parity);
+    pipeline_resolve_kernel<<<dim3(bx, a.rows_owned + 2, a.replicas), 256, 0, s>>>(a, slot, parity);
+    if (a.k.model == 1) pipeline_commit_kernel<true><<<dim3(bx, a.rows_owned, a.replicas), 256, 0, s>>>(a, slot, parity);
+    else pipeline_commit_kernel<false><<<dim3(bx, a.rows_owned, a.replicas), 256, 0, s>>>(a, slot, parity);
+    return 3;
+}
+
+// ----------------------------------------------------------------- helpers
+
+__global__ void advance_step_kernel(uint32_t* d_step, uint32_t n) { *d_step += n; }
+
+int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s) {
+    advance_step_kernel<<<1, 1, 0, s>>>(d_step, n);
+    return 1;
+}
+
+__global__ void fill_tau_kernel(double2* p, size_t n, double v) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = make_double2(v, v);
+}
+
+int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s) {
+    fill_tau_kernel<<<148 * 8, 256, 0, s>>>(p, n, v);
+    return 1;
+}
+
+__global__ void fill_u8_kernel(uint8_t* p, size_t n, uint8_t v) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s) {
+    fill_u8_kernel<<<148 * 8, 256, 0, s>>>(p, n, v);
+    return 1;
+}
+
+}  // namespace pfk
+
+namespace pfk {
+
+__global__ void selftest_rng_kernel(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                                    const uint64_t* entity, const uint32_t* counter, double mu, double sigma,
+                                    uint64_t* bits, double* uni, double* nrm) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t b = pfdev::philox_bits(seed[i], step[i], phase[i], entity[i], counter[i]);
+    bits[i] = b;
+    uni[i] = pfdev::uniform_from_bits(b);
+    const double u = __dmul_rn(__dadd_rn(__ull2double_rn(b >> 11), 0.5), 0x1.0p-53);
+    nrm[i] = __dadd_rn(mu, __dmul_rn(sigma, pfdev::inverse_normal_cdf(u)));
+}
+
+int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                        const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
+                        double* uni, double* nrm, cudaStream_t s) {
+    selftest_rng_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, seed, step, phase, entity, counter, mu, sigma, bits, uni,
+                                                         nrm);
+    return 1;
+}
+
+}  // namespace pfk

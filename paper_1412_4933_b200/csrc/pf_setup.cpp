@@ -1,0 +1,86 @@
+// Host-side scenario setup: new_environment (src/state.cpp:17-75).
+//
+// The keyed Fisher-Yates is a sequential swap chain (each swap depends on the
+// previous ones), so it stays on the host. Its draws are pure functions of
+// (seed, side, i), so they are generated in parallel first; only the swaps
+// run in order, over 32-bit cell indices.
+#include "pf_setup.h"
+
+#include <algorithm>
+#include <cmath>
+#include <thread>
+#include <vector>
+
+namespace pfhost {
+
+uint64_t philox_bits(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter) {
+    uint32_t c0 = uint32_t(entity), c1 = uint32_t(entity >> 32), c2 = step;
+    uint32_t c3 = (phase << 28) | (counter & 0x0FFFFFFFu);
+    uint32_t k0 = uint32_t(seed), k1 = uint32_t(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = uint64_t(0xD2511F53u) * c0;
+        const uint64_t p1 = uint64_t(0xCD9E8D57u) * c2;
+        const uint32_t n0 = uint32_t(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = uint32_t(p0 >> 32) ^ c3 ^ k1;
+        c1 = uint32_t(p1);
+        c3 = uint32_t(p0);
+        c0 = n0;
+        c2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return (uint64_t(c0) << 32) | c1;
+}
+
+double uniform(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter) {
+    return double(philox_bits(seed, step, phase, entity, counter) >> 11) * 0x1.0p-53;
+}
+
+int32_t band_height(int32_t agents_per_side, int32_t width) {
+    if (width <= 0) return 0;
+    return int32_t((int64_t(agents_per_side) + width - 1) / width);
+}
+
+static void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(hw, std::max<size_t>(1, n / (1u << 16)));
+    if (nt <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+    for (auto& t : ts) t.join();
+}
+
+void place_side(int32_t width, uint32_t group, int32_t row_begin, int32_t row_end, int32_t n, uint32_t first_id,
+                uint64_t seed, const std::function<void(uint32_t cell, uint32_t id)>& put) {
+    const uint64_t m = uint64_t(row_end - row_begin) * uint64_t(width);
+    if (m == 0 || n == 0) return;
+    // Draws: j_i = i + min(floor(u_i * (m - i)), m - i - 1) with
+    // u_i = uniform({seed, 0, Placement, side = group, i}) (src/state.cpp:24-30).
+    std::vector<uint32_t> jump(m - 1);
+    parallel_for(m - 1, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            const double u = uniform(seed, 0, 0 /*Placement*/, group, uint32_t(i));
+            const uint64_t left = m - i;
+            const uint64_t off = std::min<uint64_t>(uint64_t(u * double(left)), left - 1);
+            jump[i] = uint32_t(off);
+        }
+    });
+    std::vector<uint32_t> cells(m);
+    const uint32_t first = uint32_t(uint64_t(row_begin) * uint64_t(width));
+    for (uint64_t i = 0; i < m; ++i) cells[i] = first + uint32_t(i);
+    for (uint64_t i = 0; i + 1 < m; ++i) std::swap(cells[i], cells[i + jump[i]]);
+    for (int32_t k = 0; k < n; ++k) put(cells[size_t(k)], first_id + uint32_t(k));
+}
+
+void place_all(int32_t width, int32_t height, int32_t n, uint64_t seed,
+               const std::function<void(uint32_t cell, uint32_t id, uint32_t group)>& put) {
+    const int32_t band = band_height(n, width);
+    place_side(width, 1, 0, band, n, 1, seed, [&](uint32_t c, uint32_t id) { put(c, id, 1); });
+    place_side(width, 2, height - band, height, n, uint32_t(n) + 1, seed,
+               [&](uint32_t c, uint32_t id) { put(c, id, 2); });
+}
+
+}  // namespace pfhost
