@@ -1,0 +1,419 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-step grid update (BASELINE.json metric: agent-updates/s
+and cell-updates/s per step, achieved HBM GB/s vs peak, 1/2/4/8 GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5_aco]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (row-sharded)
+    python bench.py --impl reference ...                    (the reference CPU path)
+
+Default workload: C5 of BASELINE.json — ACO, 16384 x 16384 grid, 25,000,000
+agents per side (50M) — the largest configuration, the one the 1/2/4/8-GPU
+scaling is quoted on; at N GPUs it is row-sharded (strong scaling) with a
+3-row NCCL halo exchange per step. A step is one full StepEngine::step of the
+whole grid. The other BASELINE configs are parity cases; the 100K-agent config
+(C4) is reported under "secondary" as a replica-batched run (64 seeds per
+launch), its single-scenario step time beside it.
+
+Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
+device synchronize, timed with CUDA events on the library's stream, max over
+ranks. Resident state (~13 GB at C5) is far larger than the 126 MB L2, so no
+flush is needed between steps. ``value`` counts agent-updates of all ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (width, height, agents_per_side, model, replicas, description)
+    "c5_aco": (16384, 16384, 25_000_000, "aco", 1, "C5: ACO 16384x16384, 25M agents/side (50M), seed 42"),
+    "c5_lem": (16384, 16384, 25_000_000, "lem", 1, "C5-LEM: LEM 16384x16384, 25M agents/side (50M), seed 42"),
+    "c4_aco_x64": (480, 480, 51_200, "aco", 64, "C4 x64: ACO 480x480, 51,200 agents/side, 64 seeds per launch"),
+    "c3_lem_x64": (480, 480, 51_200, "lem", 64, "C3 x64: LEM 480x480, 51,200 agents/side, 64 seeds per launch"),
+    "c4_aco": (480, 480, 51_200, "aco", 1, "C4: ACO 480x480, 51,200 agents/side (102,400), seed 42"),
+    "c3_lem": (480, 480, 51_200, "lem", 1, "C3: LEM 480x480, 51,200 agents/side (102,400), seed 42"),
+    "c2_aco": (480, 480, 1_024, "aco", 1, "C2: ACO 480x480, 1,024 agents/side, seed 42"),
+    "c1_lem": (480, 480, 1_024, "lem", 1, "C1: LEM 480x480, 1,024 agents/side, seed 42"),
+}
+
+
+def alg_bytes(w, h, n, model, replicas):
+    """Algorithmic HBM bytes per step: LEM 8 B/cell (read +
+    write the 32-bit cell word); ACO 40 B/cell (+ two f64 pheromone fields
+    read + written) + 16 B/agent (f64 tour read + written)."""
+    cells = w * h * replicas
+    if model == "lem":
+        return 8 * cells
+    return 40 * cells + 16 * 2 * n * replicas
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def scenario(name):
+    import paper_1412_4933_b200 as p
+
+    w, h, n, model, reps, desc = WORKLOADS[name]
+    cfg = p.ScenarioConfig(width=w, height=h, agents_per_side=n, model=p.Model.Lem if model == "lem" else p.Model.Aco,
+                           seed=42)
+    return cfg, reps, desc
+
+
+# ------------------------------------------------------------------ CPU arms
+
+def cpu_reference_run(name, steps, warmup, budget_s):
+    """The reference CPU implementation on this host: oracle/_ref (the
+    reference library built from its own sources) when present, else the C
+    oracle port. Parallel executor with every host thread. Returns a dict."""
+    from oracle.oracle import OracleState, Reference, Scenario
+
+    w, h, n, model, reps, desc = WORKLOADS[name]
+    sc = Scenario(width=w, height=h, agents_per_side=n, model=model, seed=42)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if Reference.available():
+        eng, kind, cores = Reference(sc, threads=threads), "reference", threads
+    else:
+        eng, kind, cores = OracleState(sc), "port", 1
+    setup = time.perf_counter() - t0
+
+    def one():
+        if kind == "reference":
+            return eng.run(1)[1]
+        t = time.perf_counter()
+        eng.run(1)
+        return time.perf_counter() - t
+
+    spent = 0.0
+    for _ in range(warmup):
+        if spent > budget_s / 3:
+            break
+        spent += one()
+    done, secs = 0, 0.0
+    while done < max(1, steps):
+        secs += one()
+        done += 1
+        if secs + spent > budget_s:
+            break
+    agents = 2 * n
+    return {"value": agents * done / secs, "secs": secs, "steps": done, "kind": kind, "cores": cores,
+            "setup_s": setup, "cells": w * h,
+            "sample": f"{desc}; steps {warmup}..{warmup + done - 1} timed after new_environment "
+                      f"({setup:.1f}s untimed setup), {'Parallel executor' if kind == 'reference' else 'sequential C port'}, "
+                      f"{cores} thread(s)"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # only rank 0 times the CPU reference
+    r = cpu_reference_run(args.workload, args.steps, args.warmup, args.ref_budget)
+    w, h, n, model, reps, desc = WORKLOADS[args.workload]
+    line = {
+        "impl": "reference", "metric": "agent-updates/sec", "value": r["value"], "unit": "agent-updates/s",
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * r["secs"] / r["steps"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32",
+        "data": "synthetic (new_environment placement, seed 42)",
+        "config": {"workload": desc, "width": w, "height": h, "agents_per_side": n, "model": model, "replicas": 1},
+        "cell_updates_per_s": w * h * r["steps"] / r["secs"],
+        "cpu_baseline": {"value": r["value"], "unit": "agent-updates/s", "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "agent-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def secondary_runs(steps):
+    """C4/C3 (100K agents) replica-batched and single-scenario device timings."""
+    import paper_1412_4933_b200 as p
+
+    peak, _ = measured_peak()
+    out = {}
+    for name in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem"):
+        cfg, reps, desc = scenario(name)
+        ens = p.Ensemble(cfg, replicas=reps)
+        ens.run(5)
+        tot, ker = ens.time_steps(steps, kernel=True)
+        b = alg_bytes(cfg.width, cfg.height, cfg.agents_per_side, "lem" if cfg.model == p.Model.Lem else "aco", reps)
+        out[name] = {
+            "workload": desc, "ms_per_step": tot / steps, "kernel_ms": ker,
+            "agent_updates_per_s": 2 * cfg.agents_per_side * reps * steps / (tot / 1e3),
+            "cell_updates_per_s": cfg.width * cfg.height * reps * steps / (tot / 1e3),
+            "roofline_frac": b / (ker / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
+        }
+        ens.close()
+    return out
+
+
+def run_gpu_arm(args):
+    import torch
+
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg, reps, desc = scenario(args.workload)
+    if args.replicas:
+        reps = args.replicas
+    w, h, n = cfg.width, cfg.height, cfg.agents_per_side
+    model = "lem" if cfg.model == p.Model.Lem else "aco"
+    peak, peak_src = measured_peak()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # --- device-resident throughput -----------------------------------
+    from paper_1412_4933_b200.sharding import ShardedEngine
+
+    t_setup = time.perf_counter()
+    eng = ShardedEngine(cfg, rank, world, device=local, replicas=reps)
+    setup_s = time.perf_counter() - t_setup
+    eng.step(args.warmup)
+    eng.synchronize()
+    barrier()
+    stream = torch.cuda.ExternalStream(eng.ctx.stream(), device=f"cuda:{local}")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.ctx.launches
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        if world == 1:
+            eng.ctx.step_async(args.steps)  # CUDA-graph batches
+        else:
+            eng.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+    barrier()
+    launches = eng.ctx.launches - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    rep = eng.reports(min(args.steps, 1024))
+    moved_local = int(rep["moved"].sum())
+
+    # dominant kernel: mean per-launch duration (CUDA events around each launch)
+    _, kernel_ms = eng.ctx.time_steps(min(args.steps, 20), kernel=True)
+    kernel_ms = max_over_ranks(kernel_ms)
+    eng.close()
+
+    agents_total = 2 * n * reps
+    value = agents_total * args.steps / (ms / 1e3)
+    bytes_step = alg_bytes(w, h, n, model, reps)
+    bytes_launch = bytes_step / world  # per rank's kernel (its shard)
+    achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
+
+    # --- end to end through the C-ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks)
+
+    line = None
+    if rank == 0:
+        traffic = ncu_traffic(args.workload)
+        line = {
+            "metric": "agent-updates/sec", "value": value, "unit": "agent-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32",
+            "data": "synthetic (new_environment placement, seed 42; replica i uses seed 42+i)",
+            "config": {"workload": desc, "width": w, "height": h, "agents_per_side": n, "model": model,
+                       "replicas": reps, "parallelism": f"row-shard x{world} (3-row NCCL halo/step)" if world > 1
+                       else "single GPU", "l2": "inputs larger than L2 (resident state >> 126 MB; no flush)"},
+            "cell_updates_per_s": w * h * reps * args.steps / (ms / 1e3),
+            "hbm_gbs_alg_step": bytes_step / (ms / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "step_fused_kernel", "kernel_ms": kernel_ms,
+                         "alg_bytes_per_launch": bytes_launch},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "setup_s": setup_s,
+            "moved_in_window_rank0": moved_local,
+        }
+        if e2e:
+            line["e2e"] = e2e
+    if dist is not None:
+        dist.barrier()
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            r = cpu_reference_run(args.workload, args.cpu_steps, 0, args.cpu_budget)
+            line["cpu_baseline"] = {"value": r["value"], "unit": "agent-updates/s", "cores": r["cores"],
+                                    "kind": r["kind"], "sample": r["sample"]}
+        if world == 1 and not args.no_secondary:
+            line["secondary"] = secondary_runs(50)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
+    """Same metric through the reference-facing API with HOST buffers: upload a
+    host SimState (pf_load_state), K steps with reports read back to the host,
+    download the SimState (pf_store_state) — all inside the timed region."""
+    import numpy as np
+
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import HaloExchanger, row_partition
+
+    state = p.new_environment(cfg, 42)  # host planes (reference layout)
+    lo, hi = row_partition(cfg.height, world)[rank]
+    c = _lib.Context(_pf_config(cfg, 42, row_begin=0 if world == 1 else lo, row_end=0 if world == 1 else hi,
+                                device=local))
+    aco = cfg.model == p.Model.Aco
+    H, W = cfg.height, cfg.width
+    rows = (min(H, hi + 3) - max(0, lo - 3))
+    h2d = rows * W * (1 + 4 + (16 if aco else 0)) + len(state.agents) * 40
+    d2h = (hi - lo) * W * (1 + 4 + (16 if aco else 0)) + len(state.agents) * 40 + 16 * args.steps
+    import torch
+
+    ex = HaloExchanger(rank, world)
+    stream = torch.cuda.ExternalStream(c.stream(), device=f"cuda:{local}")
+    from paper_1412_4933_b200.sharding import _device_tensor
+
+    def planes(side, recv):
+        hh = c.halo(0, side, recv)
+        return [_device_tensor(pt, nb, local) for pt, nb in ((hh.cells, hh.cell_bytes), (hh.tau, hh.tau_bytes),
+                                                             (hh.tour, hh.tour_bytes)) if nb]
+
+    barrier()
+    t0 = time.perf_counter()
+    c.load(0, state.occupancy, state.index, state.agents, state.pheromone_top, state.pheromone_bottom, 0)
+    if world == 1:
+        rep = c.step(args.steps)
+    else:
+        for _ in range(args.steps):
+            c.step_async(1)
+            with torch.cuda.stream(stream):
+                ex.exchange(planes)
+        rep = c.read_reports(min(args.steps, 1024))
+    c.store(0, state._occ, state._index, state._agents, state._tau_top, state._tau_bot)
+    secs = max_over_ranks(time.perf_counter() - t0)
+    c.close()
+    del rep
+    return {"value": 2 * cfg.agents_per_side * args.steps / secs, "unit": "agent-updates/s",
+            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+            "seconds": secs, "path": "pf_load_state -> pf_step(K) (+reports) -> pf_store_state, pageable host planes"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5_aco")
+    ap.add_argument("--replicas", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

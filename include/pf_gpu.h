@@ -115,8 +115,9 @@ int pf_store_state(pf_ctx* ctx, int32_t replica, uint8_t* occ, uint32_t* index, 
  * [replicas][n] reports. Synchronous. */
 int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out);
 
-/* Asynchronous variant: enqueue n steps on the context's stream; reports
- * stay on the device until pf_read_reports (which synchronizes). */
+/* Asynchronous variant: enqueue n steps on the context's stream. Reports stay
+ * on the device in a ring of the last 1024 steps; pf_read_reports
+ * (synchronizes) returns those of steps [step - n, step) as [replicas][n]. */
 int pf_step_async(pf_ctx* ctx, uint32_t n);
 int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n);
 int pf_synchronize(pf_ctx* ctx);

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <functional>
 #include <map>
 #include <string>
 #include <thread>
@@ -34,7 +36,8 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(PF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-constexpr int kBatchCap = 256;  // steps per captured graph / report slab
+constexpr int kBatchCap = 256;   // steps per captured CUDA graph
+constexpr int kReportCap = 1024; // report ring slots per replica (slot = step % kReportCap)
 
 }  // namespace
 
@@ -45,7 +48,7 @@ struct pf_ctx {
     int parity = 0;                 // buffer holding the current state
     uint32_t step = 0;              // host mirror of the device step counter
     uint32_t* d_step = nullptr;
-    uint32_t* d_reports = nullptr;  // [replicas][kBatchCap][4]
+    uint32_t* d_reports = nullptr;  // [replicas][kReportCap][4] ring
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
     std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
@@ -213,7 +216,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     auto* kc = static_cast<pfdev::StepConsts*>(alloc(sizeof(pfdev::StepConsts)));
     ok = ok && kc && cudaMemcpy(kc, &ctx->args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice) == cudaSuccess;
     ctx->args.kc = kc;
-    ctx->d_reports = static_cast<uint32_t*>(alloc(size_t(cfg->replicas) * kBatchCap * 16));
+    ctx->d_reports = static_cast<uint32_t*>(alloc(size_t(cfg->replicas) * kReportCap * 16));
     if (!ok || !ctx->d_step || !ctx->d_reports) {
         cudaGetLastError();
         return cleanup(fail(PF_ERR_CUDA, "device allocation failed (out of memory?)"));
@@ -229,7 +232,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->args.seed_base = cfg->seed;
     ctx->args.d_step = ctx->d_step;
     ctx->args.reports = ctx->d_reports;
-    ctx->args.batch_cap = kBatchCap;
+    ctx->args.report_cap = kReportCap;
     ctx->args.row_begin = ctx->row_begin;
     ctx->args.rows_owned = ctx->rows_owned;
     ctx->args.rows_buf = ctx->rows_buf;
@@ -237,6 +240,19 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "init failed"));
     *out = ctx;
     return PF_OK;
+}
+
+// Run fn(begin, end) over [0, n) on the host's threads (state conversion).
+static void host_parallel(size_t n, const std::function<void(size_t, size_t)>& fn) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 32), std::max<size_t>(1, n / 64));
+    if (nt <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+    for (auto& t : ts) t.join();
 }
 
 // Global row of buffer row b.
@@ -247,14 +263,16 @@ static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& wor
                           const std::vector<double2>* tau) {
     const size_t off = size_t(rep) * ctx->plane();
     pfk::Planes& P = ctx->args.p;
+    // One host->device copy per plane; the second ping-pong buffer is filled
+    // device-side (its ghost rows must hold the same walls / halo).
     PF_CUDA(cudaMemcpyAsync(P.cell[0] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     if (ctx->aco()) {
         if (tour) PF_CUDA(cudaMemcpyAsync(P.tour + off, tour->data(), ctx->plane() * 8, cudaMemcpyHostToDevice, ctx->stream));
         else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
         if (tau) {
             PF_CUDA(cudaMemcpyAsync(P.tau[0] + off, tau->data(), ctx->plane() * 16, cudaMemcpyHostToDevice, ctx->stream));
-            PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, tau->data(), ctx->plane() * 16, cudaMemcpyHostToDevice, ctx->stream));
+            PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
         } else {
             ctx->launches += pfk::launch_fill_tau(P.tau[0] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
             ctx->launches += pfk::launch_fill_tau(P.tau[1] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
@@ -322,28 +340,48 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     std::vector<uint32_t> words(ctx->plane(), 0u);
     std::vector<double> tour(ctx->aco() ? ctx->plane() : 0, 0.0);
     std::vector<double2> tau(ctx->aco() ? ctx->plane() : 0, make_double2(0.0, 0.0));
-    for (int b = 0; b < ctx->rows_buf; ++b) {
-        const int64_t g = grow_of(ctx, b);
-        uint32_t* wrow = words.data() + size_t(b) * W;
-        if (g < 0 || g >= c.height) {
-            std::fill(wrow, wrow + W, kWall);
-            continue;
+    // check_consistency-style audit (src/state.cpp:77-110) + conversion to
+    // cell words, parallel over buffer rows.
+    std::atomic<int> bad{0};  // 0 ok, else index into kWhy
+    static const char* kWhy[] = {"", "state corrupt: index/occupancy mismatch", "state corrupt: index out of agent range",
+                                 "state corrupt: agent record id mismatch",
+                                 "state corrupt: agent position disagrees with index grid",
+                                 "state corrupt: agent group disagrees with occupancy"};
+    host_parallel(size_t(ctx->rows_buf), [&](size_t b0, size_t b1) {
+        for (size_t b = b0; b < b1 && !bad.load(std::memory_order_relaxed); ++b) {
+            const int64_t g = grow_of(ctx, int(b));
+            uint32_t* wrow = words.data() + b * W;
+            if (g < 0 || g >= c.height) {
+                std::fill(wrow, wrow + W, kWall);
+                continue;
+            }
+            for (size_t col = 0; col < W; ++col) {
+                const size_t gi = size_t(g) * W + col;
+                const uint32_t id = index[gi];
+                if (ctx->aco()) tau[b * W + col] = make_double2(tau_top[gi], tau_bot[gi]);
+                int why = 0;
+                if ((id == 0) != (occ[gi] == 0)) why = 1;
+                else if (id == 0) continue;
+                else if (id > n_agents) why = 2;
+                else {
+                    const pf_agent& a = agents[id - 1];
+                    if (a.index != id) why = 3;
+                    else if (a.row != g || a.col != int32_t(col)) why = 4;
+                    else if (a.group != occ[gi] || (a.group != 1 && a.group != 2)) why = 5;
+                    else {
+                        wrow[col] = id | (a.crossed ? pfdev::kCrossedBit : 0u) | (uint32_t(a.group) << 30);
+                        if (ctx->aco()) tour[b * W + col] = a.tour_length;
+                    }
+                }
+                if (why) {
+                    int expected = 0;
+                    bad.compare_exchange_strong(expected, why);
+                    break;
+                }
+            }
         }
-        for (size_t col = 0; col < W; ++col) {
-            const size_t gi = size_t(g) * W + col;
-            const uint32_t id = index[gi];
-            if (ctx->aco()) tau[size_t(b) * W + col] = make_double2(tau_top[gi], tau_bot[gi]);
-            if ((id == 0) != (occ[gi] == 0)) return fail(PF_ERR_STATE, "state corrupt: index/occupancy mismatch");
-            if (id == 0) continue;
-            if (id > n_agents) return fail(PF_ERR_STATE, "state corrupt: index out of agent range");
-            const pf_agent& a = agents[id - 1];
-            if (a.index != id) return fail(PF_ERR_STATE, "state corrupt: agent record id mismatch");
-            if (a.row != g || a.col != int32_t(col)) return fail(PF_ERR_STATE, "state corrupt: agent position disagrees with index grid");
-            if (a.group != occ[gi] || (a.group != 1 && a.group != 2)) return fail(PF_ERR_STATE, "state corrupt: agent group disagrees with occupancy");
-            wrow[col] = id | (a.crossed ? pfdev::kCrossedBit : 0u) | (uint32_t(a.group) << 30);
-            if (ctx->aco()) tour[size_t(b) * W + col] = a.tour_length;
-        }
-    }
+    });
+    if (bad.load()) return fail(PF_ERR_STATE, kWhy[bad.load()]);
     if (int rc = upload_replica(ctx, rep, words, ctx->aco() ? &tour : nullptr, ctx->aco() ? &tau : nullptr)) return rc;
     // Both buffers now hold the state; keep the current parity.
     set_step(ctx, step);
@@ -372,44 +410,67 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         PF_CUDA(cudaMemcpy(tau.data(), P.tau[ctx->parity] + off, own * 16, cudaMemcpyDeviceToHost));
     }
     const size_t g0 = size_t(ctx->row_begin) * W;
-    for (size_t i = 0; i < own; ++i) {
-        const uint32_t w = words[i];
-        const size_t gi = g0 + i;
-        if (tau_top && ctx->aco()) tau_top[gi] = tau[i].x;
-        if (tau_bot && ctx->aco()) tau_bot[gi] = tau[i].y;
-        const uint32_t id = w & pfdev::kIdMask;
-        if (occ) occ[gi] = uint8_t(w ? (w >> 30) : 0);
-        if (index) index[gi] = w ? id : 0;
-        if (!w) continue;
-        if (id == 0 || id > n_agents) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
-        if (agents) {
-            pf_agent& a = agents[id - 1];
-            std::memset(&a, 0, sizeof a);
-            a.index = id;
-            a.group = uint8_t(w >> 30);
-            a.row = a.future_row = int32_t(gi / W);
-            a.col = a.future_col = int32_t(gi % W);
-            a.tour_length = ctx->aco() ? tour[i] : 0.0;
-            a.crossed = (w & pfdev::kCrossedBit) ? 1 : 0;
+    std::atomic<bool> bad{false};
+    host_parallel(own, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            const uint32_t w = words[i];
+            const size_t gi = g0 + i;
+            if (tau_top && ctx->aco()) tau_top[gi] = tau[i].x;
+            if (tau_bot && ctx->aco()) tau_bot[gi] = tau[i].y;
+            const uint32_t id = w & pfdev::kIdMask;
+            if (occ) occ[gi] = uint8_t(w ? (w >> 30) : 0);
+            if (index) index[gi] = w ? id : 0;
+            if (!w) continue;
+            if (id == 0 || id > n_agents) {
+                bad = true;
+                continue;
+            }
+            if (agents) {  // ids are unique, so the writes are disjoint
+                pf_agent& a = agents[id - 1];
+                std::memset(&a, 0, sizeof a);
+                a.index = id;
+                a.group = uint8_t(w >> 30);
+                a.row = a.future_row = int32_t(gi / W);
+                a.col = a.future_col = int32_t(gi % W);
+                a.tour_length = ctx->aco() ? tour[i] : 0.0;
+                a.crossed = (w & pfdev::kCrossedBit) ? 1 : 0;
+            }
         }
-    }
+    });
+    if (bad) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
     if (step) *step = ctx->step;
     return PF_OK;
 }
 
-// Enqueue n <= kBatchCap steps starting at batch slot 0 with current parity.
-static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
-    for (uint32_t i = 0; i < n; ++i) {
-        const int par = (parity + int(i)) & 1;
-        ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED ? pfk::launch_step_fused(ctx->args, int(i), par, ctx->stream)
-                                                            : pfk::launch_step_pipeline(ctx->args, int(i), par, ctx->stream);
+// Zero the report-ring slots of steps [first, first + n) on every replica.
+static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
+    const size_t pitch = size_t(kReportCap) * 16;
+    uint32_t done = 0;
+    while (done < n) {
+        const uint32_t slot = (first + done) % kReportCap;
+        const uint32_t m = std::min<uint32_t>(n - done, kReportCap - slot);
+        PF_CUDA(cudaMemset2DAsync(reinterpret_cast<char*>(ctx->d_reports) + size_t(slot) * 16, pitch, 0,
+                                  size_t(m) * 16, size_t(ctx->cfg.replicas), ctx->stream));
+        done += m;
     }
+    return PF_OK;
+}
+
+static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
+    ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED ? pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream)
+                                                        : pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream);
+    return PF_OK;
+}
+
+// Enqueue n <= kBatchCap steps (batch slots 0..n-1) with the given start parity.
+static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
+    for (uint32_t i = 0; i < n; ++i) launch_one_step(ctx, i, (parity + int(i)) & 1);
     ctx->launches += pfk::launch_advance_step(ctx->d_step, n, ctx->stream);
     return PF_OK;
 }
 
 static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
-    PF_CUDA(cudaMemsetAsync(ctx->d_reports, 0, size_t(ctx->cfg.replicas) * kBatchCap * 16, ctx->stream));
+    if (int rc = zero_reports(ctx, ctx->step, n)) return rc;
     const auto key = std::make_pair(n, ctx->parity);
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
@@ -444,15 +505,24 @@ int pf_step_async(pf_ctx* ctx, uint32_t n) {
     return PF_OK;
 }
 
+// Reports of the last n steps ([step - n, step)) of every replica: out is
+// [replicas][n].
 int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n) {
-    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
-    if (n > kBatchCap) return fail(PF_ERR_ARG, "at most 256 reports are kept on the device");
+    if (!ctx || (!out && n)) return fail(PF_ERR_ARG, "null argument");
+    if (n > uint32_t(kReportCap)) return fail(PF_ERR_ARG, "at most 1024 step reports are kept on the device");
+    if (n > ctx->step) return fail(PF_ERR_ARG, "fewer steps than requested reports");
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
     const int R = ctx->cfg.replicas;
-    std::vector<uint32_t> buf(size_t(R) * kBatchCap * 4);
-    PF_CUDA(cudaMemcpy(buf.data(), ctx->d_reports, buf.size() * 4, cudaMemcpyDeviceToHost));
-    for (int r = 0; r < R; ++r)
-        std::memcpy(out + size_t(r) * n, buf.data() + size_t(r) * kBatchCap * 4, size_t(n) * 16);
+    const size_t pitch = size_t(kReportCap) * 16;
+    const uint32_t first = ctx->step - n;
+    uint32_t done = 0;
+    while (done < n) {
+        const uint32_t slot = (first + done) % kReportCap;
+        const uint32_t m = std::min<uint32_t>(n - done, kReportCap - slot);
+        PF_CUDA(cudaMemcpy2D(out + done, size_t(n) * 16, reinterpret_cast<const char*>(ctx->d_reports) + size_t(slot) * 16,
+                             pitch, size_t(m) * 16, size_t(R), cudaMemcpyDeviceToHost));
+        done += m;
+    }
     return PF_OK;
 }
 
@@ -504,13 +574,10 @@ int pf_time_steps(pf_ctx* ctx, uint32_t n, float* total_ms, float* kernel_ms) {
         uint32_t done = 0;
         while (done < n) {
             const uint32_t m = std::min<uint32_t>(n - done, kBatchCap);
-            PF_CUDA(cudaMemsetAsync(ctx->d_reports, 0, size_t(ctx->cfg.replicas) * kBatchCap * 16, ctx->stream));
+            if (int rc = zero_reports(ctx, ctx->step, m)) return rc;
             for (uint32_t i = 0; i < m; ++i) {
-                const int par = (ctx->parity + int(i)) & 1;
                 PF_CUDA(cudaEventRecord(ev[2 * (done + i)], ctx->stream));
-                ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED
-                                     ? pfk::launch_step_fused(ctx->args, int(i), par, ctx->stream)
-                                     : pfk::launch_step_pipeline(ctx->args, int(i), par, ctx->stream);
+                launch_one_step(ctx, i, (ctx->parity + int(i)) & 1);
                 PF_CUDA(cudaEventRecord(ev[2 * (done + i) + 1], ctx->stream));
             }
             ctx->launches += pfk::launch_advance_step(ctx->d_step, m, ctx->stream);

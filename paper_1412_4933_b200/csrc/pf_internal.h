@@ -31,8 +31,8 @@ struct StepArgs {
     Planes p;
     uint64_t seed_base;     // replica r uses seed_base + r
     const uint32_t* d_step; // device step counter: step of batch slot 0
-    uint32_t* reports;      // [replicas][batch_cap][4]
-    int batch_cap;
+    uint32_t* reports;      // [replicas][report_cap][4], ring slot = step % report_cap
+    int report_cap;
     int row_begin;          // global row of the first owned row
     int rows_owned;
     int rows_buf;           // rows_owned + 2 * kGhost

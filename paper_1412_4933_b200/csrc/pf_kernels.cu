@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256) step_fused_kernel(const StepArgs a, int s
         commit_cell<ACO>(k, w, win, vacate, src_word, a.row_begin + lr, gi, si, cout, tin, tout, tour, moved,
                          ntop, nbot);
     }
-    uint32_t* rep_slot = a.reports + (size_t(rep) * a.batch_cap + slot) * 4;
+    uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
     block_count(moved, ntop, nbot, s_cnt, rep_slot, step, blockIdx.x == 0 && blockIdx.y == 0);
 }
 
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256) pipeline_commit_kernel(const StepArgs a, 
                          ACO ? a.p.tau[parity] + base : nullptr, ACO ? a.p.tau[parity ^ 1] + base : nullptr,
                          ACO ? a.p.tour + base : nullptr, moved, ntop, nbot);
     }
-    uint32_t* rep_slot = a.reports + (size_t(rep) * a.batch_cap + slot) * 4;
+    uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
     block_count(moved, ntop, nbot, s_cnt, rep_slot, step, blockIdx.x == 0 && blockIdx.y == 0);
 }
 

@@ -1,0 +1,150 @@
+"""Row-sharded multi-GPU stepping: one process per GPU, torch.distributed (NCCL)
+for the per-step ghost-row exchange.
+
+The reference has no distributed backend; this is the new
+GPU<->GPU boundary. The grid is split into contiguous row blocks (SURVEY.md
+§8(e)); a step's dependency radius is 3 cells, so each shard keeps
+PF_GHOST_ROWS = 3 ghost rows above and below and, after every step, swaps with
+each vertical neighbour:
+
+    3 rows of cell words (u32)       — occupancy, id, crossed flag, group
+    3 rows of pheromone {top, bot}   — ACO only (f64 x 2)
+    1 row of tour lengths (f64)      — ACO only; movers read the source's
+
+Agents migrate implicitly: all agent state (id, group, crossed, tour) is
+cell-resident and arrives with the ghost rows. RNG keys use the agent id and
+the GLOBAL cell index, crossing uses the global row, so any shard count gives
+results bit-identical to one GPU and to the CPU oracle.
+
+The exchange code here is engine-agnostic: it moves torch tensors, so the CPU
+tests drive it with gloo and numpy-backed shards of the oracle, and the GPU
+path drives it with NCCL and tensors aliasing the library's device planes
+(via __cuda_array_interface__).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+GHOST = _lib.PF_GHOST_ROWS
+
+
+def row_partition(height: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced row blocks [lo, hi) for `world` shards."""
+    if world < 1:
+        raise _lib.ConfigError("world size must be >= 1")
+    parts = [(height * r // world, height * (r + 1) // world) for r in range(world)]
+    if world > 1 and min(hi - lo for lo, hi in parts) < GHOST:
+        raise _lib.ConfigError(f"each shard must own at least {GHOST} rows")
+    return parts
+
+
+class HaloExchanger:
+    """Per-step ghost-row swap with the neighbours rank-1 (above) and rank+1
+    (below) over a torch.distributed process group.
+
+    planes(side, recv) -> list of tensors, in a fixed plane order, for side 0
+    (toward row 0) or 1 (toward row H-1); recv=False: rows to send, True:
+    ghost rows to fill.
+    """
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def exchange(self, planes) -> None:
+        import torch.distributed as dist
+
+        ops = []
+        if self.rank > 0:
+            peer = self.rank - 1
+            ops += [dist.P2POp(dist.isend, t, peer, self.group) for t in planes(0, False)]
+            ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t in planes(0, True)]
+        if self.rank < self.world - 1:
+            peer = self.rank + 1
+            ops += [dist.P2POp(dist.isend, t, peer, self.group) for t in planes(1, False)]
+            ops += [dist.P2POp(dist.irecv, t, peer, self.group) for t in planes(1, True)]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+class _DeviceRange:
+    """__cuda_array_interface__ view of a library-owned device range (bytes)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3, "strides": None,
+            "stream": None,
+        }
+
+
+def _device_tensor(ptr: int, nbytes: int, device: int):
+    import torch
+
+    return torch.as_tensor(_DeviceRange(ptr, nbytes), device=f"cuda:{device}")
+
+
+class ShardedEngine:
+    """One rank's row shard of `replicas` scenarios, stepped on its GPU with a
+    ghost-row exchange after every step."""
+
+    def __init__(self, cfg, rank: int, world: int, *, device: int | None = None, replicas: int = 1,
+                 seed: int | None = None, kernel: str = "fused", group=None):
+        import torch
+
+        from .engine import _pf_config, validate
+
+        validate(cfg)
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        self.device = rank if device is None else device
+        self.lo, self.hi = row_partition(cfg.height, world)[rank]
+        whole = world == 1
+        self.ctx = _lib.Context(_pf_config(cfg, cfg.seed if seed is None else seed, replicas=replicas,
+                                           row_begin=0 if whole else self.lo, row_end=0 if whole else self.hi,
+                                           device=self.device, kernel=kernel))
+        self.ctx.init_environment()
+        self.exchanger = HaloExchanger(rank, world, group)
+        self._tcache: dict = {}
+        self._stream = torch.cuda.ExternalStream(self.ctx.stream(), device=f"cuda:{self.device}")
+
+    def _planes(self, side: int, recv: bool):
+        out = []
+        for r in range(self.ctx.replicas):
+            h = self.ctx.halo(r, side, recv)
+            for ptr, nb in ((h.cells, h.cell_bytes), (h.tau, h.tau_bytes), (h.tour, h.tour_bytes)):
+                if not nb:
+                    continue
+                key = (ptr, nb)
+                t = self._tcache.get(key)
+                if t is None:
+                    t = self._tcache[key] = _device_tensor(ptr, nb, self.device)
+                out.append(t)
+        return out
+
+    def step(self, n: int = 1) -> None:
+        """n steps; the halo swap is stream-ordered after each step's kernel."""
+        import torch
+
+        for _ in range(n):
+            self.ctx.step_async(1)
+            if self.world > 1:
+                with torch.cuda.stream(self._stream):
+                    self.exchanger.exchange(self._planes)
+
+    def reports(self, n: int) -> np.ndarray:
+        """This shard's [replicas][n] reports of the last n steps (sum over ranks
+        for the whole grid's StepReport)."""
+        return self.ctx.read_reports(n)
+
+    def synchronize(self):
+        self.ctx.synchronize()
+
+    def store(self, replica: int, occ, index, agents, tau_top, tau_bot) -> int:
+        """Write this shard's owned rows (and the agents living there) into
+        global-grid host planes."""
+        return self.ctx.store(replica, occ, index, agents, tau_top, tau_bot)
+
+    def close(self):
+        self.ctx.close()

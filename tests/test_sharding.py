@@ -1,0 +1,198 @@
+"""Row sharding (the N>1 path).
+
+CPU (gloo, world_size 2 and 3): the product's HaloExchanger drives shards of
+the C oracle (pfo_step_cells: one reference step over a row window of the
+cell-resident layout); gathering the owned rows must reproduce the
+single-domain oracle bit-for-bit. This pins the decomposition, the ghost depth
+of 3, the plane set and the global RNG keys.
+
+GPU: several shard contexts on one device, exchanging through the same halo
+ranges via pf_exchange_pair, must equal the unsharded GPU run and the oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleState, Scenario, _oracle_lib
+
+GHOST = 3
+
+
+def _cells_from_oracle(o: OracleState):
+    """Cell-resident planes (the product's device layout) from an oracle SimState."""
+    H, W = o.index.shape
+    cell = np.zeros((H, W), np.uint32)
+    tour = np.zeros((H, W), np.float64)
+    occ = o.index != 0
+    ids = o.index[occ]
+    a = o.agents[ids - 1]
+    cell[occ] = ids | (a["crossed"].astype(np.uint32) << 29) | (a["group"].astype(np.uint32) << 30)
+    tour[occ] = a["tour_length"]
+    return cell, tour
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, kw, steps, out_q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1412_4933_b200.sharding import HaloExchanger, row_partition
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc = Scenario(**kw)
+        H, W = sc.height, sc.width
+        o = OracleState(sc)
+        gcell, gtour = _cells_from_oracle(o)
+        aco = sc.model == "aco"
+        lo, hi = row_partition(H, world)[rank]
+        row0 = lo - GHOST
+        nrows = hi - lo + 2 * GHOST
+        cell = np.zeros((nrows, W), np.uint32)
+        tour = np.zeros((nrows, W), np.float64)
+        tt = np.zeros((nrows, W), np.float64)
+        tb = np.zeros((nrows, W), np.float64)
+        for b in range(nrows):
+            g = row0 + b
+            if 0 <= g < H:
+                cell[b], tour[b] = gcell[g], gtour[g]
+                if aco:
+                    tt[b], tb[b] = o.tau_top[g], o.tau_bot[g]
+        own = hi - lo
+
+        def planes(side, recv):
+            if side == 0:
+                rows = slice(0, GHOST) if recv else slice(GHOST, 2 * GHOST)
+                trow = GHOST - 1 if recv else GHOST
+            else:
+                rows = slice(GHOST + own, 2 * GHOST + own) if recv else slice(own, own + GHOST)
+                trow = GHOST + own if recv else GHOST + own - 1
+            out = [torch.from_numpy(cell[rows])]
+            if aco:
+                out += [torch.from_numpy(tt[rows]), torch.from_numpy(tb[rows]), torch.from_numpy(tour[trow])]
+            return out
+
+        ex = HaloExchanger(rank, world)
+        lib = _oracle_lib()
+        cfg = sc.cstruct()
+        rep = np.zeros(4, np.uint32)
+        reps = []
+        for t in range(steps):
+            rc = lib.pfo_step_cells(C.byref(cfg), sc.seed, t, row0, nrows, cell.ctypes.data, tour.ctypes.data,
+                                    tt.ctypes.data if aco else None, tb.ctypes.data if aco else None,
+                                    GHOST, GHOST + own, rep.ctypes.data)
+            assert rc == 0
+            reps.append(rep.copy())
+            ex.exchange(planes)
+        out_q.put((rank, lo, hi, cell[GHOST:GHOST + own].copy(), tour[GHOST:GHOST + own].copy(),
+                   tt[GHOST:GHOST + own].copy() if aco else None, tb[GHOST:GHOST + own].copy() if aco else None,
+                   np.array(reps)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kw", [
+    dict(width=48, height=48, agents_per_side=400, model="aco", seed=5),
+    dict(width=32, height=48, agents_per_side=300, model="lem", seed=9),
+])
+def test_gloo_sharded_oracle_matches_single_domain(kw, world):
+    import torch.multiprocessing as mp
+
+    steps = 40
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, kw, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    results.sort(key=lambda r: r[0])
+
+    sc = Scenario(**kw)
+    o = OracleState(sc)
+    ref_rep = o.run(steps)
+    cell, tour = _cells_from_oracle(o)
+    for rank, lo, hi, c, t, tt, tb, reps in results:
+        assert (c == cell[lo:hi]).all(), f"rank {rank} cell words differ"
+        occ = c != 0
+        assert (t[occ] == tour[lo:hi][occ]).all(), f"rank {rank} tour lengths differ"
+        if tt is not None:
+            assert (tt == o.tau_top[lo:hi]).all() and (tb == o.tau_bot[lo:hi]).all()
+    tot = sum(r[7] for r in results)
+    assert (tot[:, 1] == ref_rep["moved"]).all()
+    assert (tot[:, 2] == ref_rep["newly_crossed_top"]).all()
+    assert (tot[:, 3] == ref_rep["newly_crossed_bottom"]).all()
+
+
+def test_row_partition():
+    from paper_1412_4933_b200 import ConfigError
+    from paper_1412_4933_b200.sharding import row_partition
+
+    assert row_partition(16384, 8) == [(2048 * i, 2048 * (i + 1)) for i in range(8)]
+    parts = row_partition(100, 3)
+    assert parts[0][0] == 0 and parts[-1][1] == 100
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    with pytest.raises(ConfigError):
+        row_partition(16, 8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+@pytest.mark.parametrize("nshards", [2, 4])
+def test_gpu_multishard_one_device(model, nshards):
+    """k shard contexts on one GPU exchanging via pf_exchange_pair == unsharded run."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
+
+    cfg = p.ScenarioConfig(width=96, height=96, agents_per_side=1500, model=p.Model.Lem if model == "lem" else p.Model.Aco,
+                           seed=21)
+    steps = 60
+    whole = p.Ensemble(cfg, replicas=2, seed=21)
+    whole_rep = whole.run(steps)
+    shards = []
+    for lo, hi in row_partition(cfg.height, nshards):
+        c = _lib.Context(_pf_config(cfg, 21, replicas=2, row_begin=lo, row_end=hi))
+        c.init_environment()
+        shards.append(c)
+    for _ in range(steps):
+        for c in shards:
+            c.step_async(1)
+        for up, dn in zip(shards, shards[1:]):
+            _lib.exchange_pair(up, dn)
+    tot = sum(c.read_reports(steps)["moved"].astype(np.int64) for c in shards)
+    assert (tot == whole_rep["moved"]).all()
+    for r in range(2):
+        ref = whole.state(r)
+        H, W = cfg.height, cfg.width
+        occ = np.zeros((H, W), np.uint8)
+        idx = np.zeros((H, W), np.uint32)
+        ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+        tt = np.zeros((H, W)) if model == "aco" else None
+        tb = np.zeros((H, W)) if model == "aco" else None
+        for c in shards:
+            assert c.store(r, occ, idx, ag, tt, tb) == steps
+        assert (idx == ref.index).all() and (occ == ref.occupancy).all()
+        assert (ag["tour_length"] == ref.agents["tour_length"]).all()
+        assert (ag["crossed"] == ref.agents["crossed"]).all()
+        if tt is not None:
+            assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
