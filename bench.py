@@ -272,6 +272,8 @@ def run_gpu_arm(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = eng.ctx.launches
     with ClockSampler(local) as clocks:
+        time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
+        eng.step(max(1, args.warmup))  # keep the GPU busy while the sampler spins up
         torch.cuda.synchronize()
         e0.record(stream)
         if world == 1:
@@ -315,7 +317,7 @@ def run_gpu_arm(args):
                        "replicas": reps, "parallelism": f"row-shard x{world} (3-row NCCL halo/step)" if world > 1
                        else "single GPU", "l2": "inputs larger than L2 (resident state >> 126 MB; no flush)"},
             "cell_updates_per_s": w * h * reps * args.steps / (ms / 1e3),
-            "hbm_gbs_alg_step": bytes_step / (ms / 1e3) / 1e9,
+            "hbm_gbs_alg_step": bytes_step * args.steps / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "step_fused_kernel", "kernel_ms": kernel_ms,
@@ -395,7 +397,7 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5_aco")

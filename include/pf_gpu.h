@@ -32,8 +32,9 @@ extern "C" {
 #define PF_MODEL_LEM 0
 #define PF_MODEL_ACO 1
 
-#define PF_KERNEL_FUSED 0    /* one kernel per step (default) */
+#define PF_KERNEL_FUSED 0    /* one bit-sliced kernel per step (default) */
 #define PF_KERNEL_PIPELINE 1 /* propose / resolve / commit, three kernels per step */
+#define PF_KERNEL_TILE 2     /* one kernel per step, scalar per-cell shared-memory tile */
 
 /* Number of ghost rows kept above and below a row shard: one step's
  * dependency radius. */
@@ -50,7 +51,7 @@ typedef struct pf_config {
     int32_t row_begin; /* owned global rows [row_begin, row_end) of a row shard; */
     int32_t row_end;   /* row_end == 0 means the whole grid */
     int32_t device;    /* CUDA device ordinal */
-    int32_t kernel;    /* PF_KERNEL_FUSED or PF_KERNEL_PIPELINE */
+    int32_t kernel;    /* PF_KERNEL_FUSED, PF_KERNEL_PIPELINE or PF_KERNEL_TILE */
 } pf_config;
 
 /* Byte-identical to pedflow::AgentRecord (inc/grid.hpp:84-93), 40 bytes. */

@@ -13,11 +13,11 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpedflow_b200.so")
+LIB_PATH = os.environ.get("PEDFLOW_B200_LIB") or os.path.join(HERE, "libpedflow_b200.so")
 
 PF_OK, PF_ERR_CONFIG, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, 2, 3, 4, 5, 6
 PF_MODEL_LEM, PF_MODEL_ACO = 0, 1
-PF_KERNEL_FUSED, PF_KERNEL_PIPELINE = 0, 1
+PF_KERNEL_FUSED, PF_KERNEL_PIPELINE, PF_KERNEL_TILE = 0, 1, 2
 PF_GHOST_ROWS = 3
 
 # pedflow::AgentRecord (inc/grid.hpp:84-93) == pf_agent, 40 bytes.

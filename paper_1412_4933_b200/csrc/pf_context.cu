@@ -90,7 +90,8 @@ int pf_validate(const pf_config* c) {
     if (2 * int64_t(c->agents_per_side) >= (int64_t(1) << 29)) return fail(PF_ERR_CONFIG, "2 * agents_per_side must be < 2^29");
     if (c->replicas < 1) return fail(PF_ERR_CONFIG, "replicas must be >= 1");
     if (c->replicas > 65535) return fail(PF_ERR_CONFIG, "replicas must be <= 65535");
-    if (c->kernel != PF_KERNEL_FUSED && c->kernel != PF_KERNEL_PIPELINE) return fail(PF_ERR_CONFIG, "unknown kernel");
+    if (c->kernel != PF_KERNEL_FUSED && c->kernel != PF_KERNEL_PIPELINE && c->kernel != PF_KERNEL_TILE)
+        return fail(PF_ERR_CONFIG, "unknown kernel");
     if (c->row_end != 0) {
         if (c->row_begin < 0 || c->row_end > c->height || c->row_begin >= c->row_end)
             return fail(PF_ERR_CONFIG, "shard rows must satisfy 0 <= row_begin < row_end <= height");
@@ -187,6 +188,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         return rc;
     };
     if (cudaSetDevice(cfg->device) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "cudaSetDevice failed"));
+    if (pfk::configure_step_bits() != 0) return cleanup(fail(PF_ERR_CUDA, "cannot configure the step kernel's shared memory"));
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(PF_ERR_CUDA, "cudaStreamCreate failed"));
     auto alloc = [&](size_t bytes) -> void* {
@@ -457,8 +459,11 @@ static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
 }
 
 static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
-    ctx->launches += ctx->cfg.kernel == PF_KERNEL_FUSED ? pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream)
-                                                        : pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream);
+    switch (ctx->cfg.kernel) {
+        case PF_KERNEL_FUSED: ctx->launches += pfk::launch_step_bits(ctx->args, int(i), parity, ctx->stream); break;
+        case PF_KERNEL_TILE: ctx->launches += pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream); break;
+        default: ctx->launches += pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream); break;
+    }
     return PF_OK;
 }
 
@@ -486,7 +491,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
         it = ctx->graphs.emplace(key, ge).first;
     }
     PF_CUDA(cudaGraphLaunch(it->second, ctx->stream));
-    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_FUSED ? 1 : 3;
+    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1;
     ctx->launches += uint64_t(n) * per_step + 1;
     ctx->parity ^= int(n & 1u);
     ctx->step += n;

@@ -41,7 +41,9 @@ struct StepArgs {
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
 // Returns the number of kernel launches issued.
-int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s);
+int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s);   // PF_KERNEL_FUSED
+int configure_step_bits();
+int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s);  // PF_KERNEL_TILE
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
 // *d_step += n
 int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);

@@ -28,7 +28,7 @@ def _run_gpu(kw, steps, kernel="fused"):
     return state, rep
 
 
-@pytest.mark.parametrize("kernel", ["fused", "pipeline"])
+@pytest.mark.parametrize("kernel", ["fused", "pipeline", "tile"])
 @pytest.mark.parametrize("name", SMALL + BIG)
 def test_golden_anchor(anchors, name, kernel):
     a = anchors[name]

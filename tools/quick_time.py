@@ -26,6 +26,7 @@ run("C3 LEM 480 51200", C(width=480, height=480, agents_per_side=51200, model=L)
 run("C4 ACO 480 51200", C(width=480, height=480, agents_per_side=51200, model=A), 1, 200)
 run("C4 ACO 480 51200", C(width=480, height=480, agents_per_side=51200, model=A), 64, 50)
 run("C3 LEM 480 51200", C(width=480, height=480, agents_per_side=51200, model=L), 64, 50)
-run("C4 ACO 480 51200", C(width=480, height=480, agents_per_side=51200, model=A), 64, 20, "pipeline")
+run("C4 ACO 480 51200", C(width=480, height=480, agents_per_side=51200, model=A), 64, 20, "tile")
+run("C5 ACO 16384 25M", C(width=16384, height=16384, agents_per_side=25_000_000, model=A), 1, 10, "tile")
 run("C5 ACO 16384 25M", C(width=16384, height=16384, agents_per_side=25_000_000, model=A), 1, 10)
 run("C5 LEM 16384 25M", C(width=16384, height=16384, agents_per_side=25_000_000, model=L), 1, 10)
