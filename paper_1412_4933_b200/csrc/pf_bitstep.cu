@@ -200,7 +200,7 @@ __device__ __forceinline__ void set_winner(Smem& sm, int ai, int si, int j, int 
 }
 
 template <bool ACO>
-__global__ void __launch_bounds__(NT) step_bits_kernel(const StepArgs a, int slot, int parity) {
+__global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int slot, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -222,25 +222,35 @@ __global__ void __launch_bounds__(NT) step_bits_kernel(const StepArgs a, int slo
     for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0u;
     if (threadIdx.x == 0) sm.nq = 0u;
+    // Tiles away from the left/right edge need no per-lane column checks.
+    const bool interior = c0 >= 32 && c0 + 32 * (NS + 1) <= W;
     for (int sr = warp; sr < SR; sr += NW) {
         const int b = kGhost + r0 - 3 + sr;
         const bool row_ok = b < a.rows_buf;
-        const uint32_t* src = cin + size_t(b) * W;
+        const uint32_t* src = cin + size_t(b) * W + (c0 - 32) + lane;
         uint32_t w[SS];
+        if (row_ok && interior) {
 #pragma unroll
-        for (int si = 0; si < SS; ++si) {
-            const int c = c0 + 32 * (si - 1) + lane;
-            w[si] = (row_ok && c >= 0 && c < W) ? __ldg(src + c) : kWall;
+            for (int si = 0; si < SS; ++si) w[si] = __ldg(src + 32 * si);
+        } else {
+#pragma unroll
+            for (int si = 0; si < SS; ++si) {
+                const int c = c0 + 32 * (si - 1) + lane;
+                w[si] = (row_ok && c >= 0 && c < W) ? __ldg(src + 32 * si) : kWall;
+            }
         }
+        uint32_t m30 = 0u, m31 = 0u;  // lane si keeps segment si's planes
 #pragma unroll
         for (int si = 0; si < SS; ++si) {
             sm.word[sr][si * 32 + lane] = w[si];
-            const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, (w[si] >> 30) & 1u);
-            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w[si] >> 31);
-            if (lane == si) {
-                sm.v30[sr][si] = b30;
-                sm.v31[sr][si] = b31;
-            }
+            const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w[si] << 1) < 0);
+            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w[si]) < 0);
+            m30 = lane == si ? b30 : m30;
+            m31 = lane == si ? b31 : m31;
+        }
+        if (lane < SS) {
+            sm.v30[sr][lane] = m30;
+            sm.v31[sr][lane] = m31;
         }
     }
     __syncthreads();
@@ -336,13 +346,31 @@ __global__ void __launch_bounds__(NT) step_bits_kernel(const StepArgs a, int slo
         const int b = kGhost + lr;
         const int grow = a.row_begin + lr;
         const int sr = rr + 3, ai = rr + 1;
-#pragma unroll 2
+        const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
+        // ACO: issue the whole row's pheromone loads before using any of them.
+        double2 tv[NS];
+        if (ACO) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
         for (int si = 1; si <= NS; ++si) {
             const int gc = c0 + 32 * (si - 1) + lane;
             const bool valid = gc < W;
             const uint32_t Am = sm.A[ai][si], Gm = sm.G[rr][si];
             const uint32_t w = sm.word[sr][si * 32 + lane];
-            const size_t gi = size_t(b) * W + gc;
+            const size_t gi = row0 + 32 * (si - 1);
+            if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
+                if (valid) {
+                    cout[gi] = w;
+                    if (ACO) {
+                        const double2 t = tv[si - 1];
+                        tout[gi] = make_double2(__dmul_rn(t.x, a.k.factor), __dmul_rn(t.y, a.k.factor));
+                    }
+                }
+                continue;
+            }
             uint32_t nw = w;
             bool arrived = false;
             uint32_t group = 0;
@@ -373,7 +401,7 @@ __global__ void __launch_bounds__(NT) step_bits_kernel(const StepArgs a, int slo
             if (valid) {
                 cout[gi] = nw;
                 if (ACO) {
-                    double2 t = tin[gi];
+                    double2 t = tv[si - 1];
                     t.x = __dmul_rn(t.x, a.k.factor);
                     t.y = __dmul_rn(t.y, a.k.factor);
                     if (arrived) {
