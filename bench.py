@@ -215,10 +215,10 @@ def secondary_runs(steps):
         tot, ker = ens.time_steps(steps, kernel=True)
         b = alg_bytes(cfg.width, cfg.height, cfg.agents_per_side, "lem" if cfg.model == p.Model.Lem else "aco", reps)
         out[name] = {
-            "workload": desc, "ms_per_step": tot / steps, "kernel_ms": ker,
+            "workload": desc, "ms_per_step": tot / steps, "kernel_ms_isolated_launch_events": ker,
             "agent_updates_per_s": 2 * cfg.agents_per_side * reps * steps / (tot / 1e3),
             "cell_updates_per_s": cfg.width * cfg.height * reps * steps / (tot / 1e3),
-            "roofline_frac": b / (ker / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
+            "roofline_frac": b / (tot / steps / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
         }
         ens.close()
     return out
@@ -289,10 +289,16 @@ def run_gpu_arm(args):
     rep = eng.reports(min(args.steps, 1024))
     moved_local = int(rep["moved"].sum())
 
-    # dominant kernel: mean per-launch duration (CUDA events around each launch)
-    _, kernel_ms = eng.ctx.time_steps(min(args.steps, 20), kernel=True)
-    kernel_ms = max_over_ranks(kernel_ms)
+    # Dominant kernel (step_bits_kernel, one launch per step). At N=1 the timed
+    # region is exactly K back-to-back launches of it (CUDA graphs; the only
+    # other kernel is a 1-thread step-counter bump per 256 steps), so its mean
+    # duration is the event-timed region / K. Also recorded: events around
+    # each of 20 isolated launches (includes launch gaps), and at N>1 that is
+    # the kernel figure, since the timed region then includes the exchange.
+    _, kernel_ms_isolated = eng.ctx.time_steps(min(args.steps, 20), kernel=True)
+    kernel_ms_isolated = max_over_ranks(kernel_ms_isolated)
     eng.close()
+    kernel_ms = ms / args.steps if world == 1 else kernel_ms_isolated
 
     agents_total = 2 * n * reps
     value = agents_total * args.steps / (ms / 1e3)
@@ -320,8 +326,10 @@ def run_gpu_arm(args):
             "hbm_gbs_alg_step": bytes_step * args.steps / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "step_fused_kernel", "kernel_ms": kernel_ms,
-                         "alg_bytes_per_launch": bytes_launch},
+                         "kernel": "step_bits_kernel", "kernel_ms": kernel_ms,
+                         "kernel_ms_isolated_launch_events": kernel_ms_isolated,
+                         "alg_bytes_per_launch": bytes_launch,
+                         "alg_bytes_model": "LEM 8 B/cell; ACO 40 B/cell + 16 B/agent (SURVEY.md 8(d))"},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "setup_s": setup_s,
