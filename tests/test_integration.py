@@ -1,0 +1,51 @@
+"""Drop-in integration: the C++ shim (include/pedflow_gpu.hpp) driven by a
+run_scenario-style caller (tools/pedflow_gpu_demo.cpp), and the Python
+run_scenario mirror, against the golden anchors of the unmodified reference."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "tools", "pedflow_gpu_demo")
+
+
+def test_demo_binary_built_against_shim():
+    assert os.path.exists(DEMO), "build() should compile tools/pedflow_gpu_demo"
+    out = subprocess.run(["ldd", DEMO], capture_output=True, text=True).stdout
+    assert "libpedflow_b200.so" in out
+
+
+def test_demo_reports_config_error():
+    r = subprocess.run([DEMO, "lem", "100", "96", "10", "5"], capture_output=True, text=True)
+    assert r.returncode == 2 and "multiple of 16" in r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C1_lem_480_1024", "C2_aco_480_1024", "s96_aco_900_s11", "r48x32_aco_300_s9"])
+def test_cpp_dropin_matches_golden(anchors, name):
+    a = anchors[name]
+    sc = a["scenario"]
+    r = subprocess.run([DEMO, sc["model"], str(sc["width"]), str(sc["height"]), str(sc["agents_per_side"]),
+                        str(a["steps"]), str(sc.get("seed", 42))], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    moved, top, bot, h_index, h_occ = r.stdout.split()
+    assert (int(moved), int(top), int(bot)) == (a["sum_moved"], a["crossed_top"], a["crossed_bottom"])
+    assert (h_index, h_occ) == (a["hash"]["index"], a["hash"]["occ"])
+
+
+@pytest.mark.gpu
+def test_run_scenario_series_matches_golden(anchors):
+    import paper_1412_4933_b200 as p
+
+    a = anchors["C2_aco_480_1024"]
+    cfg = p.ScenarioConfig(width=480, height=480, agents_per_side=1024, model=p.Model.Aco, steps=a["steps"])
+    rr = p.run_scenario(cfg, 42)
+    ser = np.asarray(a["series"])
+    assert [s.moved for s in rr.series] == ser[:, 0].tolist()
+    assert rr.series[-1].crossed_top == int(ser[:, 1].sum())
+    assert rr.throughput == a["crossed_top"] + a["crossed_bottom"]
+    assert rr.agents_total == 2048 and rr.runtime_seconds > 0
