@@ -48,7 +48,8 @@ constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
 constexpr int QCAP = PF_BITS_QCAP;  // work-list capacity (overflow is handled in place)
 
 struct Smem {
-    uint32_t word[SR][SW];
+    uint32_t word[SR][SW];  // rows are 1,280 B: every row start is 16-byte aligned for TMA
+    unsigned long long mbar;
     uint32_t v30[SR][SS];
     uint32_t v31[SR][SS];
     uint32_t D[8][DROWS][SS];
@@ -61,6 +62,37 @@ struct Smem {
 };
 
 __device__ __forceinline__ uint32_t bit(uint32_t x, int j) { return (x >> j) & 1u; }
+
+// --- TMA bulk copy (cp.async.bulk) + mbarrier ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(m))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        "  .reg .pred done;\n"
+        "WAIT_%=:\n"
+        "  mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "  @!done bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
 
 // Value of a plane at column c-1 (shift in from the left segment) / c+1.
 __device__ __forceinline__ uint32_t from_left(uint32_t x, uint32_t left) { return (x << 1) | (left >> 31); }
@@ -219,32 +251,42 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     double* __restrict__ tour = ACO ? a.p.tour + base : nullptr;
 
     // ---------------------------------------------------------------- S0
+    // The staged rows arrive by TMA bulk copies (one cp.async.bulk per row,
+    // completion counted on one mbarrier); columns / rows outside the arena
+    // are filled with walls by the threads meanwhile.
+    const int col_lo = max(c0 - 32, 0), col_hi = min(c0 + 32 * (NS + 1), W);  // multiples of 16
+    const int fill_lo = col_lo - (c0 - 32), fill_hi = col_hi - (c0 - 32);      // staged column range
+    const int rows_valid = max(0, min(SR, a.rows_buf - (kGhost + r0 - 3)));
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.mbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) mbar_expect_tx(&sm.mbar, uint32_t(rows_valid) * uint32_t(fill_hi - fill_lo) * 4u);
+        __syncwarp();
+        for (int sr = lane; sr < rows_valid; sr += 32) {
+            const int b = kGhost + r0 - 3 + sr;
+            bulk_g2s(&sm.word[sr][fill_lo], cin + size_t(b) * W + col_lo, uint32_t(fill_hi - fill_lo) * 4u, &sm.mbar);
+        }
+    }
     for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
     if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0u;
     if (threadIdx.x == 0) sm.nq = 0u;
-    // Tiles away from the left/right edge need no per-lane column checks.
-    const bool interior = c0 >= 32 && c0 + 32 * (NS + 1) <= W;
+    if (fill_lo > 0 || fill_hi < SW)
+        for (int sr = warp; sr < rows_valid; sr += NW)
+            for (int c = lane; c < SW; c += 32)
+                if (c < fill_lo || c >= fill_hi) sm.word[sr][c] = kWall;
+    for (int i = rows_valid * SW + threadIdx.x; i < SR * SW; i += NT) (&sm.word[0][0])[i] = kWall;
+    mbar_wait(&sm.mbar, 0);
+    __syncthreads();
     for (int sr = warp; sr < SR; sr += NW) {
-        const int b = kGhost + r0 - 3 + sr;
-        const bool row_ok = b < a.rows_buf;
-        const uint32_t* src = cin + size_t(b) * W + (c0 - 32) + lane;
-        uint32_t w[SS];
-        if (row_ok && interior) {
-#pragma unroll
-            for (int si = 0; si < SS; ++si) w[si] = __ldg(src + 32 * si);
-        } else {
-#pragma unroll
-            for (int si = 0; si < SS; ++si) {
-                const int c = c0 + 32 * (si - 1) + lane;
-                w[si] = (row_ok && c >= 0 && c < W) ? __ldg(src + 32 * si) : kWall;
-            }
-        }
         uint32_t m30 = 0u, m31 = 0u;  // lane si keeps segment si's planes
 #pragma unroll
         for (int si = 0; si < SS; ++si) {
-            sm.word[sr][si * 32 + lane] = w[si];
-            const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w[si] << 1) < 0);
-            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w[si]) < 0);
+            const uint32_t w = sm.word[sr][si * 32 + lane];
+            const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w << 1) < 0);
+            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w) < 0);
             m30 = lane == si ? b30 : m30;
             m31 = lane == si ? b31 : m31;
         }
