@@ -1,16 +1,21 @@
 // Bit-sliced fused step kernel (the default product path, PF_KERNEL_FUSED).
 //
-// One CTA owns RT rows x NS 32-column segments of the grid. The per-step
-// update (StepEngine::step, src/engine.cpp:53-193) is evaluated on 32-cell
-// row segments held as 32-bit masks, so the common work costs one ALU op per
-// 32 cells; only agents that must draw (forward blocked, some slot open) and
-// destinations with >= 2 claimants fall to per-cell scalar code, and those are
-// compacted into shared-memory work lists so every lane of the CTA takes one.
+// The per-step update (StepEngine::step, src/engine.cpp:53-193) is evaluated
+// on 32-cell row segments held as 32-bit masks, so the common work costs one
+// ALU op per 32 cells; only agents that must draw (forward blocked, some slot
+// open) and destinations with >= 2 claimants fall to per-cell scalar code, and
+// those are compacted into shared-memory work lists so every lane takes one.
 //
-//   S0 stage   warp per segment-row, lane = column: load the step-start cell
-//              words (3-row / 1-segment halo) into shared memory and ballot
-//              them into occupancy planes v30 / v31 (bits 30/31 of the word:
-//              Top = v30 & ~v31, Bottom = v31 & ~v30, Empty = ~(v30 | v31)).
+// Persistent column sweep: a CTA owns a strip of NS 32-column segments and a
+// run of consecutive RT-row tiles. The step-start cell words of the strip live
+// in a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
+// rows); while a tile is processed, TMA bulk copies (cp.async.bulk +
+// mbarrier) bring the next tile's RT new rows, so every row is loaded and
+// balloted once and the load latency hides behind the compute.
+//
+//   S0 stage   ballot the new rows into occupancy planes v30 / v31 (bits 30/31
+//              of the word: Top = v30 & ~v31, Bottom = v31 & ~v30,
+//              Empty = ~(v30 | v31)).
 //   S1 intent  thread per segment-row: forward moves (F open, no draw,
 //              src/lem.cpp:23-26, src/aco.cpp:60-63) and boxed-in agents in
 //              bit logic; agents that must draw are queued, then run the
@@ -25,6 +30,8 @@
 //   S3 commit  warp per segment-row, lane = column: new cell word (arrival /
 //              vacate / unchanged), crossing + counters, ACO evaporation +
 //              deposit and tour (src/engine.cpp:124-175).
+#include <algorithm>
+
 #include "pf_internal.h"
 
 namespace pfk {
@@ -33,9 +40,10 @@ using namespace pfdev;
 
 namespace {
 
-constexpr int RT = 32;           // output rows per CTA
-constexpr int NS = 8;            // output 32-column segments per CTA
-constexpr int SR = RT + 6;       // staged rows: -3 .. RT+2
+constexpr int RT = 16;           // output rows per tile
+constexpr int NS = 8;            // output 32-column segments per strip
+constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
+constexpr int RING = SR + RT;    // ring slots: current window + next tile's new rows
 constexpr int SS = NS + 2;       // staged segments: -1 .. NS
 constexpr int SW = SS * 32;      // staged columns
 constexpr int NT = 256;          // threads per CTA
@@ -48,20 +56,25 @@ constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
 constexpr int QCAP = PF_BITS_QCAP;  // work-list capacity (overflow is handled in place)
 
 struct Smem {
-    uint32_t word[SR][SW];  // rows are 1,280 B: every row start is 16-byte aligned for TMA
-    unsigned long long mbar;
-    uint32_t v30[SR][SS];
-    uint32_t v31[SR][SS];
+    uint32_t word[RING][SW];  // rows are 1,280 B: every row start is 16-byte aligned for TMA
+    uint32_t v30[RING][SS];
+    uint32_t v31[RING][SS];
     uint32_t D[8][DROWS][SS];
     uint32_t A[AROWS][SS];
     uint32_t K[3][AROWS][SS];
     uint32_t G[RT][SS];
     uint32_t queue[QCAP];  // (unit << 5) | bit
+    unsigned long long mbar[2];
+    int item;
     uint32_t nq;
     uint32_t cnt[3];
 };
 
 __device__ __forceinline__ uint32_t bit(uint32_t x, int j) { return (x >> j) & 1u; }
+
+// Value of a plane at column c-1 (shift in from the left segment) / c+1.
+__device__ __forceinline__ uint32_t from_left(uint32_t x, uint32_t left) { return (x << 1) | (left >> 31); }
+__device__ __forceinline__ uint32_t from_right(uint32_t x, uint32_t right) { return (x >> 1) | (right << 31); }
 
 // --- TMA bulk copy (cp.async.bulk) + mbarrier ---------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -94,30 +107,33 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity
         : "memory");
 }
 
-// Value of a plane at column c-1 (shift in from the left segment) / c+1.
-__device__ __forceinline__ uint32_t from_left(uint32_t x, uint32_t left) { return (x << 1) | (left >> 31); }
-__device__ __forceinline__ uint32_t from_right(uint32_t x, uint32_t right) { return (x >> 1) | (right << 31); }
+// Ring slot of staged row sr (0 = tile row -3) for a window starting at base.
+__device__ __forceinline__ int slot(int base, int sr) {
+    const int s = base + sr;
+    return s >= RING ? s - RING : s;
+}
 
-// Emptiness around one intent unit (row di-2, segment si): the eight
-// neighbour planes, shifted so bit j is the neighbour of column j.
+// Emptiness around one intent unit: the eight neighbour planes, shifted so
+// bit j is the neighbour of column j.
 struct Around {
     uint32_t em, emL, emR, e0L, e0R, ep, epL, epR;
 };
 
-__device__ __forceinline__ Around around(const Smem& sm, int sr, int si) {
+__device__ __forceinline__ Around around(const Smem& sm, int base, int sr, int si) {
+    const int rm = slot(base, sr - 1), r0 = slot(base, sr), rp = slot(base, sr + 1);
     auto E = [&](int row, int seg) -> uint32_t {
         return (seg < 0 || seg >= SS) ? 0u : ~(sm.v30[row][seg] | sm.v31[row][seg]);
     };
     Around n;
-    n.em = E(sr - 1, si);
-    n.ep = E(sr + 1, si);
-    const uint32_t e0 = E(sr, si);
-    n.emL = from_left(n.em, E(sr - 1, si - 1));
-    n.emR = from_right(n.em, E(sr - 1, si + 1));
-    n.e0L = from_left(e0, E(sr, si - 1));
-    n.e0R = from_right(e0, E(sr, si + 1));
-    n.epL = from_left(n.ep, E(sr + 1, si - 1));
-    n.epR = from_right(n.ep, E(sr + 1, si + 1));
+    n.em = E(rm, si);
+    n.ep = E(rp, si);
+    const uint32_t e0 = E(r0, si);
+    n.emL = from_left(n.em, E(rm, si - 1));
+    n.emR = from_right(n.em, E(rm, si + 1));
+    n.e0L = from_left(e0, E(r0, si - 1));
+    n.e0R = from_right(e0, E(r0, si + 1));
+    n.epL = from_left(n.ep, E(rp, si - 1));
+    n.epR = from_right(n.ep, E(rp, si + 1));
     return n;
 }
 
@@ -175,10 +191,11 @@ __device__ __forceinline__ uint32_t enqueue(Smem& sm, int u, uint32_t mask) {
 // Intent of the draw-path agent at bit j of intent unit (di, si):
 // lem_select / aco_select (src/lem.cpp:28-60, src/aco.cpp:64-92).
 template <bool ACO>
-__device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, const double2* __restrict__ tin, int di,
-                                           int si, int j, bool bottom, int r0, int c0, uint64_t seed, uint32_t step) {
+__device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, int base,
+                                           const double2* __restrict__ tin, int di, int si, int j, bool bottom,
+                                           int r0, int c0, uint64_t seed, uint32_t step) {
     const int sr = di + 1;
-    const Around n = around(sm, sr, si);
+    const Around n = around(sm, base, sr, si);
     uint32_t open;  // goal-relative slots F FL FR L R B BL BR
     if (!bottom)
         open = bit(n.ep, j) | bit(n.epL, j) << 1 | bit(n.epR, j) << 2 | bit(n.e0L, j) << 3 | bit(n.e0R, j) << 4 |
@@ -186,7 +203,7 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, co
     else
         open = bit(n.em, j) | bit(n.emR, j) << 1 | bit(n.emL, j) << 2 | bit(n.e0R, j) << 3 | bit(n.e0L, j) << 4 |
                bit(n.ep, j) << 5 | bit(n.epR, j) << 6 | bit(n.epL, j) << 7;
-    const uint32_t id = sm.word[sr][si * 32 + j] & kIdMask;
+    const uint32_t id = sm.word[slot(base, sr)][si * 32 + j] & kIdMask;
     int s;
     if (!ACO) {
         s = lem_choose(a.kc, open, seed, step, id);
@@ -231,231 +248,280 @@ __device__ __forceinline__ void set_winner(Smem& sm, int ai, int si, int j, int 
     grant(sm, ai - 1, si, k, b);
 }
 
+// Issue the TMA loads of `nrows` staged rows (tile rows first_sr.., relative
+// to the tile at r0) into their ring slots, completing on mbarrier m. Rows
+// past the end of the buffer become walls. Called by one full warp.
+__device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, const uint32_t* cin, int r0, int c0, int base,
+                                          int first_sr, int nrows, int fill_lo, int fill_hi, int col_lo,
+                                          unsigned long long* m) {
+    const int lane = threadIdx.x & 31;
+    const int W = a.k.W;
+    const int b_first = kGhost + r0 - 3 + first_sr;
+    const int nvalid = max(0, min(nrows, a.rows_buf - b_first));
+    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(fill_hi - fill_lo) * 4u);
+    __syncwarp();
+    for (int i = lane; i < nvalid; i += 32)
+        bulk_g2s(&sm.word[slot(base, first_sr + i)][fill_lo], cin + size_t(b_first + i) * W + col_lo,
+                 uint32_t(fill_hi - fill_lo) * 4u, m);
+    for (int i = nvalid; i < nrows; ++i)
+        for (int c = lane; c < SW; c += 32) sm.word[slot(base, first_sr + i)][c] = kWall;
+}
+
 template <bool ACO>
-__global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int slot, int parity) {
+__global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
     const int W = a.k.W;
-    const int rep = blockIdx.z;
-    const int r0 = blockIdx.y * RT;         // owned-local row of the tile
-    const int c0 = blockIdx.x * (NS * 32);  // first owned column
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t step = *a.d_step + uint32_t(slot);
-    const uint64_t seed = a.seed_base + uint64_t(rep);
-    const size_t base = size_t(rep) * a.p.plane;
-    const uint32_t* __restrict__ cin = a.p.cell[parity] + base;
-    uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + base;
-    const double2* __restrict__ tin = ACO ? a.p.tau[parity] + base : nullptr;
-    double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + base : nullptr;
-    double* __restrict__ tour = ACO ? a.p.tour + base : nullptr;
+    const uint32_t step = *a.d_step + uint32_t(slot_idx);
+    const int strips = (W + NS * 32 - 1) / (NS * 32);
+    const int n_tiles = (a.rows_owned + RT - 1) / RT;
+    const int n_chunks = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
+    const int n_items = strips * n_chunks * a.replicas;
+    uint32_t* work = a.work + step % uint32_t(a.report_cap);
 
-    // ---------------------------------------------------------------- S0
-    // The staged rows arrive by TMA bulk copies (one cp.async.bulk per row,
-    // completion counted on one mbarrier); columns / rows outside the arena
-    // are filled with walls by the threads meanwhile.
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        fence_mbar_init();
+        sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
+    }
+    uint32_t moved = 0, ntop = 0, nbot = 0;
+    uint32_t nload = 0;  // loads issued by this CTA: load i completes mbar[i & 1], phase i >> 1
+    for (;;) {
+    // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
+    // taken from a per-step counter so heavy (crowded) chunks balance out.
+    __syncthreads();
+    if (threadIdx.x == 0) sm.item = int(atomicAdd(work, 1u));
+    __syncthreads();
+    const int item = sm.item;
+    if (item >= n_items) break;
+    const int rep = item / (strips * n_chunks);
+    const int strip = (item / n_chunks) % strips;
+    const int chunk = item % n_chunks;
+    const int c0 = strip * (NS * 32);  // first owned column of the strip
+    const int t_first = chunk * a.tiles_per_cta;
+    const int t_end = min(t_first + a.tiles_per_cta, n_tiles);
+    const uint64_t seed = a.seed_base + uint64_t(rep);
+    const size_t plane_base = size_t(rep) * a.p.plane;
+    const uint32_t* __restrict__ cin = a.p.cell[parity] + plane_base;
+    uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + plane_base;
+    const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
+    double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + plane_base : nullptr;
+    double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
+
+    // Columns of the strip outside the arena are walls in every ring slot.
     const int col_lo = max(c0 - 32, 0), col_hi = min(c0 + 32 * (NS + 1), W);  // multiples of 16
     const int fill_lo = col_lo - (c0 - 32), fill_hi = col_hi - (c0 - 32);      // staged column range
-    const int rows_valid = max(0, min(SR, a.rows_buf - (kGhost + r0 - 3)));
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.mbar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (warp == 0) {
-        if (lane == 0) mbar_expect_tx(&sm.mbar, uint32_t(rows_valid) * uint32_t(fill_hi - fill_lo) * 4u);
-        __syncwarp();
-        for (int sr = lane; sr < rows_valid; sr += 32) {
-            const int b = kGhost + r0 - 3 + sr;
-            bulk_g2s(&sm.word[sr][fill_lo], cin + size_t(b) * W + col_lo, uint32_t(fill_hi - fill_lo) * 4u, &sm.mbar);
-        }
-    }
-    for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
-    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0u;
-    if (threadIdx.x == 0) sm.nq = 0u;
     if (fill_lo > 0 || fill_hi < SW)
-        for (int sr = warp; sr < rows_valid; sr += NW)
-            for (int c = lane; c < SW; c += 32)
-                if (c < fill_lo || c >= fill_hi) sm.word[sr][c] = kWall;
-    for (int i = rows_valid * SW + threadIdx.x; i < SR * SW; i += NT) (&sm.word[0][0])[i] = kWall;
-    mbar_wait(&sm.mbar, 0);
-    __syncthreads();
-    for (int sr = warp; sr < SR; sr += NW) {
-        uint32_t m30 = 0u, m31 = 0u;  // lane si keeps segment si's planes
-#pragma unroll
-        for (int si = 0; si < SS; ++si) {
-            const uint32_t w = sm.word[sr][si * 32 + lane];
-            const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w << 1) < 0);
-            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w) < 0);
-            m30 = lane == si ? b30 : m30;
-            m31 = lane == si ? b31 : m31;
+        for (int i = threadIdx.x; i < RING * SW; i += NT) {
+            const int c = i % SW;
+            if (c < fill_lo || c >= fill_hi) (&sm.word[0][0])[i] = kWall;
         }
-        if (lane < SS) {
-            sm.v30[sr][lane] = m30;
-            sm.v31[sr][lane] = m31;
-        }
-    }
-    __syncthreads();
+    // First window: all SR staged rows of the first tile.
+    if (warp == 0) load_rows(sm, a, cin, t_first * RT, c0, 0, 0, SR, fill_lo, fill_hi, col_lo, &sm.mbar[nload & 1]);
+    ++nload;
+    __syncthreads();  // wall rows written by warp 0 are visible to all
 
-    // ---------------------------------------------------------------- S1
-    // Intents for rows -2 .. RT+1, all staged segments (halo segments only
-    // at the two columns next to the tile).
-    for (int u = threadIdx.x; u < DROWS * SS; u += NT) {
-        const int di = u / SS, si = u - di * SS;  // di = rr + 2
-        const int sr = di + 1;                    // staged row of rr
-        const Around n = around(sm, sr, si);
-        const uint32_t v30 = sm.v30[sr][si], v31 = sm.v31[sr][si];
-        const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
-        const uint32_t T = v30 & ~v31 & segmask, B = v31 & ~v30 & segmask;
-        uint32_t d[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) d[k] = 0u;
-        d[6] = T & n.ep;  // Top forward: (+1, 0)
-        d[1] = B & n.em;  // Bottom forward: (-1, 0)
-        const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
-        uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-        if (slow) slow = enqueue(sm, u, slow);
-        while (slow) {  // queue overflow: draw in place
-            const int j = __ffs(slow) - 1;
-            slow &= slow - 1u;
-            d[draw_intent<ACO>(a, sm, tin, di, si, j, bit(B, j) != 0u, r0, c0, seed, step)] |= 1u << j;
+    int base = 0;  // ring slot of staged row 0 of the current tile
+    for (int t = t_first; t < t_end; ++t) {
+        const int k = t - t_first;  // tile index within the item (k == 0: full window)
+        const int r0 = t * RT;      // owned-local row of the tile
+        const uint32_t my_load = nload - 1;  // the load that brought this tile's new rows
+        // Prefetch the next tile's RT new rows into the slots the previous
+        // tile released (all its readers passed the end-of-tile barrier).
+        if (t + 1 < t_end) {
+            if (warp == 0)
+                load_rows(sm, a, cin, r0 + RT, c0, slot(base, RT), 6, RT, fill_lo, fill_hi, col_lo,
+                          &sm.mbar[nload & 1]);
+            ++nload;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sm.D[k][di][si] = d[k];
-    }
-    __syncthreads();
-    {
-        const uint32_t nq = min(sm.nq, uint32_t(QCAP));
-        for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-            const uint32_t q = sm.queue[e];
-            const int u = int(q >> 5), j = int(q & 31u);
-            const int di = u / SS, si = u - di * SS;
-            const bool bottom = bit(sm.v31[di + 1][si], j) != 0u;
-            const int code = draw_intent<ACO>(a, sm, tin, di, si, j, bottom, r0, c0, seed, step);
-            atomicOr(&sm.D[code][di][si], 1u << j);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) sm.nq = 0u;
-    __syncthreads();
+        for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
+        if (threadIdx.x == 0) sm.nq = 0u;
+        mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
-    // ---------------------------------------------------------------- S2
-    // Claims, winners and grants for destinations in rows -1 .. RT.
-    for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
-        const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
-        uint32_t C[8];
-        claims(sm, ai, si, C);
-        uint32_t ones = 0u, twos = 0u;
+        // ------------------------------------------------------------ S0
+        for (int sr = (k == 0 ? 0 : 6) + warp; sr < SR; sr += NW) {
+            const int rs = slot(base, sr);
+            uint32_t m30 = 0u, m31 = 0u;  // lane si keeps segment si's planes
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            twos |= ones & C[k];
-            ones |= C[k];
-        }
-        uint32_t win[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) win[k] = C[k] & ~twos;
-        sm.A[ai][si] = ones;
-        sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
-        sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
-        sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (win[k]) grant(sm, ai - 1, si, k, win[k]);
-        uint32_t multi = twos ? enqueue(sm, u, twos) : 0u;
-        while (multi) {  // queue overflow: draw in place
-            const int j = __ffs(multi) - 1;
-            multi &= multi - 1u;
-            set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
-        }
-    }
-    __syncthreads();
-    {
-        const uint32_t nq = min(sm.nq, uint32_t(QCAP));
-        for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-            const uint32_t q = sm.queue[e];
-            const int u = int(q >> 5), j = int(q & 31u);
-            const int ai = u / SS, si = u - ai * SS;
-            set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
-        }
-    }
-    __syncthreads();
-
-    // ---------------------------------------------------------------- S3
-    uint32_t moved = 0, ntop = 0, nbot = 0;
-    for (int rr = warp; rr < RT; rr += NW) {
-        const int lr = r0 + rr;
-        if (lr >= a.rows_owned) break;
-        const int b = kGhost + lr;
-        const int grow = a.row_begin + lr;
-        const int sr = rr + 3, ai = rr + 1;
-        const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
-        // ACO: issue the whole row's pheromone loads before using any of them.
-        double2 tv[NS];
-        if (ACO) {
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-                tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int si = 1; si <= NS; ++si) {
-            const int gc = c0 + 32 * (si - 1) + lane;
-            const bool valid = gc < W;
-            const uint32_t Am = sm.A[ai][si], Gm = sm.G[rr][si];
-            const uint32_t w = sm.word[sr][si * 32 + lane];
-            const size_t gi = row0 + 32 * (si - 1);
-            if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
-                if (valid) {
-                    cout[gi] = w;
-                    if (ACO) {
-                        const double2 t = tv[si - 1];
-                        tout[gi] = make_double2(__dmul_rn(t.x, a.k.factor), __dmul_rn(t.y, a.k.factor));
-                    }
-                }
-                continue;
+            for (int si = 0; si < SS; ++si) {
+                const uint32_t w = sm.word[rs][si * 32 + lane];
+                const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w << 1) < 0);
+                const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w) < 0);
+                m30 = lane == si ? b30 : m30;
+                m31 = lane == si ? b31 : m31;
             }
-            uint32_t nw = w;
-            bool arrived = false;
-            uint32_t group = 0;
-            double tour_new = 0.0;
-            if (bit(Am, lane)) {
-                const int k = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                  bit(sm.K[2][ai][si], lane) << 2);
-                const uint32_t sw = sm.word[sr + kDR[k]][si * 32 + lane + kDC[k]];
-                group = sw >> 30;
-                nw = sw;
-                if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, a.k.band)) {
-                    nw |= kCrossedBit;
+            if (lane < SS) {
+                sm.v30[rs][lane] = m30;
+                sm.v31[rs][lane] = m31;
+            }
+        }
+        __syncthreads();
+
+        // ------------------------------------------------------------ S1
+        // Intents for rows -2 .. RT+1, all staged segments (halo segments
+        // only at the two columns next to the strip).
+        for (int u = threadIdx.x; u < DROWS * SS; u += NT) {
+            const int di = u / SS, si = u - di * SS;  // di = rr + 2
+            const int rs = slot(base, di + 1);
+            const Around n = around(sm, base, di + 1, si);
+            const uint32_t v30 = sm.v30[rs][si], v31 = sm.v31[rs][si];
+            const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
+            const uint32_t T = v30 & ~v31 & segmask, B = v31 & ~v30 & segmask;
+            uint32_t d[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) d[q] = 0u;
+            d[6] = T & n.ep;  // Top forward: (+1, 0)
+            d[1] = B & n.em;  // Bottom forward: (-1, 0)
+            const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
+            uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
+            if (slow) slow = enqueue(sm, u, slow);
+            while (slow) {  // queue overflow: draw in place
+                const int j = __ffs(slow) - 1;
+                slow &= slow - 1u;
+                d[draw_intent<ACO>(a, sm, base, tin, di, si, j, bit(B, j) != 0u, r0, c0, seed, step)] |= 1u << j;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sm.D[q][di][si] = d[q];
+        }
+        __syncthreads();
+        {
+            const uint32_t nq = min(sm.nq, uint32_t(QCAP));
+            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
+                const uint32_t q = sm.queue[e];
+                const int u = int(q >> 5), j = int(q & 31u);
+                const int di = u / SS, si = u - di * SS;
+                const bool bottom = bit(sm.v31[slot(base, di + 1)][si], j) != 0u;
+                const int code = draw_intent<ACO>(a, sm, base, tin, di, si, j, bottom, r0, c0, seed, step);
+                atomicOr(&sm.D[code][di][si], 1u << j);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) sm.nq = 0u;
+        __syncthreads();
+
+        // ------------------------------------------------------------ S2
+        // Claims, winners and grants for destinations in rows -1 .. RT.
+        for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
+            const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
+            uint32_t C[8];
+            claims(sm, ai, si, C);
+            uint32_t ones = 0u, twos = 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                twos |= ones & C[q];
+                ones |= C[q];
+            }
+            uint32_t win[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
+            sm.A[ai][si] = ones;
+            sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
+            sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
+            sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (win[q]) grant(sm, ai - 1, si, q, win[q]);
+            uint32_t multi = twos ? enqueue(sm, u, twos) : 0u;
+            while (multi) {  // queue overflow: draw in place
+                const int j = __ffs(multi) - 1;
+                multi &= multi - 1u;
+                set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
+            }
+        }
+        __syncthreads();
+        {
+            const uint32_t nq = min(sm.nq, uint32_t(QCAP));
+            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
+                const uint32_t q = sm.queue[e];
+                const int u = int(q >> 5), j = int(q & 31u);
+                const int ai = u / SS, si = u - ai * SS;
+                set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
+            }
+        }
+        __syncthreads();
+
+        // ------------------------------------------------------------ S3
+        for (int rr = warp; rr < RT; rr += NW) {
+            const int lr = r0 + rr;
+            if (lr >= a.rows_owned) break;
+            const int b = kGhost + lr;
+            const int grow = a.row_begin + lr;
+            const int rs = slot(base, rr + 3), ai = rr + 1;
+            const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
+            // ACO: issue the whole row's pheromone loads before using any of them.
+            double2 tv[NS];
+            if (ACO) {
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int si = 1; si <= NS; ++si) {
+                const int gc = c0 + 32 * (si - 1) + lane;
+                const bool valid = gc < W;
+                const uint32_t Am = sm.A[ai][si], Gm = sm.G[rr][si];
+                const uint32_t w = sm.word[rs][si * 32 + lane];
+                const size_t gi = row0 + 32 * (si - 1);
+                if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
                     if (valid) {
-                        if (group == 1u) ++ntop;
-                        else ++nbot;
+                        cout[gi] = w;
+                        if (ACO) {
+                            const double2 tt = tv[si - 1];
+                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+                        }
                     }
+                    continue;
                 }
-                arrived = true;
-                if (valid) ++moved;
-                if (ACO && valid) {
-                    const size_t si_src = size_t(b + kDR[k]) * W + (gc + kDC[k]);
-                    tour_new = __dadd_rn(tour[si_src], is_diag(k) ? a.k.diag : 1.0);
-                    tour[gi] = tour_new;
-                }
-            } else if (bit(Gm, lane)) {
-                nw = 0u;
-            }
-            if (valid) {
-                cout[gi] = nw;
-                if (ACO) {
-                    double2 t = tv[si - 1];
-                    t.x = __dmul_rn(t.x, a.k.factor);
-                    t.y = __dmul_rn(t.y, a.k.factor);
-                    if (arrived) {
-                        const double dep = __ddiv_rn(a.k.q, tour_new);
-                        if (group == 1u) t.x = __dadd_rn(t.x, dep);
-                        else t.y = __dadd_rn(t.y, dep);
+                uint32_t nw = w;
+                bool arrived = false;
+                uint32_t group = 0;
+                double tour_new = 0.0;
+                if (bit(Am, lane)) {
+                    const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
+                                       bit(sm.K[2][ai][si], lane) << 2);
+                    const uint32_t sw = sm.word[slot(base, rr + 3 + kDR[kc])][si * 32 + lane + kDC[kc]];
+                    group = sw >> 30;
+                    nw = sw;
+                    if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, a.k.band)) {  // src/engine.cpp:163-170
+                        nw |= kCrossedBit;
+                        if (valid) {
+                            if (group == 1u) ++ntop;
+                            else ++nbot;
+                        }
                     }
-                    tout[gi] = t;
+                    arrived = true;
+                    if (valid) ++moved;
+                    if (ACO && valid) {  // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
+                        const size_t si_src = size_t(b + kDR[kc]) * W + (gc + kDC[kc]);
+                        tour_new = __dadd_rn(tour[si_src], is_diag(kc) ? a.k.diag : 1.0);
+                        tour[gi] = tour_new;
+                    }
+                } else if (bit(Gm, lane)) {
+                    nw = 0u;
+                }
+                if (valid) {
+                    cout[gi] = nw;
+                    if (ACO) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
+                        double2 tt = tv[si - 1];
+                        tt.x = __dmul_rn(tt.x, a.k.factor);
+                        tt.y = __dmul_rn(tt.y, a.k.factor);
+                        if (arrived) {
+                            const double dep = __ddiv_rn(a.k.q, tour_new);
+                            if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
+                            else tt.y = __dadd_rn(tt.y, dep);
+                        }
+                        tout[gi] = tt;
+                    }
                 }
             }
         }
+        __syncthreads();  // end of tile: the window's slots may be refilled
+        base = slot(base, RT);
     }
+    // Counters of this item go to its replica's StepReport (src/engine.cpp:172-174).
     moved = __reduce_add_sync(0xFFFFFFFFu, moved);
     ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);
     nbot = __reduce_add_sync(0xFFFFFFFFu, nbot);
@@ -464,14 +530,17 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         atomicAdd(&sm.cnt[1], ntop);
         atomicAdd(&sm.cnt[2], nbot);
     }
+    moved = ntop = nbot = 0u;
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
-        if (blockIdx.x == 0 && blockIdx.y == 0) rep_slot[0] = step;
+        if (strip == 0 && chunk == 0) rep_slot[0] = step;
         if (sm.cnt[0]) atomicAdd(&rep_slot[1], sm.cnt[0]);
         if (sm.cnt[1]) atomicAdd(&rep_slot[2], sm.cnt[1]);
         if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
+        sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
     }
+    }  // work items
 }
 
 int configure_step_bits() {
@@ -483,11 +552,21 @@ int configure_step_bits() {
     return 0;
 }
 
-int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s) {
-    dim3 grid((a.k.W + NS * 32 - 1) / (NS * 32), (a.rows_owned + RT - 1) / RT, a.replicas);
+// Persistent grid: one CTA per (SM x 3) slot at most. Work items are chunks of
+// up to 16 consecutive RT-row tiles of one strip of one replica, sized so
+// there are about 4 items per CTA for load balance.
+int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
+    const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
+    const int n_tiles = (a.rows_owned + RT - 1) / RT;
+    const long long ctas_max = (long long)a.num_sms * 3;
+    const long long tiles = (long long)strips * n_tiles * a.replicas;
+    StepArgs b = a;
+    b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * 4))));
+    const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
+    dim3 grid(unsigned(std::min(items, ctas_max)));
     const size_t bytes = sizeof(Smem);
-    if (a.k.model == 1) step_bits_kernel<true><<<grid, NT, bytes, s>>>(a, slot, parity);
-    else step_bits_kernel<false><<<grid, NT, bytes, s>>>(a, slot, parity);
+    if (a.k.model == 1) step_bits_kernel<true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    else step_bits_kernel<false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
     return 1;
 }
 

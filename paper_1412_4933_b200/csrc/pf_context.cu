@@ -219,7 +219,13 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ok = ok && kc && cudaMemcpy(kc, &ctx->args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice) == cudaSuccess;
     ctx->args.kc = kc;
     ctx->d_reports = static_cast<uint32_t*>(alloc(size_t(cfg->replicas) * kReportCap * 16));
-    if (!ok || !ctx->d_step || !ctx->d_reports) {
+    ctx->args.work = static_cast<uint32_t*>(alloc(size_t(kReportCap) * 4));
+    {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+        ctx->args.num_sms = sms > 0 ? sms : 148;
+    }
+    if (!ok || !ctx->d_step || !ctx->d_reports || !ctx->args.work) {
         cudaGetLastError();
         return cleanup(fail(PF_ERR_CUDA, "device allocation failed (out of memory?)"));
     }
@@ -453,6 +459,7 @@ static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
         const uint32_t m = std::min<uint32_t>(n - done, kReportCap - slot);
         PF_CUDA(cudaMemset2DAsync(reinterpret_cast<char*>(ctx->d_reports) + size_t(slot) * 16, pitch, 0,
                                   size_t(m) * 16, size_t(ctx->cfg.replicas), ctx->stream));
+        PF_CUDA(cudaMemsetAsync(ctx->args.work + slot, 0, size_t(m) * 4, ctx->stream));  // work-item counters
         done += m;
     }
     return PF_OK;

@@ -37,6 +37,9 @@ struct StepArgs {
     int rows_owned;
     int rows_buf;           // rows_owned + 2 * kGhost
     int replicas;
+    int tiles_per_cta;      // bit kernel: consecutive row tiles per work item (set at launch)
+    uint32_t* work;         // bit kernel: per-step work-item counters, ring slot = step % report_cap
+    int num_sms;
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
