@@ -342,20 +342,29 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
         // ------------------------------------------------------------ S0
-        for (int sr = (k == 0 ? 0 : 6) + warp; sr < SR; sr += NW) {
-            const int rs = slot(base, sr);
-            uint32_t m30 = 0u, m31 = 0u;  // lane si keeps segment si's planes
+        // Thread per new segment-row: eight 16-byte shared loads (chunk order
+        // rotated by lane, so a quarter-warp hits eight distinct bank groups),
+        // the top byte of each word packed with PRMT, bits 31 / 30 of four
+        // words gathered into a nibble by one multiply.
+        {
+            const int first = k == 0 ? 0 : 6;
+            for (int u = threadIdx.x; u < (SR - first) * SS; u += NT) {
+                const int sr = first + u / SS, si = u % SS;
+                const int rs = slot(base, sr);
+                const uint4* p = reinterpret_cast<const uint4*>(&sm.word[rs][si * 32]);
+                uint32_t v30 = 0u, v31 = 0u;
 #pragma unroll
-            for (int si = 0; si < SS; ++si) {
-                const uint32_t w = sm.word[rs][si * 32 + lane];
-                const uint32_t b30 = __ballot_sync(0xFFFFFFFFu, int32_t(w << 1) < 0);
-                const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, int32_t(w) < 0);
-                m30 = lane == si ? b30 : m30;
-                m31 = lane == si ? b31 : m31;
-            }
-            if (lane < SS) {
-                sm.v30[rs][lane] = m30;
-                sm.v31[rs][lane] = m31;
+                for (int i = 0; i < 8; ++i) {
+                    const int c = (i + lane) & 7;
+                    const uint4 q = p[c];
+                    const uint32_t top = __byte_perm(__byte_perm(q.x, q.y, 0x0073), __byte_perm(q.z, q.w, 0x0073), 0x5410);
+                    const uint32_t n31 = ((top & 0x80808080u) * 0x00204081u) >> 28;
+                    const uint32_t n30 = (((top & 0x40404040u) * 0x00204081u) >> 27) & 0xFu;
+                    v31 |= n31 << (4 * c);
+                    v30 |= n30 << (4 * c);
+                }
+                sm.v30[rs][si] = v30;
+                sm.v31[rs][si] = v31;
             }
         }
         __syncthreads();
