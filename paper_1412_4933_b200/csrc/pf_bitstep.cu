@@ -570,7 +570,7 @@ int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s
     const long long ctas_max = (long long)a.num_sms * 3;
     const long long tiles = (long long)strips * n_tiles * a.replicas;
     StepArgs b = a;
-    b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * 4))));
+    b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
     dim3 grid(unsigned(std::min(items, ctas_max)));
     const size_t bytes = sizeof(Smem);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <functional>
@@ -224,6 +225,8 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
         ctx->args.num_sms = sms > 0 ? sms : 148;
+        const char* ipc = std::getenv("PEDFLOW_ITEMS_PER_CTA");  // tuning override (dev)
+        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : 4;
     }
     if (!ok || !ctx->d_step || !ctx->d_reports || !ctx->args.work) {
         cudaGetLastError();

@@ -40,6 +40,7 @@ struct StepArgs {
     int tiles_per_cta;      // bit kernel: consecutive row tiles per work item (set at launch)
     uint32_t* work;         // bit kernel: per-step work-item counters, ring slot = step % report_cap
     int num_sms;
+    int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
