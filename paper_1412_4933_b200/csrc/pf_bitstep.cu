@@ -43,9 +43,16 @@ namespace {
 constexpr int RT = 16;           // output rows per tile
 constexpr int NS = 8;            // output 32-column segments per strip
 constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
-constexpr int RING = SR + RT;    // ring slots: current window + next tile's new rows
+constexpr int RING = 2 * SR;     // ring slots: current window + the next tile's rows or the next item's window
 constexpr int SS = NS + 2;       // staged segments: -1 .. NS
-constexpr int SW = SS * 32;      // staged columns
+// Staged columns: the strip plus a 4-column halo on each side (the dependency
+// radius is 3; 4 keeps TMA rows 16-byte aligned). Bit j of plane segment si
+// (si = 0 .. NS+1, segment si-1 of the strip) is staged column
+// 32 * si + j - WOFF; the halo segments 0 and NS+1 only have bits 28..31 and
+// 0..3 staged.
+constexpr int HALO = 4;
+constexpr int SW = NS * 32 + 2 * HALO;
+constexpr int WOFF = 32 - HALO;
 constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
@@ -56,13 +63,14 @@ constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
 constexpr int QCAP = PF_BITS_QCAP;  // work-list capacity (overflow is handled in place)
 
 struct Smem {
-    uint32_t word[RING][SW];  // rows are 1,280 B: every row start is 16-byte aligned for TMA
+    uint32_t word[RING][SW];  // rows are 1,056 B: every row start is 16-byte aligned for TMA
     uint32_t v30[RING][SS];
     uint32_t v31[RING][SS];
     uint32_t D[8][DROWS][SS];
     uint32_t A[AROWS][SS];
     uint32_t K[3][AROWS][SS];
     uint32_t G[RT][SS];
+    uint32_t dirty[RT];  // owned row has an arrival or a vacate
     uint32_t queue[QCAP];  // (unit << 5) | bit
     unsigned long long mbar[2];
     int item;
@@ -159,6 +167,7 @@ __device__ __forceinline__ void claims(const Smem& sm, int ai, int si, uint32_t 
 __device__ __forceinline__ void grant(Smem& sm, int rr, int si, int k, uint32_t wk) {
     const int g = rr + kDR[k];
     if (g < 0 || g >= RT) return;
+    sm.dirty[g] = 1u;
     const int dc = kDC[k];
     if (dc == 0) {
         atomicOr(&sm.G[g][si], wk);
@@ -203,7 +212,7 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
     else
         open = bit(n.em, j) | bit(n.emR, j) << 1 | bit(n.emL, j) << 2 | bit(n.e0R, j) << 3 | bit(n.e0L, j) << 4 |
                bit(n.ep, j) << 5 | bit(n.epR, j) << 6 | bit(n.epL, j) << 7;
-    const uint32_t id = sm.word[slot(base, sr)][si * 32 + j] & kIdMask;
+    const uint32_t id = sm.word[slot(base, sr)][si * 32 + j - WOFF] & kIdMask;
     int s;
     if (!ACO) {
         s = lem_choose(a.kc, open, seed, step, id);
@@ -248,21 +257,51 @@ __device__ __forceinline__ void set_winner(Smem& sm, int ai, int si, int j, int 
     grant(sm, ai - 1, si, k, b);
 }
 
+// One work item: a chunk of consecutive RT-row tiles of one strip of one
+// replica, with the strip's column window.
+struct Item {
+    int rep, strip, chunk, c0, t_first, t_end;
+    int col_lo, fill_lo, fill_hi;  // arena columns [col_lo, ...) land in staged columns [fill_lo, fill_hi)
+};
+
+__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
+                                            int W) {
+    Item it;
+    it.rep = item / (strips * n_chunks);
+    it.strip = (item / n_chunks) % strips;
+    it.chunk = item % n_chunks;
+    it.c0 = it.strip * (NS * 32);
+    it.t_first = it.chunk * tiles_per_item;
+    it.t_end = min(it.t_first + tiles_per_item, n_tiles);
+    it.col_lo = max(it.c0 - HALO, 0);
+    const int col_hi = min(it.c0 + 32 * NS + HALO, W);  // 16-byte aligned: c0 % 256 == 0, W % 16 == 0
+    it.fill_lo = it.col_lo - (it.c0 - HALO);
+    it.fill_hi = col_hi - (it.c0 - HALO);
+    return it;
+}
+
 // Issue the TMA loads of `nrows` staged rows (tile rows first_sr.., relative
-// to the tile at r0) into their ring slots, completing on mbarrier m. Rows
-// past the end of the buffer become walls. Called by one full warp.
-__device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, const uint32_t* cin, int r0, int c0, int base,
-                                          int first_sr, int nrows, int fill_lo, int fill_hi, int col_lo,
-                                          unsigned long long* m) {
+// to the tile at r0) of item `it` into their ring slots, completing on
+// mbarrier m; the strip's columns outside the arena and rows past the end of
+// the buffer are written as walls. Called by one full warp.
+__device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parity, const Item& it, int r0, int base,
+                                          int first_sr, int nrows, unsigned long long* m) {
     const int lane = threadIdx.x & 31;
     const int W = a.k.W;
+    const uint32_t* cin = a.p.cell[parity] + size_t(it.rep) * a.p.plane;
     const int b_first = kGhost + r0 - 3 + first_sr;
     const int nvalid = max(0, min(nrows, a.rows_buf - b_first));
-    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(fill_hi - fill_lo) * 4u);
+    const int ncols = it.fill_hi - it.fill_lo;
+    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(ncols) * 4u);
     __syncwarp();
     for (int i = lane; i < nvalid; i += 32)
-        bulk_g2s(&sm.word[slot(base, first_sr + i)][fill_lo], cin + size_t(b_first + i) * W + col_lo,
-                 uint32_t(fill_hi - fill_lo) * 4u, m);
+        bulk_g2s(&sm.word[slot(base, first_sr + i)][it.fill_lo], cin + size_t(b_first + i) * W + it.col_lo,
+                 uint32_t(ncols) * 4u, m);
+    const int nfill = SW - ncols;  // wall columns at the arena's left / right edge
+    for (int i = lane; i < nvalid * nfill; i += 32) {
+        const int r = i / nfill, c = i - r * nfill;
+        sm.word[slot(base, first_sr + r)][c < it.fill_lo ? c : it.fill_hi + (c - it.fill_lo)] = kWall;
+    }
     for (int i = nvalid; i < nrows; ++i)
         for (int c = lane; c < SW; c += 32) sm.word[slot(base, first_sr + i)][c] = kWall;
 }
@@ -287,57 +326,62 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         fence_mbar_init();
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
     }
-    uint32_t moved = 0, ntop = 0, nbot = 0;
-    uint32_t nload = 0;  // loads issued by this CTA: load i completes mbar[i & 1], phase i >> 1
-    for (;;) {
+    __syncthreads();
     // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
     // taken from a per-step counter so heavy (crowded) chunks balance out.
-    __syncthreads();
-    if (threadIdx.x == 0) sm.item = int(atomicAdd(work, 1u));
-    __syncthreads();
-    const int item = sm.item;
-    if (item >= n_items) break;
-    const int rep = item / (strips * n_chunks);
-    const int strip = (item / n_chunks) % strips;
-    const int chunk = item % n_chunks;
-    const int c0 = strip * (NS * 32);  // first owned column of the strip
-    const int t_first = chunk * a.tiles_per_cta;
-    const int t_end = min(t_first + a.tiles_per_cta, n_tiles);
+    // The next item is claimed during the current item's last tile and its
+    // first window is loaded into the other half of the ring meanwhile.
+    int item = 0;
+    if (warp == 0) {
+        if (lane == 0) item = int(atomicAdd(work, 1u));
+        item = __shfl_sync(0xFFFFFFFFu, item, 0);
+        if (lane == 0) sm.item = item;
+        if (item < n_items) {
+            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+            load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
+        }
+    }
+    __syncthreads();  // item id and wall rows written by warp 0 are visible to all
+    item = sm.item;
+    uint32_t moved = 0, ntop = 0, nbot = 0;
+    uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
+    int base = 0;                               // ring slot of staged row 0 of the current tile
+    while (item < n_items) {
+    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+    const int rep = it.rep, c0 = it.c0;
     const uint64_t seed = a.seed_base + uint64_t(rep);
     const size_t plane_base = size_t(rep) * a.p.plane;
-    const uint32_t* __restrict__ cin = a.p.cell[parity] + plane_base;
     uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + plane_base;
     const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
     double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + plane_base : nullptr;
     double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
+    int next_base = 0;
 
-    // Columns of the strip outside the arena are walls in every ring slot.
-    const int col_lo = max(c0 - 32, 0), col_hi = min(c0 + 32 * (NS + 1), W);  // multiples of 16
-    const int fill_lo = col_lo - (c0 - 32), fill_hi = col_hi - (c0 - 32);      // staged column range
-    if (fill_lo > 0 || fill_hi < SW)
-        for (int i = threadIdx.x; i < RING * SW; i += NT) {
-            const int c = i % SW;
-            if (c < fill_lo || c >= fill_hi) (&sm.word[0][0])[i] = kWall;
-        }
-    // First window: all SR staged rows of the first tile.
-    if (warp == 0) load_rows(sm, a, cin, t_first * RT, c0, 0, 0, SR, fill_lo, fill_hi, col_lo, &sm.mbar[nload & 1]);
-    ++nload;
-    __syncthreads();  // wall rows written by warp 0 are visible to all
-
-    int base = 0;  // ring slot of staged row 0 of the current tile
-    for (int t = t_first; t < t_end; ++t) {
-        const int k = t - t_first;  // tile index within the item (k == 0: full window)
-        const int r0 = t * RT;      // owned-local row of the tile
+    for (int t = it.t_first; t < it.t_end; ++t) {
+        const int k = t - it.t_first;  // tile index within the item (k == 0: full window)
+        const int r0 = t * RT;         // owned-local row of the tile
         const uint32_t my_load = nload - 1;  // the load that brought this tile's new rows
-        // Prefetch the next tile's RT new rows into the slots the previous
-        // tile released (all its readers passed the end-of-tile barrier).
-        if (t + 1 < t_end) {
-            if (warp == 0)
-                load_rows(sm, a, cin, r0 + RT, c0, slot(base, RT), 6, RT, fill_lo, fill_hi, col_lo,
-                          &sm.mbar[nload & 1]);
+        // Prefetch into the half of the ring this tile does not use (its
+        // previous readers all passed the end-of-tile barrier): the next
+        // tile's RT new rows, or on the last tile the next item's window.
+        if (t + 1 < it.t_end) {
+            if (warp == 0) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
             ++nload;
+        } else {
+            next_base = slot(base, SR);
+            if (warp == 0) {
+                int nx = 0;
+                if (lane == 0) nx = int(atomicAdd(work, 1u));
+                nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
+                if (lane == 0) sm.item = nx;
+                if (nx < n_items) {
+                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+                    load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
+                }
+            }
         }
         for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
+        if (threadIdx.x < RT) sm.dirty[threadIdx.x] = 0u;
         if (threadIdx.x == 0) sm.nq = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
@@ -351,17 +395,29 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             for (int u = threadIdx.x; u < (SR - first) * SS; u += NT) {
                 const int sr = first + u / SS, si = u % SS;
                 const int rs = slot(base, sr);
-                const uint4* p = reinterpret_cast<const uint4*>(&sm.word[rs][si * 32]);
+                auto nibbles = [](const uint4& q, uint32_t& n30, uint32_t& n31) {
+                    const uint32_t top =
+                        __byte_perm(__byte_perm(q.x, q.y, 0x0073), __byte_perm(q.z, q.w, 0x0073), 0x5410);
+                    n31 = ((top & 0x80808080u) * 0x00204081u) >> 28;
+                    n30 = (((top & 0x40404040u) * 0x00204081u) >> 27) & 0xFu;
+                };
                 uint32_t v30 = 0u, v31 = 0u;
+                if (si == 0 || si == SS - 1) {  // halo segment: 4 staged columns, the rest walls
+                    const bool left = si == 0;
+                    uint32_t n30, n31;
+                    nibbles(*reinterpret_cast<const uint4*>(&sm.word[rs][left ? 0 : SW - HALO]), n30, n31);
+                    v30 = left ? (0x0FFFFFFFu | n30 << 28) : (0xFFFFFFF0u | n30);
+                    v31 = left ? (0x0FFFFFFFu | n31 << 28) : (0xFFFFFFF0u | n31);
+                } else {
+                    const uint4* p = reinterpret_cast<const uint4*>(&sm.word[rs][si * 32 - WOFF]);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int c = (i + lane) & 7;
-                    const uint4 q = p[c];
-                    const uint32_t top = __byte_perm(__byte_perm(q.x, q.y, 0x0073), __byte_perm(q.z, q.w, 0x0073), 0x5410);
-                    const uint32_t n31 = ((top & 0x80808080u) * 0x00204081u) >> 28;
-                    const uint32_t n30 = (((top & 0x40404040u) * 0x00204081u) >> 27) & 0xFu;
-                    v31 |= n31 << (4 * c);
-                    v30 |= n30 << (4 * c);
+                    for (int i = 0; i < 8; ++i) {
+                        const int c = (i + lane) & 7;
+                        uint32_t n30, n31;
+                        nibbles(p[c], n30, n31);
+                        v31 |= n31 << (4 * c);
+                        v30 |= n30 << (4 * c);
+                    }
                 }
                 sm.v30[rs][si] = v30;
                 sm.v31[rs][si] = v31;
@@ -427,6 +483,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
 #pragma unroll
             for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
             sm.A[ai][si] = ones;
+            if (ones && ai >= 1 && ai <= RT) sm.dirty[ai - 1] = 1u;
             sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
             sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
             sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
@@ -459,6 +516,18 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             const int b = kGhost + lr;
             const int grow = a.row_begin + lr;
             const int rs = slot(base, rr + 3), ai = rr + 1;
+            if (!ACO && !sm.dirty[rr]) {
+                // Nothing arrives or leaves in this row: copy its 256 words
+                // with 16-byte shared loads / global stores (lane = 4 columns).
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = 128 * h + 4 * lane;
+                    if (c0 + col < W)  // W is a multiple of 16: a 4-word group is all in or all out
+                        *reinterpret_cast<uint4*>(cout + size_t(b) * W + c0 + col) =
+                            *reinterpret_cast<const uint4*>(&sm.word[rs][HALO + col]);
+                }
+                continue;
+            }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
             // ACO: issue the whole row's pheromone loads before using any of them.
             double2 tv[NS];
@@ -472,7 +541,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 const int gc = c0 + 32 * (si - 1) + lane;
                 const bool valid = gc < W;
                 const uint32_t Am = sm.A[ai][si], Gm = sm.G[rr][si];
-                const uint32_t w = sm.word[rs][si * 32 + lane];
+                const uint32_t w = sm.word[rs][si * 32 + lane - WOFF];
                 const size_t gi = row0 + 32 * (si - 1);
                 if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
                     if (valid) {
@@ -491,7 +560,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 if (bit(Am, lane)) {
                     const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
                                        bit(sm.K[2][ai][si], lane) << 2);
-                    const uint32_t sw = sm.word[slot(base, rr + 3 + kDR[kc])][si * 32 + lane + kDC[kc]];
+                    const uint32_t sw = sm.word[slot(base, rr + 3 + kDR[kc])][si * 32 + lane + kDC[kc] - WOFF];
                     group = sw >> 30;
                     nw = sw;
                     if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, a.k.band)) {  // src/engine.cpp:163-170
@@ -530,6 +599,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         __syncthreads();  // end of tile: the window's slots may be refilled
         base = slot(base, RT);
     }
+    base = next_base;
     // Counters of this item go to its replica's StepReport (src/engine.cpp:172-174).
     moved = __reduce_add_sync(0xFFFFFFFFu, moved);
     ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);
@@ -543,12 +613,14 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
-        if (strip == 0 && chunk == 0) rep_slot[0] = step;
+        if (it.strip == 0 && it.chunk == 0) rep_slot[0] = step;
         if (sm.cnt[0]) atomicAdd(&rep_slot[1], sm.cnt[0]);
         if (sm.cnt[1]) atomicAdd(&rep_slot[2], sm.cnt[1]);
         if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
     }
+    item = sm.item;  // claimed during the last tile (visible after its barriers)
+    if (item < n_items) ++nload;
     }  // work items
 }
 

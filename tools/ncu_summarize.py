@@ -31,8 +31,12 @@ KEYS = [
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
 ]
 
-PHASES = ["S0 stage (loads + ballots)", "S1 intents (bit logic + enqueue)", "S1 draw queue", "queue reset",
-          "S2 claims/winners/grants", "S2 contested-cell draws", "S3 commit (+ACO pheromone)", "counter reduction"]
+# SASS between consecutive BAR.SYNCs of step_bits_kernel, in address order;
+# the noinline draw functions (lem_choose / aco_choose / AS241) sit after EXIT.
+PHASES = ["prologue (mbarrier init)", "work-item fetch", "item setup + first-window TMA",
+          "tile start: TMA prefetch/wait + S0 planes", "S1 intents (bit logic + enqueue)", "S1 draw queue",
+          "queue reset", "S2 claims/winners/grants", "S2 contested-cell draws", "S3 commit (+ACO pheromone)",
+          "per-item counter flush", "draw functions (lem_choose/aco_choose/AS241)"]
 
 
 def raw(rep):
