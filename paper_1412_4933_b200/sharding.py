@@ -49,10 +49,35 @@ class HaloExchanger:
     ghost rows to fill.
     """
 
-    def __init__(self, rank: int, world: int, group=None):
+    def __init__(self, rank: int, world: int, group=None, staged: bool = False):
         self.rank, self.world, self.group = rank, world, group
+        # staged: device tensors travel through host copies (for backends such as
+        # gloo that move only CPU tensors, e.g. two ranks sharing one GPU in tests).
+        self.staged = staged
 
     def exchange(self, planes) -> None:
+        if self.staged:
+            self._exchange_staged(planes)
+            return
+        self._exchange(planes)
+
+    def _exchange_staged(self, planes) -> None:
+        host = {}
+
+        def staged_planes(side, recv):
+            out = []
+            for t in planes(side, recv):
+                h = t.to("cpu") if not recv else t.new_empty(t.shape, device="cpu")
+                host.setdefault((side, recv), []).append((t, h))
+                out.append(h)
+            return out
+
+        self._exchange(staged_planes)
+        for side in (0, 1):
+            for dev, h in host.get((side, True), []):
+                dev.copy_(h)
+
+    def _exchange(self, planes) -> None:
         import torch.distributed as dist
 
         ops = []
@@ -105,7 +130,12 @@ class ShardedEngine:
                                            row_begin=0 if whole else self.lo, row_end=0 if whole else self.hi,
                                            device=self.device, kernel=kernel))
         self.ctx.init_environment()
-        self.exchanger = HaloExchanger(rank, world, group)
+        staged = False
+        if world > 1:
+            import torch.distributed as dist
+
+            staged = dist.get_backend(group) != "nccl"
+        self.exchanger = HaloExchanger(rank, world, group, staged=staged)
         self._tcache: dict = {}
         self._stream = torch.cuda.ExternalStream(self.ctx.stream(), device=f"cuda:{self.device}")
 
@@ -130,8 +160,13 @@ class ShardedEngine:
         for _ in range(n):
             self.ctx.step_async(1)
             if self.world > 1:
-                with torch.cuda.stream(self._stream):
+                if self.exchanger.staged:
+                    self.ctx.synchronize()  # host copies follow the kernel
                     self.exchanger.exchange(self._planes)
+                    torch.cuda.synchronize(self.device)
+                else:
+                    with torch.cuda.stream(self._stream):
+                        self.exchanger.exchange(self._planes)
 
     def reports(self, n: int) -> np.ndarray:
         """This shard's [replicas][n] reports of the last n steps (sum over ranks

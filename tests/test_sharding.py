@@ -196,3 +196,76 @@ def test_gpu_multishard_one_device(model, nshards):
         assert (ag["crossed"] == ref.agents["crossed"]).all()
         if tt is not None:
             assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
+
+
+def _gpu_rank_main(rank, world, port, kw, steps, out_q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.sharding import ShardedEngine
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        model = kw.pop("model")
+        cfg = p.ScenarioConfig(model=p.Model.Lem if model == "lem" else p.Model.Aco, **kw)
+        eng = ShardedEngine(cfg, rank, world, device=0, replicas=2)
+        eng.step(steps)
+        rep = eng.reports(steps)
+        H, W = cfg.height, cfg.width
+        res = []
+        for r in range(2):
+            occ = np.zeros((H, W), np.uint8)
+            idx = np.zeros((H, W), np.uint32)
+            ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+            tt = np.zeros((H, W)) if model == "aco" else None
+            tb = np.zeros((H, W)) if model == "aco" else None
+            eng.store(r, occ, idx, ag, tt, tb)
+            res.append((occ, idx, ag, tt, tb))
+        out_q.put((rank, eng.lo, eng.hi, rep, res))
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_gpu_sharded_engine_two_ranks_one_device(model):
+    """The N>1 product path (ShardedEngine: per-step halo swap through the
+    exchanger, halo ranges from pf_halo, parity handling) with 2 ranks sharing
+    cuda:0 over gloo (host-staged exchange), against the unsharded run."""
+    import torch.multiprocessing as mp
+
+    import paper_1412_4933_b200 as p
+
+    kw = dict(width=96, height=96, agents_per_side=1500, model=model, seed=21)
+    steps, world = 60, 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_rank_main, args=(r, world, port, dict(kw), steps, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    cfg = p.ScenarioConfig(width=96, height=96, agents_per_side=1500,
+                           model=p.Model.Lem if model == "lem" else p.Model.Aco, seed=21)
+    whole = p.Ensemble(cfg, replicas=2, seed=21)
+    whole_rep = whole.run(steps)
+    tot = sum(r[3]["moved"].astype(np.int64) for r in results)
+    assert (tot == whole_rep["moved"]).all()
+    for rep_i in range(2):
+        ref = whole.state(rep_i)
+        for rank, lo, hi, _, res in results:
+            occ, idx, ag, tt, tb = res[rep_i]
+            assert (idx[lo:hi] == ref.index[lo:hi]).all(), f"rank {rank} index differs"
+            assert (occ[lo:hi] == ref.occupancy[lo:hi]).all()
+            if tt is not None:
+                assert (tt[lo:hi] == ref.pheromone_top[lo:hi]).all()
+                assert (tb[lo:hi] == ref.pheromone_bottom[lo:hi]).all()
