@@ -349,10 +349,9 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     PF_CUDA(cudaSetDevice(c.device));
     const size_t W = size_t(c.width);
     std::vector<uint32_t> words(ctx->plane(), 0u);
-    std::vector<double> tour(ctx->aco() ? ctx->plane() : 0, 0.0);
-    std::vector<double2> tau(ctx->aco() ? ctx->plane() : 0, make_double2(0.0, 0.0));
     // check_consistency-style audit (src/state.cpp:77-110) + conversion to
-    // cell words, parallel over buffer rows.
+    // cell words, parallel over buffer rows. Tour lengths and pheromone go up
+    // in the reference's own layout and are rearranged on the device.
     std::atomic<int> bad{0};  // 0 ok, else index into kWhy
     static const char* kWhy[] = {"", "state corrupt: index/occupancy mismatch", "state corrupt: index out of agent range",
                                  "state corrupt: agent record id mismatch",
@@ -369,7 +368,6 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
             for (size_t col = 0; col < W; ++col) {
                 const size_t gi = size_t(g) * W + col;
                 const uint32_t id = index[gi];
-                if (ctx->aco()) tau[b * W + col] = make_double2(tau_top[gi], tau_bot[gi]);
                 int why = 0;
                 if ((id == 0) != (occ[gi] == 0)) why = 1;
                 else if (id == 0) continue;
@@ -381,7 +379,6 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
                     else if (a.group != occ[gi] || (a.group != 1 && a.group != 2)) why = 5;
                     else {
                         wrow[col] = id | (a.crossed ? pfdev::kCrossedBit : 0u) | (uint32_t(a.group) << 30);
-                        if (ctx->aco()) tour[b * W + col] = a.tour_length;
                     }
                 }
                 if (why) {
@@ -393,7 +390,39 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
         }
     });
     if (bad.load()) return fail(PF_ERR_STATE, kWhy[bad.load()]);
-    if (int rc = upload_replica(ctx, rep, words, ctx->aco() ? &tour : nullptr, ctx->aco() ? &tau : nullptr)) return rc;
+    const size_t off = size_t(rep) * ctx->plane();
+    pfk::Planes& P = ctx->args.p;
+    PF_CUDA(cudaMemcpyAsync(P.cell[0] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->aco()) {
+        // Pheromone: the two reference planes (the rows present in this
+        // buffer) land in the second ping-pong buffer used as scratch, then
+        // are interleaved into {top, bottom} pairs on the device.
+        const int64_t g_lo = std::max<int64_t>(0, grow_of(ctx, 0));
+        const int64_t g_hi = std::min<int64_t>(c.height, grow_of(ctx, ctx->rows_buf));
+        const size_t b_lo = size_t(g_lo - grow_of(ctx, 0));
+        const size_t n = size_t(g_hi - g_lo) * W;
+        double* top = reinterpret_cast<double*>(P.tau[1] + off);
+        double* bot = top + ctx->plane();
+        PF_CUDA(cudaMemcpyAsync(top, tau_top + size_t(g_lo) * W, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        PF_CUDA(cudaMemcpyAsync(bot, tau_bot + size_t(g_lo) * W, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        PF_CUDA(cudaMemsetAsync(P.tau[0] + off, 0, ctx->plane() * 16, ctx->stream));
+        ctx->launches += pfk::launch_interleave_tau(P.tau[0] + off + b_lo * W, top, bot, n, ctx->stream);
+        PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
+        // Tour lengths: per agent (id order) up, scattered onto the agents' cells.
+        std::vector<double> per_agent(n_agents);
+        host_parallel(n_agents, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1; ++i) per_agent[i] = agents[i].tour_length;
+        });
+        double* d_pa = nullptr;
+        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
+        cudaMemcpyAsync(d_pa, per_agent.data(), size_t(n_agents) * 8, cudaMemcpyHostToDevice, ctx->stream);
+        ctx->launches += pfk::launch_scatter_tour(P.tour + off, P.cell[0] + off, d_pa, ctx->plane(), ctx->stream);
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        cudaFree(d_pa);
+        if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state upload: ") + cudaGetErrorString(e));
+    }
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
     // Both buffers now hold the state; keep the current parity.
     set_step(ctx, step);
     return PF_OK;
@@ -412,22 +441,32 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
     const pfk::Planes& P = ctx->args.p;
     std::vector<uint32_t> words(own);
     PF_CUDA(cudaMemcpy(words.data(), P.cell[ctx->parity] + off, own * 4, cudaMemcpyDeviceToHost));
-    std::vector<double> tour;
-    std::vector<double2> tau;
-    if (ctx->aco()) {
-        tour.resize(own);
-        tau.resize(own);
-        PF_CUDA(cudaMemcpy(tour.data(), P.tour + off, own * 8, cudaMemcpyDeviceToHost));
-        PF_CUDA(cudaMemcpy(tau.data(), P.tau[ctx->parity] + off, own * 16, cudaMemcpyDeviceToHost));
-    }
     const size_t g0 = size_t(ctx->row_begin) * W;
+    std::vector<double> per_agent;
+    if (ctx->aco()) {
+        // Pheromone: de-interleaved on the device into the owned rows of the
+        // other ping-pong buffer (rewritten by the next step anyway), then
+        // copied straight into the reference planes.
+        double* top = reinterpret_cast<double*>(P.tau[ctx->parity ^ 1] + off);
+        double* bot = top + own;
+        ctx->launches += pfk::launch_deinterleave_tau(top, bot, P.tau[ctx->parity] + off, own, ctx->stream);
+        if (tau_top) PF_CUDA(cudaMemcpyAsync(tau_top + g0, top, own * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (tau_bot) PF_CUDA(cudaMemcpyAsync(tau_bot + g0, bot, own * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        // Tour lengths: gathered per agent (id order) on the device.
+        per_agent.assign(n_agents, 0.0);
+        double* d_pa = nullptr;
+        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
+        ctx->launches += pfk::launch_gather_tour(d_pa, P.cell[ctx->parity] + off, P.tour + off, own, ctx->stream);
+        cudaMemcpyAsync(per_agent.data(), d_pa, size_t(n_agents) * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        cudaFree(d_pa);
+        if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(e));
+    }
     std::atomic<bool> bad{false};
     host_parallel(own, [&](size_t i0, size_t i1) {
         for (size_t i = i0; i < i1; ++i) {
             const uint32_t w = words[i];
             const size_t gi = g0 + i;
-            if (tau_top && ctx->aco()) tau_top[gi] = tau[i].x;
-            if (tau_bot && ctx->aco()) tau_bot[gi] = tau[i].y;
             const uint32_t id = w & pfdev::kIdMask;
             if (occ) occ[gi] = uint8_t(w ? (w >> 30) : 0);
             if (index) index[gi] = w ? id : 0;
@@ -443,7 +482,7 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
                 a.group = uint8_t(w >> 30);
                 a.row = a.future_row = int32_t(gi / W);
                 a.col = a.future_col = int32_t(gi % W);
-                a.tour_length = ctx->aco() ? tour[i] : 0.0;
+                a.tour_length = ctx->aco() ? per_agent[id - 1] : 0.0;
                 a.crossed = (w & pfdev::kCrossedBit) ? 1 : 0;
             }
         }

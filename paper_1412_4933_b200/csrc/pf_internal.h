@@ -54,6 +54,11 @@ int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
 // Fill a tau plane range with {v, v}.
 int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);
+// State upload / download layout transforms.
+int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s);
+int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s);
+int launch_scatter_tour(double* tour, const uint32_t* words, const double* per_agent, size_t n, cudaStream_t s);
+int launch_gather_tour(double* per_agent, const uint32_t* words, const double* tour, size_t n, cudaStream_t s);
 int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                         const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
                         double* uni, double* nrm, cudaStream_t s);

@@ -347,6 +347,54 @@ int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s) {
     return 1;
 }
 
+// --- state upload / download layout transforms (pf_load_state / pf_store_state)
+
+__global__ void interleave_tau_kernel(double2* dst, const double* top, const double* bot, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        dst[i] = make_double2(top[i], bot[i]);
+}
+
+__global__ void deinterleave_tau_kernel(double* top, double* bot, const double2* src, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const double2 t = src[i];
+        top[i] = t.x;
+        bot[i] = t.y;
+    }
+}
+
+// tour[cell] = per_agent[id - 1] for agent cells (cell-resident tour layout).
+__global__ void scatter_tour_kernel(double* tour, const uint32_t* words, const double* per_agent, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        tour[i] = (w != 0u && w != pfdev::kWall) ? per_agent[(w & pfdev::kIdMask) - 1] : 0.0;
+    }
+}
+
+// per_agent[id - 1] = tour[cell] for agent cells.
+__global__ void gather_tour_kernel(double* per_agent, const uint32_t* words, const double* tour, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        if (w != 0u && w != pfdev::kWall) per_agent[(w & pfdev::kIdMask) - 1] = tour[i];
+    }
+}
+
+int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s) {
+    interleave_tau_kernel<<<148 * 8, 256, 0, s>>>(dst, top, bot, n);
+    return 1;
+}
+int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s) {
+    deinterleave_tau_kernel<<<148 * 8, 256, 0, s>>>(top, bot, src, n);
+    return 1;
+}
+int launch_scatter_tour(double* tour, const uint32_t* words, const double* per_agent, size_t n, cudaStream_t s) {
+    scatter_tour_kernel<<<148 * 8, 256, 0, s>>>(tour, words, per_agent, n);
+    return 1;
+}
+int launch_gather_tour(double* per_agent, const uint32_t* words, const double* tour, size_t n, cudaStream_t s) {
+    gather_tour_kernel<<<148 * 8, 256, 0, s>>>(per_agent, words, tour, n);
+    return 1;
+}
+
 }  // namespace pfk
 
 namespace pfk {
