@@ -74,7 +74,7 @@ struct Smem {
     uint32_t queue[QCAP];  // (unit << 5) | bit
     unsigned long long mbar[2];
     int item;
-    uint32_t nq;
+    uint32_t nq[2];  // work-list fill: [0] S1 draws, [1] S2 contested cells (the list is reused)
     uint32_t cnt[3];
 };
 
@@ -180,11 +180,11 @@ __device__ __forceinline__ void grant(Smem& sm, int rr, int si, int k, uint32_t 
     }
 }
 
-// Append the set bits of `mask` for unit u to the work list; returns the bits
-// that did not fit (to be processed in place).
-__device__ __forceinline__ uint32_t enqueue(Smem& sm, int u, uint32_t mask) {
+// Append the set bits of `mask` for unit u to work list `list`; returns the
+// bits that did not fit (to be processed in place).
+__device__ __forceinline__ uint32_t enqueue(Smem& sm, int u, uint32_t mask, int list) {
     const uint32_t n = __popc(mask);
-    const uint32_t pos = atomicAdd(&sm.nq, n);
+    const uint32_t pos = atomicAdd(&sm.nq[list], n);
     uint32_t overflow = 0u;
     for (uint32_t i = 0; i < n; ++i) {
         const int j = __ffs(mask) - 1;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         }
         for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
         if (threadIdx.x < RT) sm.dirty[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) sm.nq = 0u;
+        if (threadIdx.x == 0) sm.nq[0] = sm.nq[1] = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
         // ------------------------------------------------------------ S0
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             d[1] = B & n.em;  // Bottom forward: (-1, 0)
             const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
             uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) slow = enqueue(sm, u, slow);
+            if (slow) slow = enqueue(sm, u, slow, 0);
             while (slow) {  // queue overflow: draw in place
                 const int j = __ffs(slow) - 1;
                 slow &= slow - 1u;
@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             for (int q = 0; q < 8; ++q) sm.D[q][di][si] = d[q];
         }
         __syncthreads();
-        {
-            const uint32_t nq = min(sm.nq, uint32_t(QCAP));
+        // Queued draws (the barrier is skipped, uniformly, when none were queued).
+        if (const uint32_t nq = min(sm.nq[0], uint32_t(QCAP))) {
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                 const uint32_t q = sm.queue[e];
                 const int u = int(q >> 5), j = int(q & 31u);
@@ -462,10 +462,8 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 const int code = draw_intent<ACO>(a, sm, base, tin, di, si, j, bottom, r0, c0, seed, step);
                 atomicOr(&sm.D[code][di][si], 1u << j);
             }
+            __syncthreads();
         }
-        __syncthreads();
-        if (threadIdx.x == 0) sm.nq = 0u;
-        __syncthreads();
 
         // ------------------------------------------------------------ S2
         // Claims, winners and grants for destinations in rows -1 .. RT.
@@ -490,7 +488,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (win[q]) grant(sm, ai - 1, si, q, win[q]);
-            uint32_t multi = twos ? enqueue(sm, u, twos) : 0u;
+            uint32_t multi = twos ? enqueue(sm, u, twos, 1) : 0u;
             while (multi) {  // queue overflow: draw in place
                 const int j = __ffs(multi) - 1;
                 multi &= multi - 1u;
@@ -498,16 +496,15 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             }
         }
         __syncthreads();
-        {
-            const uint32_t nq = min(sm.nq, uint32_t(QCAP));
+        if (const uint32_t nq = min(sm.nq[1], uint32_t(QCAP))) {
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                 const uint32_t q = sm.queue[e];
                 const int u = int(q >> 5), j = int(q & 31u);
                 const int ai = u / SS, si = u - ai * SS;
                 set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
             }
+            __syncthreads();
         }
-        __syncthreads();
 
         // ------------------------------------------------------------ S3
         for (int rr = warp; rr < RT; rr += NW) {

@@ -1,0 +1,18 @@
+#!/bin/bash
+# A/B builds for same-box timing comparisons (dev tool):
+#   tools/debug/lib_base.so  from git REF (default HEAD)
+#   tools/debug/lib_new.so   from the working tree
+# then on the GPU box:  python tools/ab_time.py c5_lem c4_aco_x64 ...
+set -e
+cd "$(dirname "$0")/.."
+REF=${1:-HEAD}
+mkdir -p tools/debug
+TMP=$(mktemp -d)
+git archive "$REF" paper_1412_4933_b200/csrc include | tar -x -C "$TMP"
+FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off"
+SRCS="pf_kernels.cu pf_bitstep.cu pf_context.cu pf_setup.cpp"
+nvcc $FLAGS -I "$TMP/include" -shared -o tools/debug/lib_base.so $(for s in $SRCS; do echo "$TMP/paper_1412_4933_b200/csrc/$s"; done) &
+nvcc $FLAGS -I include -shared -o tools/debug/lib_new.so $(for s in $SRCS; do echo "paper_1412_4933_b200/csrc/$s"; done) &
+wait
+rm -rf "$TMP"
+echo "built tools/debug/lib_base.so ($REF) and tools/debug/lib_new.so (working tree)"

@@ -1,0 +1,41 @@
+"""Same-box A/B step timing of tools/debug/lib_base.so vs lib_new.so (dev tool).
+
+    python tools/ab_time.py c5_lem c4_aco_x64 [--rounds 3] [--steps 100]
+"""
+import argparse
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CODE = r'''
+import sys, os
+sys.path.insert(0, os.getcwd())
+import bench, paper_1412_4933_b200 as p
+steps = int(sys.argv[1])
+for name in sys.argv[2:]:
+    cfg, reps, desc = bench.scenario(name)
+    e = p.Ensemble(cfg, replicas=reps); e.run(5)
+    tot, _ = e.time_steps(steps)
+    print(f"{name} {tot/steps*1e3:.2f}", flush=True); e.close()
+'''
+
+ap = argparse.ArgumentParser()
+ap.add_argument("workloads", nargs="+")
+ap.add_argument("--rounds", type=int, default=3)
+ap.add_argument("--steps", type=int, default=100)
+args = ap.parse_args()
+res = {}
+for r in range(args.rounds):
+    for tag in ("base", "new"):
+        env = dict(os.environ, PEDFLOW_B200_LIB=os.path.join(ROOT, "tools", "debug", f"lib_{tag}.so"))
+        out = subprocess.run([sys.executable, "-c", CODE, str(args.steps)] + args.workloads, env=env, cwd=ROOT,
+                             capture_output=True, text=True).stdout
+        for line in out.split("\n"):
+            if line.strip():
+                name, us = line.split()
+                res.setdefault((name, tag), []).append(float(us))
+for name in args.workloads:
+    b, n = min(res.get((name, "base"), [0])), min(res.get((name, "new"), [0]))
+    print(f"{name:12s} base {b:9.1f} us   new {n:9.1f} us   new/base {n / b if b else 0:.3f}   "
+          f"(all base {res.get((name, 'base'))}, new {res.get((name, 'new'))})")
