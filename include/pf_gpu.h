@@ -144,6 +144,14 @@ int pf_halo(pf_ctx* ctx, int32_t replica, int32_t side, int32_t recv, pf_halo_ro
  * (upper owns the rows just above lower) on the same or peer devices. */
 int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower);
 
+/* Device-side state audit of one replica, the cell-resident form of
+ * check_consistency (src/state.cpp:77-110): every agent cell holds an id in
+ * [1, 2n] of the right side, no id twice, no wall inside the arena, and (for
+ * an unsharded context) exactly 2n agents. PF_ERR_STATE with the first bad
+ * cell otherwise. *agent_cells (may be NULL) = agents found in owned rows.
+ * Checks the resident state in place: nothing is downloaded. */
+int pf_audit(pf_ctx* ctx, int32_t replica, uint64_t* agent_cells);
+
 /* Device self-test of the keyed generator (src/rng.cpp:43-59,152-156): for
  * n keys computes random_bits, uniform and normal(mu, sigma) ON THE DEVICE
  * (the same device functions the step kernels use). Pins the device RNG and

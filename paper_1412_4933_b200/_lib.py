@@ -100,6 +100,7 @@ _sigs = {
     "pf_halo": (C.c_int, [_vp, _i32, _i32, _i32, C.POINTER(PfHalo)]),
     "pf_exchange_pair": (C.c_int, [_vp, _vp]),
     "pf_selftest_rng": (C.c_int, [_i32, _u32, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double, _vp, _vp, _vp]),
+    "pf_audit": (C.c_int, [_vp, _i32, C.POINTER(_u64)]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(lib, _name)
@@ -197,6 +198,13 @@ class Context:
 
     def stream(self) -> int:
         return lib.pf_stream(self.h)
+
+    def audit(self, replica: int = 0) -> int:
+        """Device-side check_consistency of one replica; returns its agent count
+        (raises StateCorrupt on a violation)."""
+        n = C.c_uint64(0)
+        check(lib.pf_audit(self.h, replica, C.byref(n)))
+        return n.value
 
     def halo(self, replica: int, side: int, recv: bool) -> PfHalo:
         h = PfHalo()

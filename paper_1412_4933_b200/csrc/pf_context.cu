@@ -716,6 +716,45 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
     return PF_OK;
 }
 
+int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    const uint32_t n_agents = 2u * uint32_t(ctx->cfg.agents_per_side);
+    const size_t words = (size_t(n_agents) + 31) / 32;
+    char* d = nullptr;
+    PF_CUDA(cudaMalloc(&d, words * 4 + 3 * 8));
+    auto* counts = reinterpret_cast<unsigned long long*>(d);
+    auto* seen = reinterpret_cast<uint32_t*>(d + 3 * 8);
+    unsigned long long h[3] = {0ull, 0ull, ~0ull};
+    int rc = PF_OK;
+    if (cudaMemcpyAsync(counts, h, sizeof h, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(seen, 0, words * 4, ctx->stream) != cudaSuccess) {
+        rc = fail(PF_ERR_CUDA, "audit setup failed");
+    } else {
+        const size_t W = size_t(ctx->cfg.width);
+        ctx->launches += pfk::launch_audit(ctx->args.p.cell[ctx->parity] + size_t(rep) * ctx->plane(),
+                                           size_t(pfk::kGhost) * W, size_t(ctx->rows_owned) * W, n_agents, seen,
+                                           counts, ctx->stream);
+        if (cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = fail(PF_ERR_CUDA, "audit failed");
+    }
+    cudaFree(d);
+    if (rc) return rc;
+    if (agent_cells) *agent_cells = h[0];
+    if (h[1]) {
+        const size_t cell = size_t(h[2] - 1);
+        const size_t W = size_t(ctx->cfg.width);
+        return fail(PF_ERR_STATE, "state corrupt: " + std::to_string(h[1]) + " bad cell(s), first at (" +
+                                      std::to_string(ctx->row_begin + cell / W) + "," + std::to_string(cell % W) + ")");
+    }
+    // A single (unsharded) context must hold every agent exactly once.
+    if (ctx->rows_owned == ctx->cfg.height && h[0] != n_agents)
+        return fail(PF_ERR_STATE, "state corrupt: agent count disagrees with occupied cells");
+    return PF_OK;
+}
+
 int pf_selftest_rng(int32_t device, uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                     const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits_out,
                     double* uniform_out, double* normal_out) {

@@ -54,6 +54,8 @@ int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
 // Fill a tau plane range with {v, v}.
 int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);
+int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agents, uint32_t* seen,
+                 unsigned long long* counts, cudaStream_t s);
 // State upload / download layout transforms.
 int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s);
 int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s);

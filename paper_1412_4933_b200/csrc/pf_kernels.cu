@@ -378,6 +378,43 @@ __global__ void gather_tour_kernel(double* per_agent, const uint32_t* words, con
     }
 }
 
+// Device-side state audit (check_consistency, src/state.cpp:77-110, in the
+// cell-resident layout): every agent cell holds an id in [1, n_agents] whose
+// group matches its side (ids 1..n Top, n+1..2n Bottom, src/state.cpp:72-73),
+// no id appears twice (bitmap), no wall inside the arena. counts[0] = agent
+// cells, counts[1] = violations, counts[2] = first violating cell + 1.
+__global__ void audit_kernel(const uint32_t* words, size_t first, size_t n, uint32_t n_agents, uint32_t* seen,
+                             unsigned long long* counts) {
+    unsigned long long agents = 0;
+    for (size_t i = first + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < first + n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        if (w == 0u) continue;
+        bool bad = w == pfdev::kWall;
+        if (!bad) {
+            const uint32_t id = w & pfdev::kIdMask, g = w >> 30;
+            bad = id == 0u || id > n_agents || g != (id <= n_agents / 2 ? 1u : 2u);
+            if (!bad) {
+                const uint32_t b = 1u << ((id - 1) & 31u);
+                bad = (atomicOr(&seen[(id - 1) >> 5], b) & b) != 0u;  // duplicate id
+                ++agents;
+            }
+        }
+        if (bad) {
+            atomicAdd(&counts[1], 1ull);
+            atomicMin(&counts[2], (unsigned long long)(i - first + 1));
+        }
+    }
+    agents = __reduce_add_sync(0xFFFFFFFFu, unsigned(agents));
+    if ((threadIdx.x & 31) == 0 && agents) atomicAdd(&counts[0], agents);
+}
+
+int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agents, uint32_t* seen,
+                 unsigned long long* counts, cudaStream_t s) {
+    audit_kernel<<<148 * 8, 256, 0, s>>>(words, first, n, n_agents, seen, counts);
+    return 1;
+}
+
 int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s) {
     interleave_tau_kernel<<<148 * 8, 256, 0, s>>>(dst, top, bot, n);
     return 1;

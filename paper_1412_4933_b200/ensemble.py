@@ -51,6 +51,11 @@ class Ensemble:
         s._step = self.ctx.store(replica, s._occ, s._index, s._agents, s._tau_top, s._tau_bot)
         return s
 
+    def audit(self, replica: int = 0) -> int:
+        """Device-side check_consistency (src/state.cpp:77-110) of one replica,
+        in place; returns the agent count, raises StateCorrupt on a violation."""
+        return self.ctx.audit(replica)
+
     def load(self, replica: int, s: SimState):
         self.ctx.load(replica, s.occupancy, s.index, s.agents, s.pheromone_top, s.pheromone_bottom, s.step)
 

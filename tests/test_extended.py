@@ -1,0 +1,127 @@
+"""Wider parity and the §8(f) rows: randomized configurations against the C
+oracle (in the spirit of SPEC acceptance #1: 32x32 / 96x96 grids, both models,
+random parameters), the device-side audit (check_consistency on the GPU), and
+the CSV `simulate` driver."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.helpers import first_divergence, to_config, to_scenario
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def random_configs(n, seed=1234):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        w = int(rng.choice([16, 32, 48, 64, 96]))
+        h = int(rng.choice([16, 32, 48, 64, 96]))
+        cap = w * h // 2
+        n_side = int(rng.integers(0, cap + 1))
+        while 2 * ((n_side + w - 1) // w) > h:
+            n_side //= 2
+        kw = dict(width=w, height=h, agents_per_side=n_side, model=str(rng.choice(["lem", "aco"])),
+                  seed=int(rng.integers(0, 2**40)), d0=float(rng.choice([1.5, 2.0, 3.0])),
+                  sel_mu=float(rng.choice([0.5, 1.0, 1.3])), sel_sigma=float(rng.choice([0.0, 0.5, 2.0])),
+                  alpha=float(rng.choice([0.0, 1.0])), beta=float(rng.choice([0.0, 1.0, 2.0, 3.5])),
+                  rho=float(rng.choice([0.01, 0.05, 0.5, 1.0])), tau0=float(rng.choice([0.1, 1.0, 1e-3])),
+                  q=float(rng.choice([0.5, 1.0, 4.0])))
+        out.append(kw)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kw", random_configs(24), ids=lambda kw: f"{kw['model']}{kw['width']}x{kw['height']}n{kw['agents_per_side']}")
+def test_random_config_vs_oracle(kw):
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    steps = 150
+    ora = OracleState(to_scenario(kw))
+    orep = ora.run(steps)
+    cfg = to_config(kw)
+    state = p.new_environment(cfg, kw["seed"])
+    eng = p.StepEngine(p.EngineOptions.from_config(cfg, kw["seed"]))
+    rep = eng.run_array(state, steps)
+    assert (rep == orep).all(), "per-step reports differ"
+    assert first_divergence(state, ora) == "identical"
+
+
+@pytest.mark.gpu
+def test_alpha_fractional_matches_oracle():
+    """alpha not in {0,1} uses pow (tolerance-only by contract); in practice the
+    trajectories and fields still agree for this scenario."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    kw = dict(width=64, height=64, agents_per_side=800, model="aco", seed=77, alpha=0.7, rho=0.2)
+    ora = OracleState(to_scenario(kw))
+    ora.run(80)
+    cfg = to_config(kw)
+    s = p.new_environment(cfg, 77)
+    p.StepEngine(p.EngineOptions.from_config(cfg, 77)).run(s, 80)
+    assert (s.index == ora.index).all()
+    np.testing.assert_allclose(s.pheromone_top, ora.tau_top, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(s.pheromone_bottom, ora.tau_bot, rtol=1e-12, atol=0)
+
+
+@pytest.mark.gpu
+def test_device_audit_accepts_valid_and_detects_corruption():
+    import torch
+
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200.sharding import _device_tensor
+
+    cfg = p.ScenarioConfig(width=480, height=480, agents_per_side=51200, model=p.Model.Aco)
+    ens = p.Ensemble(cfg, replicas=4)
+    for r in range(4):
+        assert ens.audit(r) == 102400
+    ens.run(100)
+    for r in range(4):
+        assert ens.audit(r) == 102400
+    # duplicate an id inside the arena (first owned rows of replica 1)
+    h = ens.ctx.halo(1, 0, False)
+    rows = _device_tensor(h.cells, h.cell_bytes, 0).view(torch.int32)
+    occupied = torch.nonzero(rows != 0).flatten()
+    empty = torch.nonzero(rows == 0).flatten()
+    rows[empty[0]] = rows[occupied[0]]
+    torch.cuda.synchronize()
+    with pytest.raises(p.StateCorrupt):
+        ens.audit(1)
+    assert ens.audit(0) == 102400
+
+
+def test_cli_config_error_exit_code(tmp_path):
+    r = subprocess.run([sys.executable, "-m", "paper_1412_4933_b200.cli", "simulate", "--width", "100",
+                        "--out", str(tmp_path)], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 2 and "multiple of 16" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_simulate_csv_matches_oracle_and_is_deterministic(tmp_path):
+    from oracle.oracle import OracleState, Scenario
+
+    args = ["--model", "aco", "--width", "96", "--height", "96", "--agents-per-side", "500", "--steps", "120",
+            "--repeats", "3", "--seed", "9", "--zero-timings"]
+    outs = []
+    for k in range(2):
+        out = tmp_path / f"run{k}"
+        r = subprocess.run([sys.executable, "-m", "paper_1412_4933_b200.cli", "simulate", *args, "--out", str(out)],
+                           capture_output=True, text=True, cwd=ROOT)
+        assert r.returncode == 0, r.stderr
+        outs.append(((out / "steps.csv").read_bytes(), (out / "summary.csv").read_bytes()))
+    assert outs[0] == outs[1]  # byte-determinism (SPEC acceptance #9)
+    lines = outs[0][0].decode().strip().split("\n")
+    assert lines[0] == "run_id,seed,model,executor,step,crossed_top,crossed_bottom,crossed_total,moved"
+    for run in range(3):
+        o = OracleState(Scenario(width=96, height=96, agents_per_side=500, model="aco", seed=9 + run))
+        rep = o.run(120)
+        rows = [l.split(",") for l in lines[1:] if l.startswith(f"{run},")]
+        assert [int(r[8]) for r in rows] == rep["moved"].tolist()
+        assert int(rows[-1][7]) == int(rep["newly_crossed_top"].sum() + rep["newly_crossed_bottom"].sum())
