@@ -43,7 +43,14 @@ namespace {
 constexpr int RT = 16;           // output rows per tile
 constexpr int NS = 8;            // output 32-column segments per strip
 constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
-constexpr int RING = 2 * SR;     // ring slots: current window + the next tile's rows or the next item's window
+#ifndef PF_BITS_RING
+#define PF_BITS_RING (2 * SR)
+#endif
+// Ring slots: the current window + the next tile's rows, or (2 * SR) the next
+// item's whole window, prefetched during an item's last tile.
+constexpr int RING = PF_BITS_RING;
+constexpr bool kCrossPrefetch = RING >= 2 * SR;
+static_assert(RING >= SR + RT, "the ring must hold a window and the next tile's rows");
 constexpr int SS = NS + 2;       // staged segments: -1 .. NS
 // Staged columns: the strip plus a 4-column halo on each side (the dependency
 // radius is 3; 4 keeps TMA rows 16-byte aligned). Bit j of plane segment si
@@ -368,13 +375,13 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             if (warp == 0) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
             ++nload;
         } else {
-            next_base = slot(base, SR);
+            next_base = kCrossPrefetch ? slot(base, SR) : 0;
             if (warp == 0) {
                 int nx = 0;
                 if (lane == 0) nx = int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item = nx;
-                if (nx < n_items) {
+                if (kCrossPrefetch && nx < n_items) {
                     const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
                     load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
                 }
@@ -617,6 +624,15 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
     }
     item = sm.item;  // claimed during the last tile (visible after its barriers)
+    if (!kCrossPrefetch && item < n_items) {
+        // Small ring: the next item's window is loaded only now, into the
+        // slots the finished item released.
+        if (warp == 0) {
+            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+            load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
+        }
+        __syncthreads();  // wall rows written by warp 0 are visible to all
+    }
     if (item < n_items) ++nload;
     }  // work items
 }
