@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             if (!ACO && !sm.dirty[rr]) {
                 // Nothing arrives or leaves in this row: copy its 256 words
                 // with 16-byte shared loads / global stores (lane = 4 columns).
+                // (Not for ACO: the extra live registers cost it more in spills.)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int col = 128 * h + 4 * lane;
@@ -636,6 +637,11 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     if (item < n_items) ++nload;
     }  // work items
 }
+
+// Three CTAs per SM must fit the 196 KB shared-memory carve-out step (1 KB
+// reserved per CTA): the next step up (228 KB) leaves 28 KB of L1 instead of
+// 60 KB, and the ACO pheromone stream then loses ~15% (measured).
+static_assert(sizeof(Smem) <= (196 * 1024) / 3 - 1024 - 64, "shared memory would cost 3 CTAs/SM their L1");
 
 int configure_step_bits() {
     const int bytes = int(sizeof(Smem));
