@@ -12,6 +12,7 @@
 #include <atomic>
 #include <functional>
 #include <map>
+#include <memory>
 #include <string>
 #include <thread>
 #include <utility>
@@ -51,6 +52,7 @@ struct pf_ctx {
     uint32_t* d_step = nullptr;
     uint32_t* d_reports = nullptr;  // [replicas][kReportCap][4] ring
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // side stream for host<->device state transfers
     uint64_t launches = 0;
     std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
     std::vector<void*> allocs;
@@ -139,6 +141,7 @@ int pf_destroy(pf_ctx* ctx) {
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (void* p : ctx->allocs) cudaFree(p);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
     delete ctx;
     return PF_OK;
 }
@@ -190,7 +193,8 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     };
     if (cudaSetDevice(cfg->device) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "cudaSetDevice failed"));
     if (pfk::configure_step_bits() != 0) return cleanup(fail(PF_ERR_CUDA, "cannot configure the step kernel's shared memory"));
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(PF_ERR_CUDA, "cudaStreamCreate failed"));
     auto alloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
@@ -347,11 +351,45 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     if (n_agents && !agents) return fail(PF_ERR_ARG, "null agents");
     if (ctx->aco() && (!tau_top || !tau_bot)) return fail(PF_ERR_ARG, "ACO state needs both pheromone fields");
     PF_CUDA(cudaSetDevice(c.device));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));  // no step may still be using the planes
     const size_t W = size_t(c.width);
-    std::vector<uint32_t> words(ctx->plane(), 0u);
+    const size_t off = size_t(rep) * ctx->plane();
+    pfk::Planes& P = ctx->args.p;
+    // Pheromone planes and per-agent tour lengths go up in the reference's own
+    // layout on a side stream, driven by a helper thread while this thread
+    // audits and converts the cell words; they are rearranged on the device.
+    std::unique_ptr<uint32_t[]> words_buf(new uint32_t[ctx->plane()]);
+    uint32_t* words = words_buf.get();
+    double* d_pa = nullptr;
+    cudaError_t side_err = cudaSuccess;
+    std::thread side;
+    const int64_t g_lo = std::max<int64_t>(0, grow_of(ctx, 0));
+    const int64_t g_hi = std::min<int64_t>(c.height, grow_of(ctx, ctx->rows_buf));
+    const size_t b_lo = size_t(g_lo - grow_of(ctx, 0));
+    const size_t n_tau = size_t(g_hi - g_lo) * W;
+    double* d_top = ctx->aco() ? reinterpret_cast<double*>(P.tau[1] + off) : nullptr;
+    double* d_bot = d_top ? d_top + ctx->plane() : nullptr;
+    if (ctx->aco()) {
+        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
+        side = std::thread([&] {
+            cudaSetDevice(c.device);
+            std::vector<double> per_agent(n_agents);
+            for (size_t i = 0; i < n_agents; ++i) per_agent[i] = agents[i].tour_length;
+            cudaError_t e = cudaMemcpyAsync(d_top, tau_top + size_t(g_lo) * W, n_tau * 8, cudaMemcpyHostToDevice,
+                                            ctx->stream2);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_bot, tau_bot + size_t(g_lo) * W, n_tau * 8, cudaMemcpyHostToDevice, ctx->stream2);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_pa, per_agent.data(), size_t(n_agents) * 8, cudaMemcpyHostToDevice, ctx->stream2);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream2);
+            side_err = e;
+        });
+    }
+    auto join_side = [&] {
+        if (side.joinable()) side.join();
+    };
     // check_consistency-style audit (src/state.cpp:77-110) + conversion to
-    // cell words, parallel over buffer rows. Tour lengths and pheromone go up
-    // in the reference's own layout and are rearranged on the device.
+    // cell words, parallel over buffer rows.
     std::atomic<int> bad{0};  // 0 ok, else index into kWhy
     static const char* kWhy[] = {"", "state corrupt: index/occupancy mismatch", "state corrupt: index out of agent range",
                                  "state corrupt: agent record id mismatch",
@@ -360,7 +398,7 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     host_parallel(size_t(ctx->rows_buf), [&](size_t b0, size_t b1) {
         for (size_t b = b0; b < b1 && !bad.load(std::memory_order_relaxed); ++b) {
             const int64_t g = grow_of(ctx, int(b));
-            uint32_t* wrow = words.data() + b * W;
+            uint32_t* wrow = words + b * W;
             if (g < 0 || g >= c.height) {
                 std::fill(wrow, wrow + W, kWall);
                 continue;
@@ -369,6 +407,7 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
                 const size_t gi = size_t(g) * W + col;
                 const uint32_t id = index[gi];
                 int why = 0;
+                wrow[col] = 0u;
                 if ((id == 0) != (occ[gi] == 0)) why = 1;
                 else if (id == 0) continue;
                 else if (id > n_agents) why = 2;
@@ -389,40 +428,29 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
             }
         }
     });
-    if (bad.load()) return fail(PF_ERR_STATE, kWhy[bad.load()]);
-    const size_t off = size_t(rep) * ctx->plane();
-    pfk::Planes& P = ctx->args.p;
-    PF_CUDA(cudaMemcpyAsync(P.cell[0] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (ctx->aco()) {
-        // Pheromone: the two reference planes (the rows present in this
-        // buffer) land in the second ping-pong buffer used as scratch, then
-        // are interleaved into {top, bottom} pairs on the device.
-        const int64_t g_lo = std::max<int64_t>(0, grow_of(ctx, 0));
-        const int64_t g_hi = std::min<int64_t>(c.height, grow_of(ctx, ctx->rows_buf));
-        const size_t b_lo = size_t(g_lo - grow_of(ctx, 0));
-        const size_t n = size_t(g_hi - g_lo) * W;
-        double* top = reinterpret_cast<double*>(P.tau[1] + off);
-        double* bot = top + ctx->plane();
-        PF_CUDA(cudaMemcpyAsync(top, tau_top + size_t(g_lo) * W, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-        PF_CUDA(cudaMemcpyAsync(bot, tau_bot + size_t(g_lo) * W, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-        PF_CUDA(cudaMemsetAsync(P.tau[0] + off, 0, ctx->plane() * 16, ctx->stream));
-        ctx->launches += pfk::launch_interleave_tau(P.tau[0] + off + b_lo * W, top, bot, n, ctx->stream);
-        PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
-        // Tour lengths: per agent (id order) up, scattered onto the agents' cells.
-        std::vector<double> per_agent(n_agents);
-        host_parallel(n_agents, [&](size_t i0, size_t i1) {
-            for (size_t i = i0; i < i1; ++i) per_agent[i] = agents[i].tour_length;
-        });
-        double* d_pa = nullptr;
-        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
-        cudaMemcpyAsync(d_pa, per_agent.data(), size_t(n_agents) * 8, cudaMemcpyHostToDevice, ctx->stream);
-        ctx->launches += pfk::launch_scatter_tour(P.tour + off, P.cell[0] + off, d_pa, ctx->plane(), ctx->stream);
-        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (bad.load()) {
+        join_side();
         cudaFree(d_pa);
-        if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state upload: ") + cudaGetErrorString(e));
+        return fail(PF_ERR_STATE, kWhy[bad.load()]);
     }
-    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaError_t e = cudaMemcpyAsync(P.cell[0] + off, words, ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    join_side();
+    if (e == cudaSuccess) e = side_err;
+    if (e == cudaSuccess && ctx->aco()) {
+        // The two pheromone planes sit in the second ping-pong buffer (used as
+        // scratch): interleave them into {top, bottom} pairs, then scatter the
+        // per-agent tour lengths onto the agents' cells.
+        e = cudaMemsetAsync(P.tau[0] + off, 0, ctx->plane() * 16, ctx->stream);
+        ctx->launches += pfk::launch_interleave_tau(P.tau[0] + off + b_lo * W, d_top, d_bot, n_tau, ctx->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream);
+        ctx->launches += pfk::launch_scatter_tour(P.tour + off, P.cell[0] + off, d_pa, ctx->plane(), ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d_pa);
+    if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state upload: ") + cudaGetErrorString(e));
     // Both buffers now hold the state; keep the current parity.
     set_step(ctx, step);
     return PF_OK;
@@ -439,28 +467,37 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
     const size_t own = size_t(ctx->rows_owned) * W;
     const size_t off = size_t(rep) * ctx->plane() + size_t(pfk::kGhost) * W;
     const pfk::Planes& P = ctx->args.p;
-    std::vector<uint32_t> words(own);
-    PF_CUDA(cudaMemcpy(words.data(), P.cell[ctx->parity] + off, own * 4, cudaMemcpyDeviceToHost));
+    std::unique_ptr<uint32_t[]> words_buf(new uint32_t[own]);
+    uint32_t* words = words_buf.get();
+    PF_CUDA(cudaMemcpyAsync(words, P.cell[ctx->parity] + off, own * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
     const size_t g0 = size_t(ctx->row_begin) * W;
+    // ACO: pheromone is de-interleaved on the device into the owned rows of
+    // the other ping-pong buffer (rewritten by the next step anyway) and tour
+    // lengths are gathered per agent (id order); a helper thread copies both
+    // down while this thread converts the cell words.
     std::vector<double> per_agent;
+    double* d_pa = nullptr;
+    cudaError_t side_err = cudaSuccess;
+    std::thread side;
     if (ctx->aco()) {
-        // Pheromone: de-interleaved on the device into the owned rows of the
-        // other ping-pong buffer (rewritten by the next step anyway), then
-        // copied straight into the reference planes.
+        per_agent.assign(n_agents, 0.0);
+        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
         double* top = reinterpret_cast<double*>(P.tau[ctx->parity ^ 1] + off);
         double* bot = top + own;
         ctx->launches += pfk::launch_deinterleave_tau(top, bot, P.tau[ctx->parity] + off, own, ctx->stream);
-        if (tau_top) PF_CUDA(cudaMemcpyAsync(tau_top + g0, top, own * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        if (tau_bot) PF_CUDA(cudaMemcpyAsync(tau_bot + g0, bot, own * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        // Tour lengths: gathered per agent (id order) on the device.
-        per_agent.assign(n_agents, 0.0);
-        double* d_pa = nullptr;
-        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
         ctx->launches += pfk::launch_gather_tour(d_pa, P.cell[ctx->parity] + off, P.tour + off, own, ctx->stream);
-        cudaMemcpyAsync(per_agent.data(), d_pa, size_t(n_agents) * 8, cudaMemcpyDeviceToHost, ctx->stream);
-        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
-        cudaFree(d_pa);
-        if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(e));
+        side = std::thread([&, top, bot] {
+            cudaSetDevice(c.device);
+            cudaError_t e = cudaSuccess;
+            if (tau_top) e = cudaMemcpyAsync(tau_top + g0, top, own * 8, cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess && tau_bot)
+                e = cudaMemcpyAsync(tau_bot + g0, bot, own * 8, cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(per_agent.data(), d_pa, size_t(n_agents) * 8, cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+            side_err = e;
+        });
     }
     std::atomic<bool> bad{false};
     host_parallel(own, [&](size_t i0, size_t i1) {
@@ -482,11 +519,20 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
                 a.group = uint8_t(w >> 30);
                 a.row = a.future_row = int32_t(gi / W);
                 a.col = a.future_col = int32_t(gi % W);
-                a.tour_length = ctx->aco() ? per_agent[id - 1] : 0.0;
                 a.crossed = (w & pfdev::kCrossedBit) ? 1 : 0;
             }
         }
     });
+    if (side.joinable()) side.join();
+    cudaFree(d_pa);
+    if (side_err != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(side_err));
+    if (agents && ctx->aco() && !bad) {
+        // Only agents on this shard's cells were gathered.
+        host_parallel(own, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1; ++i)
+                if (const uint32_t w = words[i]) agents[(w & pfdev::kIdMask) - 1].tour_length = per_agent[(w & pfdev::kIdMask) - 1];
+        });
+    }
     if (bad) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
     if (step) *step = ctx->step;
     return PF_OK;
