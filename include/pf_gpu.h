@@ -98,14 +98,25 @@ int pf_new_environment(const pf_config* cfg, uint64_t seed, uint8_t* occ, uint32
 int pf_create(const pf_config* cfg, pf_ctx** out);
 int pf_destroy(pf_ctx* ctx);
 
-/* new_environment for every replica (seed + i), built on the host and
- * uploaded; for a shard only the owned rows and ghost rows travel. */
+/* Per-replica scenarios. By default replica i runs cfg.seed + i at
+ * cfg.agents_per_side (the repeat loop, tools/pedflow.cpp:135). This call
+ * overrides either or both per replica (arrays of cfg.replicas entries, NULL
+ * keeps the current values), so one context can batch a whole density sweep
+ * (tools/pedflow.cpp:159-189): each density is checked as validate() would
+ * (src/config.cpp:101-124). Call it before pf_init_environment / pf_load_state;
+ * the crossing band (src/metrics.cpp:8-11) follows each replica's density. */
+int pf_set_replicas(pf_ctx* ctx, const int32_t* agents_per_side, const uint64_t* seeds);
+/* agents_per_side of one replica, or -1 for a bad argument. */
+int32_t pf_replica_agents(const pf_ctx* ctx, int32_t replica);
+
+/* new_environment for every replica (its seed and density), built on the host
+ * and uploaded; for a shard only the owned rows and ghost rows travel. */
 int pf_init_environment(pf_ctx* ctx);
 
 /* Upload / download one replica's SimState (inc/state.hpp:16-31) as the
  * reference's planes over the GLOBAL grid. A shard reads rows
  * [row_begin-3, row_end+3) and writes back only its owned rows (agents living
- * there). n_agents must be 2*agents_per_side. */
+ * there). n_agents must be 2 * the replica's agents_per_side. */
 int pf_load_state(pf_ctx* ctx, int32_t replica, const uint8_t* occ, const uint32_t* index, const pf_agent* agents,
                   uint32_t n_agents, const double* tau_top, const double* tau_bot, uint32_t step);
 int pf_store_state(pf_ctx* ctx, int32_t replica, uint8_t* occ, uint32_t* index, pf_agent* agents, uint32_t n_agents,

@@ -86,6 +86,8 @@ _sigs = {
     "pf_new_environment": (C.c_int, [C.POINTER(PfConfig), _u64, _vp, _vp, _vp, _vp, _vp]),
     "pf_create": (C.c_int, [C.POINTER(PfConfig), C.POINTER(_vp)]),
     "pf_destroy": (C.c_int, [_vp]),
+    "pf_set_replicas": (C.c_int, [_vp, _vp, _vp]),
+    "pf_replica_agents": (_i32, [_vp, _i32]),
     "pf_init_environment": (C.c_int, [_vp]),
     "pf_load_state": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _u32, _vp, _vp, _u32]),
     "pf_store_state": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _u32, _vp, _vp, C.POINTER(_u32)]),
@@ -153,6 +155,18 @@ class Context:
     @property
     def aco(self) -> bool:
         return self.cfg.model == PF_MODEL_ACO
+
+    def set_replicas(self, agents_per_side=None, seeds=None):
+        """Per-replica densities and/or seeds (pf_set_replicas)."""
+        aps = None if agents_per_side is None else np.ascontiguousarray(agents_per_side, np.int32)
+        sds = None if seeds is None else np.ascontiguousarray(seeds, np.uint64)
+        for a in (aps, sds):
+            if a is not None and a.shape != (self.replicas,):
+                raise ValueError(f"expected {self.replicas} per-replica values, got shape {a.shape}")
+        check(lib.pf_set_replicas(self.h, ptr(aps), ptr(sds)))
+
+    def replica_agents(self, replica: int) -> int:
+        return int(lib.pf_replica_agents(self.h, replica))
 
     def init_environment(self):
         check(lib.pf_init_environment(self.h))

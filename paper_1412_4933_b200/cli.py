@@ -1,85 +1,159 @@
-"""`simulate` on the GPU engine with the reference CLI's CSV outputs.
+"""The reference CLI's `simulate` and `sweep` on the GPU engine, with its CSV outputs.
 
     python -m paper_1412_4933_b200.cli simulate --model aco --agents-per-side 1280 --steps 2000 --repeats 2 --out runs/
+    python -m paper_1412_4933_b200.cli sweep --model lem --steps 1000 --repeats 10 --densities 1280,2560 --out runs/
 
-The reference's `pedflow simulate` (tools/pedflow.cpp:132-146) runs `repeats`
-seeds (seed, seed+1, ..., tools/pedflow.cpp:135) through run_scenario and
-writes steps.csv / summary.csv with the headers of SPEC.md:519-522 and
-doubles as %.10g (src/csv.cpp:8-44). This mirror runs all repeats in one
-replica-batched launch per step. Runtime columns are the GPU job's wall time
-(split evenly over the repeats), or blank with --zero-timings
-(inc/csv.hpp:11-16). Exit codes: 2 config error, 1 other (tools/pedflow.cpp:253-258).
+Flags, the `--config` scenario file and their precedence follow
+tools/pedflow.cpp:40-97 (only flags the user passed override the file).
+`simulate` (tools/pedflow.cpp:132-146) runs `repeats` seeds (seed, seed+1, ...)
+and writes steps.csv / summary.csv; `sweep` (tools/pedflow.cpp:148-189) runs
+every density x model x repeat and writes sweep.csv. Headers, row order,
+%.10g doubles, the summary's `mean` row and --zero-timings (0 in the
+wall-clock columns) follow src/csv.cpp:8-54. All runs of one model share each
+step's launch (paper_1412_4933_b200/sweep.py). The executor column reads `gpu`.
+Runtime columns are the batch's wall time split evenly over its runs. Exit
+codes: 2 config error, 1 other (tools/pedflow.cpp:253-258). The reference's
+`bench` (sequential vs parallel CPU executors) has no GPU counterpart; see
+bench.py.
 """
 from __future__ import annotations
 
 import argparse
 import os
+import re
 import sys
-import time
 
-import numpy as np
-
-from .engine import ConfigError, Model, ScenarioConfig, validate
-from .ensemble import Ensemble
+from .config import parse_config
+from .engine import ConfigError, Model, RunReport
+from .sweep import SweepRow, aggregate, run_batch, sweep
 
 STEPS_HEADER = "run_id,seed,model,executor,step,crossed_top,crossed_bottom,crossed_total,moved"
 SUMMARY_HEADER = "run_id,seed,model,executor,agents_total,steps,throughput,runtime_seconds"
+SWEEP_HEADER = "agents_total,model,repeats,throughput_mean,throughput_sd,runtime_mean_seconds"
+EXECUTOR = "gpu"
+_STOI = re.compile(r"[ \t\n\v\f\r]*[+-]?[0-9]+\Z")
 
 
 def format_double(v: float) -> str:
     return "%.10g" % v  # src/csv.cpp:8-12
 
 
-def simulate(cfg: ScenarioConfig, out_dir: str, zero_timings: bool = False, device: int = 0) -> list[dict]:
-    validate(cfg)
-    os.makedirs(out_dir, exist_ok=True)
-    model = "lem" if Model(cfg.model) == Model.Lem else "aco"
-    t0 = time.perf_counter()
-    ens = Ensemble(cfg, replicas=cfg.repeats, seed=cfg.seed, device=device)
-    rep = ens.run(cfg.steps) if cfg.steps else np.zeros((cfg.repeats, 0))
-    ens.close()
-    wall = time.perf_counter() - t0
-    runs = []
-    with open(os.path.join(out_dir, "steps.csv"), "w") as f:
-        f.write(STEPS_HEADER + "\n")
-        for i in range(cfg.repeats):
-            r = rep[i]
-            top = np.cumsum(r["newly_crossed_top"].astype(np.int64)) if cfg.steps else np.zeros(0, np.int64)
-            bot = np.cumsum(r["newly_crossed_bottom"].astype(np.int64)) if cfg.steps else np.zeros(0, np.int64)
-            for s in range(cfg.steps):
-                f.write(f"{i},{cfg.seed + i},{model},gpu,{int(r['step'][s])},{int(top[s])},{int(bot[s])},"
-                        f"{int(top[s] + bot[s])},{int(r['moved'][s])}\n")
-            runs.append(dict(run_id=i, seed=cfg.seed + i, throughput=int(top[-1] + bot[-1]) if cfg.steps else 0))
-    with open(os.path.join(out_dir, "summary.csv"), "w") as f:
-        f.write(SUMMARY_HEADER + "\n")
-        for r in runs:
-            rt = "" if zero_timings else format_double(wall / cfg.repeats)
-            f.write(f"{r['run_id']},{r['seed']},{model},gpu,{2 * cfg.agents_per_side},{cfg.steps},{r['throughput']},{rt}\n")
+def _model(m) -> str:
+    return "lem" if Model(m) == Model.Lem else "aco"  # src/config.cpp:12
+
+
+def write_steps_csv(runs: list[RunReport]) -> str:
+    """src/csv.cpp:14-24."""
+    out = [STEPS_HEADER + "\n"]
+    for i, r in enumerate(runs):
+        for row in r.series:
+            out.append(f"{i},{r.seed},{_model(r.model)},{EXECUTOR},{row.step},{row.crossed_top},"
+                       f"{row.crossed_bottom},{row.crossed_total},{row.moved}\n")
+    return "".join(out)
+
+
+def write_summary_csv(runs: list[RunReport], zero_timings: bool) -> str:
+    """src/csv.cpp:26-44, including the trailing `mean` row for repeats > 1."""
+    out = [SUMMARY_HEADER + "\n"]
+    for i, r in enumerate(runs):
+        rt = 0.0 if zero_timings else r.runtime_seconds
+        out.append(f"{i},{r.seed},{_model(r.model)},{EXECUTOR},{r.agents_total},{r.config.steps},{r.throughput},"
+                   f"{format_double(rt)}\n")
+    if len(runs) > 1:
+        agg = aggregate(runs)
+        rt = 0.0 if zero_timings else agg.runtime_mean_seconds
+        out.append(f"mean,{runs[0].seed},{_model(runs[0].model)},{EXECUTOR},{agg.agents_total},"
+                   f"{runs[0].config.steps},{format_double(agg.throughput_mean)},{format_double(rt)}\n")
+    return "".join(out)
+
+
+def write_sweep_csv(rows: list[SweepRow], zero_timings: bool) -> str:
+    """src/csv.cpp:46-54."""
+    out = [SWEEP_HEADER + "\n"]
+    for r in rows:
+        rt = 0.0 if zero_timings else r.runtime_mean_seconds
+        out.append(f"{r.agents_total},{_model(r.model)},{r.repeats},{format_double(r.throughput_mean)},"
+                   f"{format_double(r.throughput_sd)},{format_double(rt)}\n")
+    return "".join(out)
+
+
+def _write(path: str, text: str):
+    with open(path, "w", encoding="utf-8", newline="") as f:
+        f.write(text)
+
+
+def simulate(cfg, zero_timings: bool = False, device: int = 0) -> list[RunReport]:
+    """cmd_simulate (tools/pedflow.cpp:132-146)."""
+    runs = run_batch(cfg, [(cfg.agents_per_side, (cfg.seed + i) % 2**64) for i in range(cfg.repeats)], device=device)
+    os.makedirs(cfg.out_dir, exist_ok=True)
+    _write(os.path.join(cfg.out_dir, "steps.csv"), write_steps_csv(runs))
+    _write(os.path.join(cfg.out_dir, "summary.csv"), write_summary_csv(runs, zero_timings))
     return runs
 
 
+def run_sweep(cfg, densities: list[int] | None, zero_timings: bool = False, device: int = 0) -> list[SweepRow]:
+    """cmd_sweep (tools/pedflow.cpp:159-189)."""
+    rows = sweep(cfg, densities, device=device)
+    os.makedirs(cfg.out_dir, exist_ok=True)
+    _write(os.path.join(cfg.out_dir, "sweep.csv"), write_sweep_csv(rows, zero_timings))
+    return rows
+
+
+def parse_densities(text: str) -> list[int]:
+    """tools/pedflow.cpp:91-111: comma-separated items, each a whole std::stoi
+    parse (leading whitespace and sign allowed) of a non-negative int."""
+    out = []
+    pos = 0
+    while pos < len(text):
+        comma = text.find(",", pos)
+        if comma < 0:
+            comma = len(text)
+        item = text[pos:comma]
+        if not _STOI.match(item) or not 0 <= int(item) <= 2**31 - 1:
+            raise ConfigError(f"malformed value for key 'densities': '{item}'")
+        out.append(int(item))
+        pos = comma + 1
+    return out
+
+
+_FLAGS = [  # (flag, config key, argparse type)
+    ("--width", "width", int), ("--height", "height", int), ("--agents-per-side", "agents_per_side", int),
+    ("--model", "model", str), ("--steps", "steps", int), ("--seed", "seed", int), ("--repeats", "repeats", int),
+    ("--executor", "executor", str), ("--threads", "threads", int), ("--d0", "d0", float),
+    ("--sel-mu", "sel_mu", float), ("--sel-sigma", "sel_sigma", float), ("--alpha", "alpha", float),
+    ("--beta", "beta", float), ("--rho", "rho", float), ("--tau0", "tau0", float), ("--q", "q", float),
+    ("--out", "out_dir", str),
+]
+
+
+def _fmt(v) -> str:
+    return "%.17g" % v if isinstance(v, float) else str(v)  # fmt_full, tools/pedflow.cpp:35-39
+
+
 def main(argv=None) -> int:
-    ap = argparse.ArgumentParser(prog="pedflow-b200")
+    ap = argparse.ArgumentParser(prog="pedflow-b200", description="bi-directional pedestrian flow simulator (GPU)")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    s = sub.add_parser("simulate")
-    d = ScenarioConfig()
-    for name in ("width", "height", "agents_per_side", "steps", "seed", "repeats"):
-        s.add_argument("--" + name.replace("_", "-"), type=int, default=getattr(d, name))
-    for name in ("d0", "sel_mu", "sel_sigma", "alpha", "beta", "rho", "tau0", "q"):
-        s.add_argument("--" + name.replace("_", "-"), type=float, default=getattr(d, name))
-    s.add_argument("--model", choices=["lem", "aco"], default="aco")
-    s.add_argument("--out", default=".")
-    s.add_argument("--zero-timings", action="store_true")
-    s.add_argument("--device", type=int, default=0)
+    cmds = {"simulate": sub.add_parser("simulate", help="run one scenario over repeated seeds"),
+            "sweep": sub.add_parser("sweep", help="density sweep over one or both models")}
+    for name, p in cmds.items():
+        p.add_argument("--config", default="", help="flat key = value scenario file")
+        for flag, key, typ in _FLAGS:
+            p.add_argument(flag, dest=key, type=typ, default=None)
+        p.add_argument("--zero-timings", action="store_true")
+        p.add_argument("--device", type=int, default=0)
+        if name == "sweep":
+            p.add_argument("--densities", default="")
     args = ap.parse_args(argv)
     try:
-        cfg = ScenarioConfig(width=args.width, height=args.height, agents_per_side=args.agents_per_side,
-                             model=Model.Lem if args.model == "lem" else Model.Aco, steps=args.steps, seed=args.seed,
-                             repeats=args.repeats, d0=args.d0, sel_mu=args.sel_mu, sel_sigma=args.sel_sigma,
-                             alpha=args.alpha, beta=args.beta, rho=args.rho, tau0=args.tau0, q=args.q,
-                             out_dir=args.out)
-        simulate(cfg, args.out, args.zero_timings, args.device)
-        print(f"wrote {os.path.join(args.out, 'steps.csv')} and summary.csv")
+        overrides = [(key, _fmt(getattr(args, key))) for _, key, _ in _FLAGS if getattr(args, key) is not None]
+        cfg = parse_config(args.config, overrides)
+        densities = parse_densities(args.densities) if getattr(args, "densities", "") else []
+        if args.cmd == "simulate":
+            simulate(cfg, args.zero_timings, args.device)
+            print(f"wrote {os.path.join(cfg.out_dir, 'steps.csv')} and {os.path.join(cfg.out_dir, 'summary.csv')}")
+        else:
+            run_sweep(cfg, densities or None, args.zero_timings, args.device)
+            print(f"wrote {os.path.join(cfg.out_dir, 'sweep.csv')}")
         return 0
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)

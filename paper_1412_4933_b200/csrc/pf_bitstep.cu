@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     while (item < n_items) {
     const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
     const int rep = it.rep, c0 = it.c0;
-    const uint64_t seed = a.seed_base + uint64_t(rep);
+    const uint64_t seed = __ldg(&a.rep[rep].seed);
+    const int band = __ldg(&a.rep[rep].band);
     const size_t plane_base = size_t(rep) * a.p.plane;
     uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + plane_base;
     const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                     const uint32_t sw = sm.word[slot(base, rr + 3 + kDR[kc])][si * 32 + lane + kDC[kc] - WOFF];
                     group = sw >> 30;
                     nw = sw;
-                    if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, a.k.band)) {  // src/engine.cpp:163-170
+                    if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
                         nw |= kCrossedBit;
                         if (valid) {
                             if (group == 1u) ++ntop;

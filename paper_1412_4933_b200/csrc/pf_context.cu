@@ -56,6 +56,8 @@ struct pf_ctx {
     uint64_t launches = 0;
     std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
     std::vector<void*> allocs;
+    std::vector<int32_t> rep_aps;               // agents_per_side of each replica
+    std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
     size_t plane() const { return size_t(rows_buf) * size_t(cfg.width); }
     size_t total() const { return plane() * size_t(cfg.replicas); }
@@ -170,7 +172,6 @@ static int fill_consts(pf_ctx* ctx) {
     k.model = c.model;
     k.W = c.width;
     k.H = c.height;
-    k.band = pfhost::band_height(c.agents_per_side, c.width);
     return PF_OK;
 }
 
@@ -244,7 +245,18 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         ctx->launches += pfk::launch_fill_u8(P.intent, n, pfdev::kNone, ctx->stream);
         ctx->launches += pfk::launch_fill_u8(P.win, n, pfdev::kNone, ctx->stream);
     }
-    ctx->args.seed_base = cfg->seed;
+    ctx->rep_aps.assign(size_t(cfg->replicas), cfg->agents_per_side);
+    ctx->reps.resize(size_t(cfg->replicas));
+    for (int r = 0; r < cfg->replicas; ++r)
+        ctx->reps[size_t(r)] = {cfg->seed + uint64_t(r), pfhost::band_height(cfg->agents_per_side, cfg->width),
+                                2u * uint32_t(cfg->agents_per_side)};
+    {
+        auto* d_rep = static_cast<pfdev::ReplicaParams*>(alloc(ctx->reps.size() * sizeof(pfdev::ReplicaParams)));
+        if (!d_rep || cudaMemcpy(d_rep, ctx->reps.data(), ctx->reps.size() * sizeof(pfdev::ReplicaParams),
+                                 cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup(fail(PF_ERR_CUDA, "device allocation failed (out of memory?)"));
+        ctx->args.rep = d_rep;
+    }
     ctx->args.d_step = ctx->d_step;
     ctx->args.reports = ctx->d_reports;
     ctx->args.report_cap = kReportCap;
@@ -255,6 +267,36 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "init failed"));
     *out = ctx;
     return PF_OK;
+}
+
+int pf_set_replicas(pf_ctx* ctx, const int32_t* agents_per_side, const uint64_t* seeds) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    const int R = ctx->cfg.replicas;
+    std::vector<pfdev::ReplicaParams> reps = ctx->reps;
+    std::vector<int32_t> aps = ctx->rep_aps;
+    for (int r = 0; r < R; ++r) {
+        if (agents_per_side) {
+            pf_config v = ctx->cfg;  // validate() of the replica's scenario (src/config.cpp:101-124)
+            v.agents_per_side = agents_per_side[r];
+            if (int rc = pf_validate(&v)) return rc;
+            aps[size_t(r)] = v.agents_per_side;
+            reps[size_t(r)].band = pfhost::band_height(v.agents_per_side, v.width);
+            reps[size_t(r)].n_agents = 2u * uint32_t(v.agents_per_side);
+        }
+        if (seeds) reps[size_t(r)].seed = seeds[r];
+    }
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    PF_CUDA(cudaMemcpy(const_cast<pfdev::ReplicaParams*>(ctx->args.rep), reps.data(),
+                       reps.size() * sizeof(pfdev::ReplicaParams), cudaMemcpyHostToDevice));
+    ctx->reps.swap(reps);
+    ctx->rep_aps.swap(aps);
+    return PF_OK;
+}
+
+int32_t pf_replica_agents(const pf_ctx* ctx, int32_t rep) {
+    if (!ctx || rep < 0 || rep >= ctx->cfg.replicas) return -1;
+    return ctx->rep_aps[size_t(rep)];
 }
 
 // Run fn(begin, end) over [0, n) on the host's threads (state conversion).
@@ -325,7 +367,7 @@ int pf_init_environment(pf_ctx* ctx) {
                     if (g < 0 || g >= c.height) std::fill(w.begin() + size_t(b) * W, w.begin() + size_t(b + 1) * W, kWall);
                 }
                 const int64_t lo = grow_of(ctx, 0), hi = grow_of(ctx, ctx->rows_buf);
-                pfhost::place_all(c.width, c.height, c.agents_per_side, c.seed + uint64_t(r0 + t),
+                pfhost::place_all(c.width, c.height, ctx->rep_aps[size_t(r0 + t)], ctx->reps[size_t(r0 + t)].seed,
                                   [&](uint32_t cell, uint32_t id, uint32_t g) {
                                       const int64_t row = cell / W;
                                       if (row < lo || row >= hi) return;
@@ -347,7 +389,7 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     if (!ctx || !occ || !index) return fail(PF_ERR_ARG, "null argument");
     if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
     const pf_config& c = ctx->cfg;
-    if (n_agents != 2u * uint32_t(c.agents_per_side)) return fail(PF_ERR_STATE, "state corrupt: agent count disagrees with config");
+    if (n_agents != ctx->reps[size_t(rep)].n_agents) return fail(PF_ERR_STATE, "state corrupt: agent count disagrees with config");
     if (n_agents && !agents) return fail(PF_ERR_ARG, "null agents");
     if (ctx->aco() && (!tau_top || !tau_bot)) return fail(PF_ERR_ARG, "ACO state needs both pheromone fields");
     PF_CUDA(cudaSetDevice(c.device));
@@ -766,7 +808,7 @@ int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
-    const uint32_t n_agents = 2u * uint32_t(ctx->cfg.agents_per_side);
+    const uint32_t n_agents = ctx->reps[size_t(rep)].n_agents;
     const size_t words = (size_t(n_agents) + 31) / 32;
     char* d = nullptr;
     PF_CUDA(cudaMalloc(&d, words * 4 + 3 * 8));

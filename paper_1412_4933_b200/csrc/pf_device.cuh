@@ -42,7 +42,15 @@ struct StepConsts {
     double q;
     double diag;         // sqrt(2) (src/aco.cpp:11)
     int model;           // 0 LEM, 1 ACO
-    int W, H, band;
+    int W, H;
+};
+
+// Per-replica scenario parameters: replicas of one context share the grid and
+// the model but may differ in seed and density (sweep, tools/pedflow.cpp:159-189).
+struct ReplicaParams {
+    uint64_t seed;      // RngKey seed (inc/rng.hpp:9-37)
+    int32_t band;       // band_height(agents_per_side, W) (src/metrics.cpp:8-11)
+    uint32_t n_agents;  // 2 * agents_per_side
 };
 
 // ----------------------------------------------------------------- Philox

@@ -29,7 +29,7 @@ struct StepArgs {
     pfdev::StepConsts k;              // by value: hot scalars read from param space
     const pfdev::StepConsts* kc;      // device copy: tables read by the slow paths
     Planes p;
-    uint64_t seed_base;     // replica r uses seed_base + r
+    const pfdev::ReplicaParams* rep;  // [replicas] seed / band / agent count
     const uint32_t* d_step; // device step counter: step of batch slot 0
     uint32_t* reports;      // [replicas][report_cap][4], ring slot = step % report_cap
     int report_cap;

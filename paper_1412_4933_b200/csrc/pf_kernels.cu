@@ -48,7 +48,7 @@ __device__ __forceinline__ void block_count(uint32_t moved, uint32_t ntop, uint3
 // empty (kNone otherwise), `vacate` whether the occupant's move was granted,
 // `src_word` the winner's word.
 template <bool ACO>
-__device__ __forceinline__ void commit_cell(const StepConsts& k, uint32_t w, uint8_t win, bool vacate,
+__device__ __forceinline__ void commit_cell(const StepConsts& k, int band, uint32_t w, uint8_t win, bool vacate,
                                             uint32_t src_word, int grow, size_t gi, size_t si,
                                             uint32_t* __restrict__ cout, const double2* __restrict__ tin,
                                             double2* __restrict__ tout, double* __restrict__ tour,
@@ -61,7 +61,7 @@ __device__ __forceinline__ void commit_cell(const StepConsts& k, uint32_t w, uin
         if (win != kNone) {
             group = src_word >> 30;
             nw = src_word;
-            if (!(src_word & kCrossedBit) && crossed_at(group, grow, k.H, k.band)) {
+            if (!(src_word & kCrossedBit) && crossed_at(group, grow, k.H, band)) {
                 nw |= kCrossedBit;
                 if (group == 1u) ++ntop; else ++nbot;
             }
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) step_fused_kernel(const StepArgs a, int s
     const int r0 = blockIdx.y * TH; // owned-local row of the tile origin
     const int c0 = blockIdx.x * TW;
     const uint32_t step = *a.d_step + uint32_t(slot);
-    const uint64_t seed = a.seed_base + uint64_t(rep);
+    const uint64_t seed = a.rep[rep].seed;
     const size_t base = size_t(rep) * a.p.plane;
     const uint32_t* __restrict__ cin = a.p.cell[parity] + base;
     uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + base;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) step_fused_kernel(const StepArgs a, int s
             const uint8_t ic = s_int[tr * TW + tc];
             vacate = ic != kNone && s_win[(tr + 1 + kDR[ic]) * CW + tc + 1 + kDC[ic]] == uint8_t(7 - ic);
         }
-        commit_cell<ACO>(k, w, win, vacate, src_word, a.row_begin + lr, gi, si, cout, tin, tout, tour, moved,
+        commit_cell<ACO>(k, a.rep[rep].band, w, win, vacate, src_word, a.row_begin + lr, gi, si, cout, tin, tout, tour, moved,
                          ntop, nbot);
     }
     uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) pipeline_propose_kernel(const StepArgs a,
     if (w != 0u && w != kWall) {
         const uint32_t step = *a.d_step + uint32_t(slot);
         code = propose(
-            a.kc, a.k.model, w, a.seed_base + uint64_t(rep), step,
+            a.kc, a.k.model, w, a.rep[rep].seed, step,
             [&](int dr, int dc) {
                 const int cc = c + dc;
                 if (cc < 0 || cc >= W) return kWall;
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) pipeline_resolve_kernel(const StepArgs a,
         if (claims) {
             const uint32_t step = *a.d_step + uint32_t(slot);
             const int64_t grow = int64_t(a.row_begin) + (b - kGhost);
-            wv = resolve(claims, a.seed_base + uint64_t(rep), step, uint64_t(grow) * uint64_t(W) + uint64_t(c));
+            wv = resolve(claims, a.rep[rep].seed, step, uint64_t(grow) * uint64_t(W) + uint64_t(c));
         }
     }
     a.p.win[base + size_t(b) * W + c] = wv;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(256) pipeline_commit_kernel(const StepArgs a, 
             const uint8_t ic = intent[gi];
             vacate = ic != kNone && winp[size_t(b + kDR[ic]) * W + (c + kDC[ic])] == uint8_t(7 - ic);
         }
-        commit_cell<ACO>(a.k, w, win, vacate, src_word, a.row_begin + lr, gi, si, a.p.cell[parity ^ 1] + base,
+        commit_cell<ACO>(a.k, a.rep[rep].band, w, win, vacate, src_word, a.row_begin + lr, gi, si, a.p.cell[parity ^ 1] + base,
                          ACO ? a.p.tau[parity] + base : nullptr, ACO ? a.p.tau[parity ^ 1] + base : nullptr,
                          ACO ? a.p.tour + base : nullptr, moved, ntop, nbot);
     }

@@ -63,6 +63,9 @@ class ScenarioConfig:
     tau0: float = 0.1
     q: float = 1.0
     out_dir: str = "."
+    # True when the model was picked (file or flag) rather than defaulted;
+    # sweep runs both models otherwise (inc/config.hpp:45-48).
+    model_explicit: bool = False
 
 
 def _pf_config(cfg: ScenarioConfig, seed: int | None = None, *, replicas: int = 1, row_begin: int = 0,
@@ -80,16 +83,25 @@ def _pf_config(cfg: ScenarioConfig, seed: int | None = None, *, replicas: int = 
 
 
 def validate(cfg: ScenarioConfig) -> None:
-    """validate() (src/config.cpp:101-124) plus the GPU preconditions. Raises ConfigError."""
+    """validate() (src/config.cpp:101-124, same checks in the same order) plus
+    the GPU preconditions. Raises ConfigError."""
+    if cfg.width < 16 or cfg.width % 16 != 0:
+        raise ConfigError("width must be a multiple of 16 and >= 16")
+    if cfg.height < 16 or cfg.height % 16 != 0:
+        raise ConfigError("height must be a multiple of 16 and >= 16")
+    if cfg.agents_per_side < 0:
+        raise ConfigError("agents_per_side must be >= 0")
     if cfg.steps < 0:
         raise ConfigError("steps must be >= 0")
     if cfg.repeats < 1:
         raise ConfigError("repeats must be >= 1")
     if cfg.threads < 0:
         raise ConfigError("threads must be >= 0")
-    if not cfg.out_dir:
-        raise ConfigError("out_dir must not be empty")
     c = _pf_config(cfg)
+    if not cfg.out_dir:  # after the numeric checks, before capacity (src/config.cpp:115-117)
+        c.agents_per_side = 0
+        _lib.check(_lib.lib.pf_validate(c))
+        raise ConfigError("out_dir must not be empty")
     _lib.check(_lib.lib.pf_validate(c))
 
 

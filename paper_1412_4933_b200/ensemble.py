@@ -15,14 +15,24 @@ from .engine import Model, ScenarioConfig, SimState, StepReport, _pf_config, val
 
 
 class Ensemble:
+    """R replicas of one grid and model in one launch per step.
+
+    By default replica i is `cfg` with seed `seed + i`. `agents_per_side` and
+    `seeds` (sequences of R values) override density and seed per replica, so
+    a whole density sweep (tools/pedflow.cpp:159-189) shares each launch.
+    """
+
     def __init__(self, cfg: ScenarioConfig, replicas: int, *, seed: int | None = None, device: int = 0,
-                 kernel: str = "fused", row_begin: int = 0, row_end: int = 0):
+                 kernel: str = "fused", row_begin: int = 0, row_end: int = 0, agents_per_side=None, seeds=None):
         validate(cfg)
         self.cfg = cfg
         self.seed = cfg.seed if seed is None else seed
         self.replicas = replicas
         self.ctx = _lib.Context(_pf_config(cfg, self.seed, replicas=replicas, device=device, kernel=kernel,
                                            row_begin=row_begin, row_end=row_end))
+        if agents_per_side is not None or seeds is not None:
+            self.ctx.set_replicas(agents_per_side, seeds)
+        self.agents_per_side = [self.ctx.replica_agents(r) for r in range(replicas)]
         self.ctx.init_environment()
 
     # --- stepping --------------------------------------------------------
@@ -47,7 +57,7 @@ class Ensemble:
     def state(self, replica: int = 0) -> SimState:
         """Download one replica as a reference-layout SimState."""
         c = self.cfg
-        s = SimState(c.width, c.height, c.model, 2 * c.agents_per_side)
+        s = SimState(c.width, c.height, c.model, 2 * self.agents_per_side[replica])
         s._step = self.ctx.store(replica, s._occ, s._index, s._agents, s._tau_top, s._tau_bot)
         return s
 
