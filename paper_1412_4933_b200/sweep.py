@@ -61,6 +61,34 @@ def aggregate(reports: list[RunReport]) -> SweepRow:
     return row
 
 
+@dataclass
+class ProportionTest:
+    """inc/metrics.hpp:40-43."""
+
+    p_value: float = 1.0
+    defined: bool = True  # False when both runs have zero agents
+
+
+def proportion_test(a: RunReport, b: RunReport) -> ProportionTest:
+    """proportion_test (src/metrics.cpp:18-32): two-sided two-proportion z-test
+    on the crossing fractions of two runs with the same agents_total."""
+    if a.agents_total != b.agents_total:
+        raise ValueError("proportion_test: runs must share agents_total")
+    if a.agents_total == 0:
+        return ProportionTest(1.0, False)
+    if a.throughput == b.throughput:
+        return ProportionTest(1.0, True)
+    n = float(a.agents_total)
+    p1 = float(a.throughput) / n
+    p2 = float(b.throughput) / n
+    pooled = (float(a.throughput) + float(b.throughput)) / (2.0 * n)
+    se = math.sqrt(pooled * (1.0 - pooled) * (2.0 / n))
+    if se == 0.0:
+        return ProportionTest(1.0, True)
+    z = (p1 - p2) / se
+    return ProportionTest(math.erfc(abs(z) / math.sqrt(2.0)), True)
+
+
 def default_sweep_densities(cfg: ScenarioConfig) -> list[int]:
     """tools/pedflow.cpp:148-157: 1,280 .. 51,200 per side on 480x480."""
     if cfg.width == 480 and cfg.height == 480:
@@ -129,4 +157,4 @@ def sweep(cfg: ScenarioConfig, densities: list[int] | None = None, *, device: in
     return rows
 
 
-__all__ = ["SweepRow", "aggregate", "default_sweep_densities", "models_to_run", "run_batch", "sweep"]
+__all__ = ["ProportionTest", "SweepRow", "aggregate", "proportion_test", "default_sweep_densities", "models_to_run", "run_batch", "sweep"]

@@ -98,6 +98,20 @@ def test_aggregate_spec_examples():
         aggregate([])
 
 
+def test_proportion_test_spec_examples():
+    from paper_1412_4933_b200.sweep import proportion_test
+
+    assert proportion_test(_run(7, n=50), _run(7, n=50)).p_value == 1.0
+    assert proportion_test(_run(17417, n=25600), _run(25600, n=25600)).p_value < 1e-6
+    assert proportion_test(_run(100, n=2560), _run(102, n=2560)).p_value > 0.05
+    a, b = _run(100, n=2560), _run(140, n=2560)
+    assert proportion_test(a, b).p_value == proportion_test(b, a).p_value  # symmetric
+    t = proportion_test(_run(0, n=0), _run(0, n=0))
+    assert t.p_value == 1.0 and not t.defined
+    with pytest.raises(ValueError):
+        proportion_test(_run(1, n=10), _run(1, n=12))
+
+
 def test_csv_writers_format():
     rows = [SweepRow(2560, p.Model.Lem, 10, 2559.5, 0.5270462767, 1.25), SweepRow(2560, p.Model.Aco, 1, 1.0 / 3, 0.0, 0.0)]
     assert write_sweep_csv(rows, False) == (
