@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <functional>
 #include <map>
 #include <memory>
@@ -38,6 +39,113 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(PF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Run fn(begin, end) over [0, n) on the host's threads (state conversion).
+static void host_parallel(size_t n, const std::function<void(size_t, size_t)>& fn) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 32), std::max<size_t>(1, n / 64));
+    if (nt <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+    for (auto& t : ts) t.join();
+}
+
+// Large host<->device copies of the caller's pageable planes. A plain
+// cudaMemcpy from pageable memory is staged by the driver through a small
+// pinned buffer with one host thread (a few GB/s). Here the host side of each
+// chunk is a multi-threaded memcpy into / out of our own pinned double buffer
+// and the DMA of chunk i overlaps the host copy of chunk i-1 (or i+1).
+class Stager {
+  public:
+    static constexpr size_t kChunk = size_t(64) << 20;
+    static constexpr size_t kDirect = size_t(4) << 20;  // smaller copies go direct
+
+    ~Stager() {
+        for (int i = 0; i < 2; ++i) {
+            if (ev_[i]) cudaEventDestroy(ev_[i]);
+            if (buf_[i]) cudaFreeHost(buf_[i]);
+        }
+    }
+
+    cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+        if (n < kDirect) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s);
+        if (cudaError_t e = ready()) return e;
+        const size_t nch = (n + kChunk - 1) / kChunk;
+        for (size_t i = 0; i < nch; ++i) {
+            const int slot = int(i & 1);
+            const size_t off = i * kChunk, len = std::min(kChunk, n - off);
+            if (cudaError_t e = cudaEventSynchronize(ev_[slot])) return e;  // DMA of chunk i-2 done
+            par_copy(buf_[slot], static_cast<const char*>(src) + off, len);
+            if (cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off, buf_[slot], len, cudaMemcpyHostToDevice, s))
+                return e;
+            if (cudaError_t e = cudaEventRecord(ev_[slot], s)) return e;
+        }
+        return cudaSuccess;
+    }
+
+    cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
+        if (n < kDirect) {
+            cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s);
+            return e ? e : cudaStreamSynchronize(s);
+        }
+        if (cudaError_t e = ready()) return e;
+        const size_t nch = (n + kChunk - 1) / kChunk;
+        for (size_t i = 0; i <= nch; ++i) {
+            if (i < nch) {
+                const int slot = int(i & 1);
+                const size_t off = i * kChunk, len = std::min(kChunk, n - off);
+                if (cudaError_t e = cudaMemcpyAsync(buf_[slot], static_cast<const char*>(src) + off, len,
+                                                    cudaMemcpyDeviceToHost, s))
+                    return e;
+                if (cudaError_t e = cudaEventRecord(ev_[slot], s)) return e;
+            }
+            if (i >= 1) {
+                const size_t j = i - 1, off = j * kChunk, len = std::min(kChunk, n - off);
+                if (cudaError_t e = cudaEventSynchronize(ev_[j & 1])) return e;
+                par_copy(static_cast<char*>(dst) + off, buf_[j & 1], len);
+            }
+        }
+        return cudaSuccess;
+    }
+
+    // Allocate the pinned buffers now (pf_create does this for large grids so
+    // that the first state transfer does not pay for it).
+    cudaError_t ready() {
+        for (int i = 0; i < 2; ++i) {
+            if (!ev_[i])
+                if (cudaError_t e = cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming)) return e;
+            if (!buf_[i])
+                if (cudaError_t e = cudaHostAlloc(&buf_[i], kChunk, cudaHostAllocDefault)) return e;
+        }
+        return cudaSuccess;
+    }
+
+  private:
+    static void par_copy(void* dst, const void* src, size_t n) {
+        host_parallel(n / 4096 + 1, [&](size_t b0, size_t b1) {
+            const size_t lo = std::min(n, b0 * 4096), hi = std::min(n, b1 * 4096);
+            if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+        });
+    }
+    void* buf_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
+
+// PEDFLOW_IO_TRACE=1: per-phase wall times of state load/store on stderr (dev).
+struct IoTrace {
+    bool on = std::getenv("PEDFLOW_IO_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void operator()(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pedflow io] %-48s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 constexpr int kBatchCap = 256;   // steps per captured CUDA graph
 constexpr int kReportCap = 1024; // report ring slots per replica (slot = step % kReportCap)
 
@@ -56,6 +164,10 @@ struct pf_ctx {
     uint64_t launches = 0;
     std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
     std::vector<void*> allocs;
+    Stager stage[2];                            // [0] main thread, [1] side thread
+    void* io_scratch = nullptr;                 // device staging of exported SimState planes
+    size_t io_scratch_bytes = 0;
+    cudaEvent_t io_event = nullptr;
     std::vector<int32_t> rep_aps;               // agents_per_side of each replica
     std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
@@ -144,6 +256,8 @@ int pf_destroy(pf_ctx* ctx) {
     for (void* p : ctx->allocs) cudaFree(p);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+    if (ctx->io_scratch) cudaFree(ctx->io_scratch);
+    if (ctx->io_event) cudaEventDestroy(ctx->io_event);
     delete ctx;
     return PF_OK;
 }
@@ -265,6 +379,9 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->args.rows_buf = ctx->rows_buf;
     ctx->args.replicas = cfg->replicas;
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "init failed"));
+    if (ctx->plane() * 4 >= Stager::kChunk &&
+        (ctx->stage[0].ready() != cudaSuccess || ctx->stage[1].ready() != cudaSuccess))
+        return cleanup(fail(PF_ERR_CUDA, "pinned staging allocation failed"));
     *out = ctx;
     return PF_OK;
 }
@@ -299,19 +416,6 @@ int32_t pf_replica_agents(const pf_ctx* ctx, int32_t rep) {
     return ctx->rep_aps[size_t(rep)];
 }
 
-// Run fn(begin, end) over [0, n) on the host's threads (state conversion).
-static void host_parallel(size_t n, const std::function<void(size_t, size_t)>& fn) {
-    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 32), std::max<size_t>(1, n / 64));
-    if (nt <= 1) {
-        fn(0, n);
-        return;
-    }
-    std::vector<std::thread> ts;
-    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
-    for (auto& t : ts) t.join();
-}
-
 // Global row of buffer row b.
 static inline int64_t grow_of(const pf_ctx* ctx, int b) { return int64_t(ctx->row_begin) - pfk::kGhost + b; }
 
@@ -322,13 +426,13 @@ static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& wor
     pfk::Planes& P = ctx->args.p;
     // One host->device copy per plane; the second ping-pong buffer is filled
     // device-side (its ghost rows must hold the same walls / halo).
-    PF_CUDA(cudaMemcpyAsync(P.cell[0] + off, words.data(), ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PF_CUDA(ctx->stage[0].h2d(P.cell[0] + off, words.data(), ctx->plane() * 4, ctx->stream));
     PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     if (ctx->aco()) {
-        if (tour) PF_CUDA(cudaMemcpyAsync(P.tour + off, tour->data(), ctx->plane() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        if (tour) PF_CUDA(ctx->stage[0].h2d(P.tour + off, tour->data(), ctx->plane() * 8, ctx->stream));
         else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
         if (tau) {
-            PF_CUDA(cudaMemcpyAsync(P.tau[0] + off, tau->data(), ctx->plane() * 16, cudaMemcpyHostToDevice, ctx->stream));
+            PF_CUDA(ctx->stage[0].h2d(P.tau[0] + off, tau->data(), ctx->plane() * 16, ctx->stream));
             PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
         } else {
             ctx->launches += pfk::launch_fill_tau(P.tau[0] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
@@ -384,6 +488,19 @@ int pf_init_environment(pf_ctx* ctx) {
     return PF_OK;
 }
 
+// Device scratch for state transfers, grown on demand and kept.
+static int ensure_scratch(pf_ctx* ctx, size_t need) {
+    if (ctx->io_scratch_bytes >= need) return PF_OK;
+    if (ctx->io_scratch) cudaFree(ctx->io_scratch);
+    ctx->io_scratch = nullptr;
+    ctx->io_scratch_bytes = 0;
+    PF_CUDA(cudaMalloc(&ctx->io_scratch, need));
+    ctx->io_scratch_bytes = need;
+    return PF_OK;
+}
+
+static size_t up256(size_t b) { return (b + 255) & ~size_t(255); }
+
 int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* index, const pf_agent* agents,
                   uint32_t n_agents, const double* tau_top, const double* tau_bot, uint32_t step) {
     if (!ctx || !occ || !index) return fail(PF_ERR_ARG, "null argument");
@@ -394,35 +511,47 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     if (ctx->aco() && (!tau_top || !tau_bot)) return fail(PF_ERR_ARG, "ACO state needs both pheromone fields");
     PF_CUDA(cudaSetDevice(c.device));
     PF_CUDA(cudaStreamSynchronize(ctx->stream));  // no step may still be using the planes
+    IoTrace io_trace;
     const size_t W = size_t(c.width);
     const size_t off = size_t(rep) * ctx->plane();
     pfk::Planes& P = ctx->args.p;
-    // Pheromone planes and per-agent tour lengths go up in the reference's own
-    // layout on a side stream, driven by a helper thread while this thread
-    // audits and converts the cell words; they are rearranged on the device.
-    std::unique_ptr<uint32_t[]> words_buf(new uint32_t[ctx->plane()]);
-    uint32_t* words = words_buf.get();
-    double* d_pa = nullptr;
-    cudaError_t side_err = cudaSuccess;
-    std::thread side;
+    // The planes go up as they are (the reference's layout); the device checks
+    // them and builds the cell words and the cell-resident tour. Rows of the
+    // buffer window that lie inside the grid: [g_lo, g_hi).
     const int64_t g_lo = std::max<int64_t>(0, grow_of(ctx, 0));
     const int64_t g_hi = std::min<int64_t>(c.height, grow_of(ctx, ctx->rows_buf));
     const size_t b_lo = size_t(g_lo - grow_of(ctx, 0));
-    const size_t n_tau = size_t(g_hi - g_lo) * W;
-    double* d_top = ctx->aco() ? reinterpret_cast<double*>(P.tau[1] + off) : nullptr;
-    double* d_bot = d_top ? d_top + ctx->plane() : nullptr;
+    const size_t win = size_t(g_hi - g_lo) * W;
+    const size_t plane = ctx->plane();
+    const size_t need = up256(win) + up256(win * 4) + up256(size_t(n_agents) * 40) + up256(plane * 4) +
+                        (ctx->aco() ? up256(plane * 8) : 0) + 16;
+    if (int rc = ensure_scratch(ctx, need)) return rc;
+    if (!ctx->io_event) PF_CUDA(cudaEventCreateWithFlags(&ctx->io_event, cudaEventDisableTiming));
+    char* sp = static_cast<char*>(ctx->io_scratch);
+    auto take = [&](size_t bytes) {
+        char* p = sp;
+        sp += up256(bytes);
+        return p;
+    };
+    auto* d_occ = reinterpret_cast<uint8_t*>(take(win));
+    auto* d_index = reinterpret_cast<uint32_t*>(take(win * 4));
+    char* d_agents = take(size_t(n_agents) * 40);
+    auto* d_words = reinterpret_cast<uint32_t*>(take(plane * 4));
+    double* d_tour = ctx->aco() ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
+    auto* d_status = reinterpret_cast<unsigned long long*>(sp);
+    // Pheromone fields go up on a helper thread into the non-current ping-pong
+    // buffer (scratch until the state is known to be valid).
+    const int cur = ctx->parity;
+    double* d_top = ctx->aco() ? reinterpret_cast<double*>(P.tau[cur ^ 1] + off) : nullptr;
+    double* d_bot = d_top ? d_top + plane : nullptr;
+    cudaError_t side_err = cudaSuccess;
+    std::thread side;
     if (ctx->aco()) {
-        PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
         side = std::thread([&] {
             cudaSetDevice(c.device);
-            std::vector<double> per_agent(n_agents);
-            for (size_t i = 0; i < n_agents; ++i) per_agent[i] = agents[i].tour_length;
-            cudaError_t e = cudaMemcpyAsync(d_top, tau_top + size_t(g_lo) * W, n_tau * 8, cudaMemcpyHostToDevice,
-                                            ctx->stream2);
-            if (e == cudaSuccess)
-                e = cudaMemcpyAsync(d_bot, tau_bot + size_t(g_lo) * W, n_tau * 8, cudaMemcpyHostToDevice, ctx->stream2);
-            if (e == cudaSuccess)
-                e = cudaMemcpyAsync(d_pa, per_agent.data(), size_t(n_agents) * 8, cudaMemcpyHostToDevice, ctx->stream2);
+            Stager& st = ctx->stage[1];
+            cudaError_t e = st.h2d(d_top, tau_top + size_t(g_lo) * W, win * 8, ctx->stream2);
+            if (e == cudaSuccess) e = st.h2d(d_bot, tau_bot + size_t(g_lo) * W, win * 8, ctx->stream2);
             if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream2);
             side_err = e;
         });
@@ -430,71 +559,112 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     auto join_side = [&] {
         if (side.joinable()) side.join();
     };
-    // check_consistency-style audit (src/state.cpp:77-110) + conversion to
-    // cell words, parallel over buffer rows.
-    std::atomic<int> bad{0};  // 0 ok, else index into kWhy
-    static const char* kWhy[] = {"", "state corrupt: index/occupancy mismatch", "state corrupt: index out of agent range",
-                                 "state corrupt: agent record id mismatch",
-                                 "state corrupt: agent position disagrees with index grid",
-                                 "state corrupt: agent group disagrees with occupancy"};
-    host_parallel(size_t(ctx->rows_buf), [&](size_t b0, size_t b1) {
-        for (size_t b = b0; b < b1 && !bad.load(std::memory_order_relaxed); ++b) {
-            const int64_t g = grow_of(ctx, int(b));
-            uint32_t* wrow = words + b * W;
-            if (g < 0 || g >= c.height) {
-                std::fill(wrow, wrow + W, kWall);
-                continue;
-            }
-            for (size_t col = 0; col < W; ++col) {
-                const size_t gi = size_t(g) * W + col;
-                const uint32_t id = index[gi];
-                int why = 0;
-                wrow[col] = 0u;
-                if ((id == 0) != (occ[gi] == 0)) why = 1;
-                else if (id == 0) continue;
-                else if (id > n_agents) why = 2;
-                else {
-                    const pf_agent& a = agents[id - 1];
-                    if (a.index != id) why = 3;
-                    else if (a.row != g || a.col != int32_t(col)) why = 4;
-                    else if (a.group != occ[gi] || (a.group != 1 && a.group != 2)) why = 5;
-                    else {
-                        wrow[col] = id | (a.crossed ? pfdev::kCrossedBit : 0u) | (uint32_t(a.group) << 30);
-                    }
-                }
-                if (why) {
-                    int expected = 0;
-                    bad.compare_exchange_strong(expected, why);
-                    break;
-                }
-            }
-        }
-    });
-    if (bad.load()) {
-        join_side();
-        cudaFree(d_pa);
-        return fail(PF_ERR_STATE, kWhy[bad.load()]);
-    }
-    cudaError_t e = cudaMemcpyAsync(P.cell[0] + off, words, ctx->plane() * 4, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream);
-    join_side();
-    if (e == cudaSuccess) e = side_err;
-    if (e == cudaSuccess && ctx->aco()) {
-        // The two pheromone planes sit in the second ping-pong buffer (used as
-        // scratch): interleave them into {top, bottom} pairs, then scatter the
-        // per-agent tour lengths onto the agents' cells.
-        e = cudaMemsetAsync(P.tau[0] + off, 0, ctx->plane() * 16, ctx->stream);
-        ctx->launches += pfk::launch_interleave_tau(P.tau[0] + off + b_lo * W, d_top, d_bot, n_tau, ctx->stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream);
-        ctx->launches += pfk::launch_scatter_tour(P.tour + off, P.cell[0] + off, d_pa, ctx->plane(), ctx->stream);
+    Stager& st = ctx->stage[0];
+    cudaError_t e = st.h2d(d_occ, occ + size_t(g_lo) * W, win, ctx->stream);
+    if (e == cudaSuccess) e = st.h2d(d_index, index + size_t(g_lo) * W, win * 4, ctx->stream);
+    if (e == cudaSuccess && n_agents) e = st.h2d(d_agents, agents, size_t(n_agents) * 40, ctx->stream);
+    io_trace("load: occupancy/index/agents up");
+    // check_consistency-style audit (src/state.cpp:77-110) + conversion, on the device.
+    unsigned long long status = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_status, &status, 8, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+        ctx->launches += pfk::launch_import_state(d_occ, d_index, d_agents, n_agents, uint32_t(W), c.height,
+                                                  grow_of(ctx, 0), g_lo, plane, d_words, d_tour, d_status,
+                                                  ctx->stream);
+        e = cudaMemcpyAsync(&status, d_status, 8, cudaMemcpyDeviceToHost, ctx->stream);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(d_pa);
+    io_trace("load: device audit + conversion");
+    if (e == cudaSuccess && status != ~0ull) {
+        join_side();
+        static const char* kWhy[] = {"", "state corrupt: index/occupancy mismatch",
+                                     "state corrupt: index out of agent range", "state corrupt: agent record id mismatch",
+                                     "state corrupt: agent position disagrees with index grid",
+                                     "state corrupt: agent group disagrees with occupancy"};
+        return fail(PF_ERR_STATE, kWhy[status & 7]);
+    }
+    // Valid: both ping-pong buffers receive the state (the parity is kept).
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.cell[cur] + off, d_words, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.cell[cur ^ 1] + off, d_words, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess && ctx->aco())
+        e = cudaMemcpyAsync(P.tour + off, d_tour, plane * 8, cudaMemcpyDeviceToDevice, ctx->stream);
+    join_side();
+    io_trace("load: side join (pheromone)");
+    if (e == cudaSuccess) e = side_err;
+    if (e == cudaSuccess && ctx->aco()) {
+        // Interleave the two fields into {top, bottom} pairs (ghost rows
+        // outside the grid hold zeros), then mirror into the scratch buffer.
+        e = cudaMemsetAsync(P.tau[cur] + off, 0, plane * 16, ctx->stream);
+        ctx->launches += pfk::launch_interleave_tau(P.tau[cur] + off + b_lo * W, d_top, d_bot, win, ctx->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(P.tau[cur ^ 1] + off, P.tau[cur] + off, plane * 16, cudaMemcpyDeviceToDevice,
+                                ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state upload: ") + cudaGetErrorString(e));
-    // Both buffers now hold the state; keep the current parity.
+    io_trace("load: device transforms");
     set_step(ctx, step);
+    return PF_OK;
+}
+
+// Store of a whole (unsharded) grid: the device writes the reference planes
+// (export_state_kernel, tau de-interleave), the host only copies them down,
+// the pheromone fields on a helper thread.
+static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_agent* agents, uint32_t n_agents,
+                       double* tau_top, double* tau_bot) {
+    const pf_config& c = ctx->cfg;
+    const size_t W = size_t(c.width);
+    const size_t own = size_t(ctx->rows_owned) * W;
+    const size_t off = size_t(rep) * ctx->plane() + size_t(pfk::kGhost) * W;
+    const pfk::Planes& P = ctx->args.p;
+    IoTrace io_trace;
+    auto up = up256;
+    const size_t need = up(own) + up(own * 4) + up(size_t(n_agents) * 40) + 16;
+    if (int rc = ensure_scratch(ctx, need)) return rc;
+    if (!ctx->io_event) PF_CUDA(cudaEventCreateWithFlags(&ctx->io_event, cudaEventDisableTiming));
+    char* s = static_cast<char*>(ctx->io_scratch);
+    auto* d_occ = reinterpret_cast<uint8_t*>(s);
+    auto* d_index = reinterpret_cast<uint32_t*>(s + up(own));
+    char* d_agents = s + up(own) + up(own * 4);
+    auto* d_status = reinterpret_cast<unsigned long long*>(d_agents + up(size_t(n_agents) * 40));
+    PF_CUDA(cudaMemsetAsync(d_status, 0, 16, ctx->stream));
+    if (agents) PF_CUDA(cudaMemsetAsync(d_agents, 0, size_t(n_agents) * 40, ctx->stream));
+    ctx->launches += pfk::launch_export_state(P.cell[ctx->parity] + off, ctx->aco() ? P.tour + off : nullptr, own,
+                                              uint32_t(W), uint32_t(ctx->row_begin), occ ? d_occ : nullptr,
+                                              index ? d_index : nullptr, agents ? d_agents : nullptr, n_agents,
+                                              d_status, ctx->stream);
+    double* top = nullptr;
+    if (ctx->aco() && (tau_top || tau_bot)) {
+        top = reinterpret_cast<double*>(P.tau[ctx->parity ^ 1] + off);
+        ctx->launches += pfk::launch_deinterleave_tau(top, top + own, P.tau[ctx->parity] + off, own, ctx->stream);
+    }
+    PF_CUDA(cudaEventRecord(ctx->io_event, ctx->stream));
+    PF_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->io_event, 0));
+    cudaError_t side_err = cudaSuccess;
+    std::thread side;
+    if (top) {
+        side = std::thread([&] {
+            cudaSetDevice(c.device);
+            cudaError_t e = cudaSuccess;
+            if (tau_top) e = ctx->stage[1].d2h(tau_top, top, own * 8, ctx->stream2);
+            if (e == cudaSuccess && tau_bot) e = ctx->stage[1].d2h(tau_bot, top + own, own * 8, ctx->stream2);
+            side_err = e;
+        });
+    }
+    unsigned long long status[2] = {0, 0};
+    cudaError_t e = ctx->stage[0].d2h(status, d_status, 16, ctx->stream);
+    if (e == cudaSuccess && occ) e = ctx->stage[0].d2h(occ, d_occ, own, ctx->stream);
+    if (e == cudaSuccess && index) e = ctx->stage[0].d2h(index, d_index, own * 4, ctx->stream);
+    if (e == cudaSuccess && agents) e = ctx->stage[0].d2h(agents, d_agents, size_t(n_agents) * 40, ctx->stream);
+    io_trace("store: occ/index/agents down");
+    if (side.joinable()) side.join();
+    io_trace("store: side join (pheromone)");
+    if (e == cudaSuccess) e = side_err;
+    if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(e));
+    if (status[1]) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
+    if (status[0] != n_agents) return fail(PF_ERR_STATE, "state corrupt: agents on the grid disagree with the agent count");
     return PF_OK;
 }
 
@@ -505,14 +675,19 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
     const pf_config& c = ctx->cfg;
     PF_CUDA(cudaSetDevice(c.device));
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->rows_owned == c.height && n_agents == ctx->reps[size_t(rep)].n_agents) {
+        if (int rc = store_whole(ctx, rep, occ, index, agents, n_agents, tau_top, tau_bot)) return rc;
+        if (step) *step = ctx->step;
+        return PF_OK;
+    }
+    IoTrace io_trace;
     const size_t W = size_t(c.width);
     const size_t own = size_t(ctx->rows_owned) * W;
     const size_t off = size_t(rep) * ctx->plane() + size_t(pfk::kGhost) * W;
     const pfk::Planes& P = ctx->args.p;
     std::unique_ptr<uint32_t[]> words_buf(new uint32_t[own]);
     uint32_t* words = words_buf.get();
-    PF_CUDA(cudaMemcpyAsync(words, P.cell[ctx->parity] + off, own * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    PF_CUDA(ctx->stage[0].d2h(words, P.cell[ctx->parity] + off, own * 4, ctx->stream));
     const size_t g0 = size_t(ctx->row_begin) * W;
     // ACO: pheromone is de-interleaved on the device into the owned rows of
     // the other ping-pong buffer (rewritten by the next step anyway) and tour
@@ -532,16 +707,16 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         side = std::thread([&, top, bot] {
             cudaSetDevice(c.device);
             cudaError_t e = cudaSuccess;
-            if (tau_top) e = cudaMemcpyAsync(tau_top + g0, top, own * 8, cudaMemcpyDeviceToHost, ctx->stream);
-            if (e == cudaSuccess && tau_bot)
-                e = cudaMemcpyAsync(tau_bot + g0, bot, own * 8, cudaMemcpyDeviceToHost, ctx->stream);
-            if (e == cudaSuccess)
-                e = cudaMemcpyAsync(per_agent.data(), d_pa, size_t(n_agents) * 8, cudaMemcpyDeviceToHost, ctx->stream);
+            Stager& st = ctx->stage[1];
+            if (tau_top) e = st.d2h(tau_top + g0, top, own * 8, ctx->stream);
+            if (e == cudaSuccess && tau_bot) e = st.d2h(tau_bot + g0, bot, own * 8, ctx->stream);
+            if (e == cudaSuccess) e = st.d2h(per_agent.data(), d_pa, size_t(n_agents) * 8, ctx->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
             side_err = e;
         });
     }
     std::atomic<bool> bad{false};
+    io_trace("store: words down");
     host_parallel(own, [&](size_t i0, size_t i1) {
         for (size_t i = i0; i < i1; ++i) {
             const uint32_t w = words[i];
@@ -566,6 +741,7 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         }
     });
     if (side.joinable()) side.join();
+    io_trace("store: conversion + side join");
     cudaFree(d_pa);
     if (side_err != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(side_err));
     if (agents && ctx->aco() && !bad) {
@@ -576,6 +752,7 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         });
     }
     if (bad) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
+    io_trace("store: tour fill");
     if (step) *step = ctx->step;
     return PF_OK;
 }

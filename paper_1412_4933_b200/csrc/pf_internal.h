@@ -59,8 +59,16 @@ int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agent
 // State upload / download layout transforms.
 int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s);
 int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s);
-int launch_scatter_tour(double* tour, const uint32_t* words, const double* per_agent, size_t n, cudaStream_t s);
 int launch_gather_tour(double* per_agent, const uint32_t* words, const double* tour, size_t n, cudaStream_t s);
+// Reference planes (window rows from g_lo) + AgentRecords -> buffer cell words
+// and cell-resident tour; *status = min(buffer cell << 3 | reason) over violations.
+int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* agents, uint32_t n_agents, uint32_t W,
+                        int H, long long g0, long long g_lo, size_t n, uint32_t* words, double* tour,
+                        unsigned long long* status, cudaStream_t s);
+// Owned cell words -> reference occupancy / index planes and AgentRecords
+// (40-byte pf_agent, by id); status[0] += agent cells, status[1] += bad ids.
+int launch_export_state(const uint32_t* words, const double* tour, size_t n, uint32_t W, uint32_t row0, uint8_t* occ,
+                        uint32_t* index, void* agents, uint32_t n_agents, unsigned long long* status, cudaStream_t s);
 int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                         const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
                         double* uni, double* nrm, cudaStream_t s);

@@ -362,19 +362,102 @@ __global__ void deinterleave_tau_kernel(double* top, double* bot, const double2*
     }
 }
 
-// tour[cell] = per_agent[id - 1] for agent cells (cell-resident tour layout).
-__global__ void scatter_tour_kernel(double* tour, const uint32_t* words, const double* per_agent, size_t n) {
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        const uint32_t w = words[i];
-        tour[i] = (w != 0u && w != pfdev::kWall) ? per_agent[(w & pfdev::kIdMask) - 1] : 0.0;
-    }
-}
-
 // per_agent[id - 1] = tour[cell] for agent cells.
 __global__ void gather_tour_kernel(double* per_agent, const uint32_t* words, const double* tour, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t w = words[i];
         if (w != 0u && w != pfdev::kWall) per_agent[(w & pfdev::kIdMask) - 1] = tour[i];
+    }
+}
+
+// State import: the check_consistency-style audit (src/state.cpp:77-110) of
+// the uploaded reference planes and their conversion to cell words, per
+// buffer cell. Buffer row b is global row g0 + b; rows outside the grid are
+// walls; occ/index hold the window rows from g_lo. Agent records are the
+// 40-byte pf_agent as five u64 words (see export_state_kernel). The first
+// violating buffer cell is reported as status = min(cell << 3 | reason), with
+// the reasons of pf_load_state.
+__global__ void import_state_kernel(const uint8_t* __restrict__ occ, const uint32_t* __restrict__ index,
+                                    const unsigned long long* __restrict__ agents, uint32_t n_agents, uint32_t W,
+                                    int H, long long g0, long long g_lo, size_t n, uint32_t* __restrict__ words,
+                                    double* __restrict__ tour, unsigned long long* status) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const long long g = g0 + (long long)(i / W);
+        const uint32_t col = uint32_t(i % W);
+        uint32_t w = pfdev::kWall;
+        double t = 0.0;
+        unsigned why = 0;
+        if (g >= 0 && g < H) {
+            const size_t wi = size_t(g - g_lo) * W + col;
+            const uint32_t id = index[wi];
+            const uint32_t o = occ[wi];
+            w = 0u;
+            if ((id == 0u) != (o == 0u)) why = 1;
+            else if (id != 0u) {
+                if (id > n_agents) why = 2;
+                else {
+                    const unsigned long long* a = agents + size_t(id - 1) * 5;
+                    const unsigned long long q0 = a[0], q1 = a[1];
+                    const uint32_t grp = uint32_t(q0 >> 32) & 0xFFu;
+                    if (uint32_t(q0) != id) why = 3;
+                    else if (int32_t(uint32_t(q1)) != g || int32_t(uint32_t(q1 >> 32)) != int32_t(col)) why = 4;
+                    else if (grp != o || (grp != 1u && grp != 2u)) why = 5;
+                    else {
+                        w = id | ((a[4] & 0xFFull) ? pfdev::kCrossedBit : 0u) | (grp << 30);
+                        t = __longlong_as_double(static_cast<long long>(a[3]));
+                    }
+                }
+            }
+        }
+        if (why) {
+            atomicMin(status, (static_cast<unsigned long long>(i) << 3) | why);
+            w = 0u;
+        }
+        words[i] = w;
+        if (tour) tour[i] = t;
+    }
+}
+
+// Whole-grid export into the reference's SimState planes (the inverse of the
+// host conversion in pf_load_state): per owned cell, occupancy (u8) and index
+// (u32) in row-major order, and for an agent cell its AgentRecord
+// (inc/grid.hpp:84-93, 40 bytes as five u64 words: index | group << 32,
+// row | col << 32, future_row | future_col << 32 (= position after the
+// reset phase, src/engine.cpp:183-193), tour_length, crossed; padding zero).
+// status[0] += agent cells, status[1] += cells with an out-of-range id.
+__global__ void export_state_kernel(const uint32_t* __restrict__ words, const double* __restrict__ tour, size_t n,
+                                    uint32_t W, uint32_t row0, uint8_t* __restrict__ occ,
+                                    uint32_t* __restrict__ index, unsigned long long* __restrict__ agents,
+                                    uint32_t n_agents, unsigned long long* status) {
+    unsigned long long found = 0, bad = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        const uint32_t id = w & pfdev::kIdMask;
+        if (occ) occ[i] = uint8_t(w ? (w >> 30) : 0u);
+        if (index) index[i] = w ? id : 0u;
+        if (!w) continue;
+        if (id == 0u || id > n_agents) {
+            ++bad;
+            continue;
+        }
+        ++found;
+        if (agents) {
+            const unsigned long long row = uint32_t(row0 + uint32_t(i / W)), col = uint32_t(i % W);
+            unsigned long long* a = agents + size_t(id - 1) * 5;
+            a[0] = id | (static_cast<unsigned long long>(w >> 30) << 32);
+            a[1] = row | (col << 32);
+            a[2] = row | (col << 32);
+            a[3] = tour ? static_cast<unsigned long long>(__double_as_longlong(tour[i])) : 0ull;
+            a[4] = (w & pfdev::kCrossedBit) ? 1ull : 0ull;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        found += __shfl_xor_sync(0xFFFFFFFFu, found, o);
+        bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (found) atomicAdd(&status[0], found);
+        if (bad) atomicAdd(&status[1], bad);
     }
 }
 
@@ -423,8 +506,17 @@ int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t
     deinterleave_tau_kernel<<<148 * 8, 256, 0, s>>>(top, bot, src, n);
     return 1;
 }
-int launch_scatter_tour(double* tour, const uint32_t* words, const double* per_agent, size_t n, cudaStream_t s) {
-    scatter_tour_kernel<<<148 * 8, 256, 0, s>>>(tour, words, per_agent, n);
+int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* agents, uint32_t n_agents, uint32_t W,
+                        int H, long long g0, long long g_lo, size_t n, uint32_t* words, double* tour,
+                        unsigned long long* status, cudaStream_t s) {
+    import_state_kernel<<<148 * 8, 256, 0, s>>>(occ, index, static_cast<const unsigned long long*>(agents), n_agents,
+                                                W, H, g0, g_lo, n, words, tour, status);
+    return 1;
+}
+int launch_export_state(const uint32_t* words, const double* tour, size_t n, uint32_t W, uint32_t row0, uint8_t* occ,
+                        uint32_t* index, void* agents, uint32_t n_agents, unsigned long long* status, cudaStream_t s) {
+    export_state_kernel<<<148 * 8, 256, 0, s>>>(words, tour, n, W, row0, occ, index,
+                                                static_cast<unsigned long long*>(agents), n_agents, status);
     return 1;
 }
 int launch_gather_tour(double* per_agent, const uint32_t* words, const double* tour, size_t n, cudaStream_t s) {
