@@ -64,10 +64,8 @@ constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
 constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
-#ifndef PF_BITS_QCAP
-#define PF_BITS_QCAP 1024
-#endif
-constexpr int QCAP = PF_BITS_QCAP;  // work-list capacity (overflow is handled in place)
+constexpr int NU = DROWS * SS;   // intent units (>= resolution units AROWS * SS)
+static_assert(NU * 32 < (1 << 16), "work-list bit counts must fit 16 bits");
 
 struct Smem {
     uint32_t word[RING][SW];  // rows are 1,056 B: every row start is 16-byte aligned for TMA
@@ -78,10 +76,18 @@ struct Smem {
     uint32_t K[3][AROWS][SS];
     uint32_t G[RT][SS];
     uint32_t dirty[RT];  // owned row has an arrival or a vacate
-    uint32_t queue[QCAP];  // (unit << 5) | bit
+    // Scalar work list (S1 draws, then reused for S2 contested cells): one
+    // entry per unit with work, in the order a packed counter handed out
+    // (entry count << 16 | bit count, one native 32-bit shared atomic; at
+    // most NU * 32 < 2^16 bits), so qp (first rank of the entry) is sorted
+    // and rank r maps to its (unit, bit) by binary search. Bounded by the
+    // unit count: it cannot overflow.
+    uint32_t qu[NU];  // unit
+    uint32_t qm[NU];  // its bits
+    uint32_t qp[NU];  // rank of its first bit
     unsigned long long mbar[2];
+    uint32_t qc[2];  // [0] S1 draws, [1] S2 contested cells
     int item;
-    uint32_t nq[2];  // work-list fill: [0] S1 draws, [1] S2 contested cells (the list is reused)
     uint32_t cnt[3];
 };
 
@@ -187,19 +193,40 @@ __device__ __forceinline__ void grant(Smem& sm, int rr, int si, int k, uint32_t 
     }
 }
 
-// Append the set bits of `mask` for unit u to work list `list`; returns the
-// bits that did not fit (to be processed in place).
-__device__ __forceinline__ uint32_t enqueue(Smem& sm, int u, uint32_t mask, int list) {
-    const uint32_t n = __popc(mask);
-    const uint32_t pos = atomicAdd(&sm.nq[list], n);
-    uint32_t overflow = 0u;
-    for (uint32_t i = 0; i < n; ++i) {
-        const int j = __ffs(mask) - 1;
-        mask &= mask - 1u;
-        if (pos + i < uint32_t(QCAP)) sm.queue[pos + i] = (uint32_t(u) << 5) | uint32_t(j);
-        else overflow |= 1u << j;
+// Add unit u's bits `mask` to work list `list`.
+__device__ __forceinline__ void enqueue(Smem& sm, int u, uint32_t mask, int list) {
+    const uint32_t old = atomicAdd(&sm.qc[list], (1u << 16) | uint32_t(__popc(mask)));
+    const int e = int(old >> 16);
+    sm.qu[e] = uint32_t(u);
+    sm.qm[e] = mask;
+    sm.qp[e] = old & 0xFFFFu;
+}
+
+// Position of the k-th (0-based) set bit of m.
+__device__ __forceinline__ int nth_bit(uint32_t m, int k) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const int c = __popc(m & ((1u << w) - 1u));
+        if (k >= c) {
+            k -= c;
+            m >>= w;
+            pos += w;
+        }
     }
-    return overflow;
+    return pos;
+}
+
+// Work-list rank r -> (unit, bit), n entries.
+__device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t r, int& u, int& j) {
+    int lo = 0, hi = int(n) - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sm.qp[mid] <= r) lo = mid;
+        else hi = mid - 1;
+    }
+    u = int(sm.qu[lo]);
+    j = nth_bit(sm.qm[lo], int(r - sm.qp[lo]));
 }
 
 }  // namespace
@@ -227,16 +254,20 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
         const int W = a.k.W;
         const int b = kGhost + r0 + di - 2;
         const int c = c0 + 32 * (si - 1) + j;
-        double num[8];
+        // All eight neighbour loads are issued before any is used (they are
+        // in bounds for every agent cell: rows b-1 .. b+1 lie inside the
+        // buffer and a column step off the row lands in the adjacent row).
+        const double* t0 = reinterpret_cast<const double*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
+        double tn[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            num[i] = 0.0;
-            if (open >> i & 1u) {
-                const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-                const double* t = reinterpret_cast<const double*>(tin + size_t(b + kDR[code]) * W + (c + kDC[code]));
-                num[i] = __dmul_rn(pheromone_term(a.kc, __ldg(t + (bottom ? 1 : 0))), __ldg(&a.kc->eta[i]));
-            }
+            const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
+            tn[i] = __ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code]));
         }
+        double num[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            num[i] = (open >> i & 1u) ? __dmul_rn(pheromone_term(a.kc, tn[i]), __ldg(&a.kc->eta[i])) : 0.0;
         s = aco_choose(num, open, seed, step, id);
     }
     return bottom ? 7 - kSlotCodeTop[s] : kSlotCodeTop[s];
@@ -390,7 +421,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         }
         for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
         if (threadIdx.x < RT) sm.dirty[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) sm.nq[0] = sm.nq[1] = 0u;
+        if (threadIdx.x == 0) sm.qc[0] = sm.qc[1] = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
         // ------------------------------------------------------------ S0
@@ -449,22 +480,19 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             d[6] = T & n.ep;  // Top forward: (+1, 0)
             d[1] = B & n.em;  // Bottom forward: (-1, 0)
             const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
-            uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) slow = enqueue(sm, u, slow, 0);
-            while (slow) {  // queue overflow: draw in place
-                const int j = __ffs(slow) - 1;
-                slow &= slow - 1u;
-                d[draw_intent<ACO>(a, sm, base, tin, di, si, j, bit(B, j) != 0u, r0, c0, seed, step)] |= 1u << j;
-            }
+            const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
+            if (slow) enqueue(sm, u, slow, 0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) sm.D[q][di][si] = d[q];
         }
         __syncthreads();
-        // Queued draws (the barrier is skipped, uniformly, when none were queued).
-        if (const uint32_t nq = min(sm.nq[0], uint32_t(QCAP))) {
+        // Draws, spread evenly over the CTA (the barrier is skipped,
+        // uniformly, when there are none).
+        if (const uint32_t nq = sm.qc[0] & 0xFFFFu) {
+            const uint32_t ne = sm.qc[0] >> 16;
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                const uint32_t q = sm.queue[e];
-                const int u = int(q >> 5), j = int(q & 31u);
+                int u, j;
+                list_entry(sm, ne, e, u, j);
                 const int di = u / SS, si = u - di * SS;
                 const bool bottom = bit(sm.v31[slot(base, di + 1)][si], j) != 0u;
                 const int code = draw_intent<ACO>(a, sm, base, tin, di, si, j, bottom, r0, c0, seed, step);
@@ -496,18 +524,14 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (win[q]) grant(sm, ai - 1, si, q, win[q]);
-            uint32_t multi = twos ? enqueue(sm, u, twos, 1) : 0u;
-            while (multi) {  // queue overflow: draw in place
-                const int j = __ffs(multi) - 1;
-                multi &= multi - 1u;
-                set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
-            }
+            if (twos) enqueue(sm, u, twos, 1);
         }
         __syncthreads();
-        if (const uint32_t nq = min(sm.nq[1], uint32_t(QCAP))) {
+        if (const uint32_t nq = sm.qc[1] & 0xFFFFu) {
+            const uint32_t ne = sm.qc[1] >> 16;
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                const uint32_t q = sm.queue[e];
-                const int u = int(q >> 5), j = int(q & 31u);
+                int u, j;
+                list_entry(sm, ne, e, u, j);
                 const int ai = u / SS, si = u - ai * SS;
                 set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
             }

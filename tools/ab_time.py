@@ -1,6 +1,9 @@
 """Same-box A/B step timing of tools/debug/lib_base.so vs lib_new.so (dev tool).
 
-    python tools/ab_time.py c5_lem c4_aco_x64 [--rounds 3] [--steps 100]
+    python tools/ab_time.py c5_lem c4_aco_x64 [--rounds 3] [--steps 100] [--skip 0]
+
+--skip runs that many extra steps before the timed window (the 480^2 crowds
+jam after ~125 steps, so --skip 200 times the congested regime).
 """
 import argparse
 import os
@@ -12,10 +15,10 @@ CODE = r'''
 import sys, os
 sys.path.insert(0, os.getcwd())
 import bench, paper_1412_4933_b200 as p
-steps = int(sys.argv[1])
-for name in sys.argv[2:]:
+steps, skip = int(sys.argv[1]), int(sys.argv[2])
+for name in sys.argv[3:]:
     cfg, reps, desc = bench.scenario(name)
-    e = p.Ensemble(cfg, replicas=reps); e.run(5)
+    e = p.Ensemble(cfg, replicas=reps); e.run(5 + skip)
     tot, _ = e.time_steps(steps)
     print(f"{name} {tot/steps*1e3:.2f}", flush=True); e.close()
 '''
@@ -24,12 +27,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("workloads", nargs="+")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--steps", type=int, default=100)
+ap.add_argument("--skip", type=int, default=0)
 args = ap.parse_args()
 res = {}
 for r in range(args.rounds):
     for tag in ("base", "new"):
         env = dict(os.environ, PEDFLOW_B200_LIB=os.path.join(ROOT, "tools", "debug", f"lib_{tag}.so"))
-        out = subprocess.run([sys.executable, "-c", CODE, str(args.steps)] + args.workloads, env=env, cwd=ROOT,
+        out = subprocess.run([sys.executable, "-c", CODE, str(args.steps), str(args.skip)] + args.workloads, env=env, cwd=ROOT,
                              capture_output=True, text=True).stdout
         for line in out.split("\n"):
             if line.strip():
