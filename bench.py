@@ -379,8 +379,8 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
 
     def planes(side, recv):
         hh = c.halo(0, side, recv)
-        return [_device_tensor(pt, nb, local) for pt, nb in ((hh.cells, hh.cell_bytes), (hh.tau, hh.tau_bytes),
-                                                             (hh.tour, hh.tour_bytes)) if nb]
+        return [_device_tensor(pt, nb, local) for pt, nb in ((hh.cells, hh.cell_bytes), (hh.occ, hh.occ_bytes),
+                                                             (hh.tau, hh.tau_bytes), (hh.tour, hh.tour_bytes)) if nb]
 
     barrier()
     t0 = time.perf_counter()

@@ -32,7 +32,7 @@ extern "C" {
 #define PF_MODEL_LEM 0
 #define PF_MODEL_ACO 1
 
-#define PF_KERNEL_FUSED 0    /* one bit-sliced kernel per step (default) */
+#define PF_KERNEL_FUSED 0    /* one bit-sliced kernel per step on occupancy bit planes (default) */
 #define PF_KERNEL_PIPELINE 1 /* propose / resolve / commit, three kernels per step */
 #define PF_KERNEL_TILE 2     /* one kernel per step, scalar per-cell shared-memory tile */
 
@@ -76,6 +76,7 @@ typedef struct pf_halo_rows {
     void* cells; size_t cell_bytes; /* PF_GHOST_ROWS rows of u32 cell words */
     void* tau;   size_t tau_bytes;  /* PF_GHOST_ROWS rows of {f64 top, f64 bottom} (ACO) */
     void* tour;  size_t tour_bytes; /* 1 row of f64 tour lengths (ACO) */
+    void* occ;   size_t occ_bytes;  /* PF_GHOST_ROWS rows of occupancy bit planes (PF_KERNEL_FUSED; else NULL) */
 } pf_halo_rows;
 
 const char* pf_last_error(void);

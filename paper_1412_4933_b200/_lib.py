@@ -67,6 +67,7 @@ class PfHalo(C.Structure):
         ("cells", C.c_void_p), ("cell_bytes", C.c_size_t),
         ("tau", C.c_void_p), ("tau_bytes", C.c_size_t),
         ("tour", C.c_void_p), ("tour_bytes", C.c_size_t),
+        ("occ", C.c_void_p), ("occ_bytes", C.c_size_t),
     ]
 
 

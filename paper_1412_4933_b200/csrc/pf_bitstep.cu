@@ -1,4 +1,21 @@
-// Bit-sliced fused step kernel (the default product path, PF_KERNEL_FUSED).
+// Bit-sliced fused step kernel on occupancy bit planes (the default product
+// path, PF_KERNEL_FUSED).
+//
+// State representation:
+//   occ[parity]  ping-pong occupancy bit planes, one uint2 {v30, v31} per
+//                32-cell row segment: bit j of v30 / v31 is bit 30 / 31 of the
+//                cell word of column 32*seg + j (Top = v30 & ~v31, Bottom =
+//                v31 & ~v30, Empty = ~(v30 | v31), wall = both). Rows are
+//                padded with two wall segments on each side, so a strip's
+//                plane window is one aligned run of NS + 4 segments.
+//   cell         the 32-bit cell words (id | crossed | group), updated IN
+//                PLACE and meaningful only where the planes say "occupied":
+//                a step reads words only at cells occupied at its start
+//                (draw keys, arrival sources) and writes them only at cells
+//                empty at its start (arrivals), so the two sets never meet
+//                and no ping-pong copy of the 4 B/cell words is needed.
+//                Vacated cells keep a stale word; state export masks words
+//                with the planes (launch_sanitize_words).
 //
 // The per-step update (StepEngine::step, src/engine.cpp:53-193) is evaluated
 // on 32-cell row segments held as 32-bit masks, so the common work costs one
@@ -7,15 +24,11 @@
 // those are compacted into shared-memory work lists so every lane takes one.
 //
 // Persistent column sweep: a CTA owns a strip of NS 32-column segments and a
-// run of consecutive RT-row tiles. The step-start cell words of the strip live
-// in a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
-// rows); while a tile is processed, TMA bulk copies (cp.async.bulk +
-// mbarrier) bring the next tile's RT new rows, so every row is loaded and
-// balloted once and the load latency hides behind the compute.
+// run of consecutive RT-row tiles. The step-start planes of the strip live in
+// a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
+// rows); while a tile is processed, TMA bulk copies (cp.async.bulk + mbarrier,
+// one 96-byte row each) bring the next tile's RT new rows.
 //
-//   S0 stage   ballot the new rows into occupancy planes v30 / v31 (bits 30/31
-//              of the word: Top = v30 & ~v31, Bottom = v31 & ~v30,
-//              Empty = ~(v30 | v31)).
 //   S1 intent  thread per segment-row: forward moves (F open, no draw,
 //              src/lem.cpp:23-26, src/aco.cpp:60-63) and boxed-in agents in
 //              bit logic; agents that must draw are queued, then run the
@@ -27,9 +40,10 @@
 //              row-major contender order), at-least-two detection in bit logic;
 //              contested cells are queued for the keyed draw. Winner code
 //              planes (A, K0..K2); granted moves are OR-ed onto the sources.
-//   S3 commit  warp per segment-row, lane = column: new cell word (arrival /
-//              vacate / unchanged), crossing + counters, ACO evaporation +
-//              deposit and tour (src/engine.cpp:124-175).
+//   S3 commit  warp per row, lane = column: arrivals (source word, crossing,
+//              counters, tour), the new occupancy planes (vacates cleared,
+//              arrivals set by group ballots), ACO evaporation + deposit over
+//              every cell (src/engine.cpp:124-175).
 #include <algorithm>
 
 #include "pf_internal.h"
@@ -51,15 +65,9 @@ constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
 constexpr int RING = PF_BITS_RING;
 constexpr bool kCrossPrefetch = RING >= 2 * SR;
 static_assert(RING >= SR + RT, "the ring must hold a window and the next tile's rows");
-constexpr int SS = NS + 2;       // staged segments: -1 .. NS
-// Staged columns: the strip plus a 4-column halo on each side (the dependency
-// radius is 3; 4 keeps TMA rows 16-byte aligned). Bit j of plane segment si
-// (si = 0 .. NS+1, segment si-1 of the strip) is staged column
-// 32 * si + j - WOFF; the halo segments 0 and NS+1 only have bits 28..31 and
-// 0..3 staged.
-constexpr int HALO = 4;
-constexpr int SW = NS * 32 + 2 * HALO;
-constexpr int WOFF = 32 - HALO;
+constexpr int SS = NS + 2;       // intent / resolution segments: -1 .. NS
+constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index = si + 1)
+static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
 constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
@@ -68,14 +76,12 @@ constexpr int NU = DROWS * SS;   // intent units (>= resolution units AROWS * SS
 static_assert(NU * 32 < (1 << 16), "work-list bit counts must fit 16 bits");
 
 struct Smem {
-    uint32_t word[RING][SW];  // rows are 1,056 B: every row start is 16-byte aligned for TMA
-    uint32_t v30[RING][SS];
-    uint32_t v31[RING][SS];
-    uint32_t D[8][DROWS][SS];
+    uint2 pl[RING][SP];             // staged {v30, v31} planes; pl[.][si + 1] = segment si
+    uint32_t D[8][DROWS][SS + 2];   // intent planes, D[.][.][si + 1]; the end columns stay 0
     uint32_t A[AROWS][SS];
     uint32_t K[3][AROWS][SS];
-    uint32_t G[RT][SS];
-    uint32_t dirty[RT];  // owned row has an arrival or a vacate
+    uint32_t G[2][RT][SS];          // grants (vacates) onto owned rows, double-buffered per tile
+    uint32_t dirty[2][RT];          // owned row has an arrival or a vacate
     // Scalar work list (S1 draws, then reused for S2 contested cells): one
     // entry per unit with work, in the order a packed counter handed out
     // (entry count << 16 | bit count, one native 32-bit shared atomic; at
@@ -86,7 +92,7 @@ struct Smem {
     uint32_t qm[NU];  // its bits
     uint32_t qp[NU];  // rank of its first bit
     unsigned long long mbar[2];
-    uint32_t qc[2];  // [0] S1 draws, [1] S2 contested cells
+    uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
     int item;
     uint32_t cnt[3];
 };
@@ -134,6 +140,8 @@ __device__ __forceinline__ int slot(int base, int sr) {
     return s >= RING ? s - RING : s;
 }
 
+__device__ __forceinline__ uint32_t empty_of(uint2 p) { return ~(p.x | p.y); }
+
 // Emptiness around one intent unit: the eight neighbour planes, shifted so
 // bit j is the neighbour of column j.
 struct Around {
@@ -141,27 +149,26 @@ struct Around {
 };
 
 __device__ __forceinline__ Around around(const Smem& sm, int base, int sr, int si) {
-    const int rm = slot(base, sr - 1), r0 = slot(base, sr), rp = slot(base, sr + 1);
-    auto E = [&](int row, int seg) -> uint32_t {
-        return (seg < 0 || seg >= SS) ? 0u : ~(sm.v30[row][seg] | sm.v31[row][seg]);
-    };
+    const uint2* rm = sm.pl[slot(base, sr - 1)] + si + 1;
+    const uint2* r0 = sm.pl[slot(base, sr)] + si + 1;
+    const uint2* rp = sm.pl[slot(base, sr + 1)] + si + 1;
     Around n;
-    n.em = E(rm, si);
-    n.ep = E(rp, si);
-    const uint32_t e0 = E(r0, si);
-    n.emL = from_left(n.em, E(rm, si - 1));
-    n.emR = from_right(n.em, E(rm, si + 1));
-    n.e0L = from_left(e0, E(r0, si - 1));
-    n.e0R = from_right(e0, E(r0, si + 1));
-    n.epL = from_left(n.ep, E(rp, si - 1));
-    n.epR = from_right(n.ep, E(rp, si + 1));
+    n.em = empty_of(rm[0]);
+    n.ep = empty_of(rp[0]);
+    const uint32_t e0 = empty_of(r0[0]);
+    n.emL = from_left(n.em, empty_of(rm[-1]));
+    n.emR = from_right(n.em, empty_of(rm[1]));
+    n.e0L = from_left(e0, empty_of(r0[-1]));
+    n.e0R = from_right(e0, empty_of(r0[1]));
+    n.epL = from_left(n.ep, empty_of(rp[-1]));
+    n.epR = from_right(n.ep, empty_of(rp[1]));
     return n;
 }
 
 // Claims on the destinations of resolution unit (row ai-1, segment si).
 __device__ __forceinline__ void claims(const Smem& sm, int ai, int si, uint32_t (&C)[8]) {
-    auto D = [&](int k, int row, int seg) -> uint32_t { return (seg < 0 || seg >= SS) ? 0u : sm.D[k][row][seg]; };
     const int dm = ai, d0 = ai + 1, dp = ai + 2;  // intent rows of rr-1, rr, rr+1
+    auto D = [&](int k, int row, int s) -> uint32_t { return sm.D[k][row][s + 1]; };
     C[0] = from_left(D(7, dm, si), D(7, dm, si - 1));
     C[1] = D(6, dm, si);
     C[2] = from_right(D(5, dm, si), D(5, dm, si + 1));
@@ -177,25 +184,25 @@ __device__ __forceinline__ void claims(const Smem& sm, int ai, int si, uint32_t 
 
 // OR the source-grant bits of winners `wk` (direction k) at destination row
 // rr of segment si into G.
-__device__ __forceinline__ void grant(Smem& sm, int rr, int si, int k, uint32_t wk) {
+__device__ __forceinline__ void grant(Smem& sm, int cur, int rr, int si, int k, uint32_t wk) {
     const int g = rr + kDR[k];
     if (g < 0 || g >= RT) return;
-    sm.dirty[g] = 1u;
+    sm.dirty[cur][g] = 1u;
     const int dc = kDC[k];
     if (dc == 0) {
-        atomicOr(&sm.G[g][si], wk);
+        atomicOr(&sm.G[cur][g][si], wk);
     } else if (dc < 0) {
-        atomicOr(&sm.G[g][si], wk >> 1);
-        if ((wk & 1u) && si > 0) atomicOr(&sm.G[g][si - 1], 0x80000000u);
+        atomicOr(&sm.G[cur][g][si], wk >> 1);
+        if ((wk & 1u) && si > 0) atomicOr(&sm.G[cur][g][si - 1], 0x80000000u);
     } else {
-        atomicOr(&sm.G[g][si], wk << 1);
-        if ((wk >> 31) && si + 1 < SS) atomicOr(&sm.G[g][si + 1], 1u);
+        atomicOr(&sm.G[cur][g][si], wk << 1);
+        if ((wk >> 31) && si + 1 < SS) atomicOr(&sm.G[cur][g][si + 1], 1u);
     }
 }
 
 // Add unit u's bits `mask` to work list `list`.
-__device__ __forceinline__ void enqueue(Smem& sm, int u, uint32_t mask, int list) {
-    const uint32_t old = atomicAdd(&sm.qc[list], (1u << 16) | uint32_t(__popc(mask)));
+__device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t mask) {
+    const uint32_t old = atomicAdd(qc, (1u << 16) | uint32_t(__popc(mask)));
     const int e = int(old >> 16);
     sm.qu[e] = uint32_t(u);
     sm.qm[e] = mask;
@@ -232,12 +239,18 @@ __device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t 
 }  // namespace
 
 // Intent of the draw-path agent at bit j of intent unit (di, si):
-// lem_select / aco_select (src/lem.cpp:28-60, src/aco.cpp:64-92).
+// lem_select / aco_select (src/lem.cpp:28-60, src/aco.cpp:64-92). The agent's
+// id (the selection key, src/engine.cpp:82) is read from its cell word: the
+// cell is occupied at step start, so no thread writes it during this step.
 template <bool ACO>
-__device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, int base,
+__device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, int base, const uint32_t* cells,
                                            const double2* __restrict__ tin, int di, int si, int j, bool bottom,
                                            int r0, int c0, uint64_t seed, uint32_t step) {
     const int sr = di + 1;
+    const int W = a.k.W;
+    const int b = kGhost + r0 + di - 2;
+    const int c = c0 + 32 * (si - 1) + j;
+    const uint32_t id = cells[size_t(b) * W + c] & kIdMask;
     const Around n = around(sm, base, sr, si);
     uint32_t open;  // goal-relative slots F FL FR L R B BL BR
     if (!bottom)
@@ -246,14 +259,10 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
     else
         open = bit(n.em, j) | bit(n.emR, j) << 1 | bit(n.emL, j) << 2 | bit(n.e0R, j) << 3 | bit(n.e0L, j) << 4 |
                bit(n.ep, j) << 5 | bit(n.epR, j) << 6 | bit(n.epL, j) << 7;
-    const uint32_t id = sm.word[slot(base, sr)][si * 32 + j - WOFF] & kIdMask;
     int s;
     if (!ACO) {
         s = lem_choose(a.kc, open, seed, step, id);
     } else {
-        const int W = a.k.W;
-        const int b = kGhost + r0 + di - 2;
-        const int c = c0 + 32 * (si - 1) + j;
         // All eight neighbour loads are issued before any is used (they are
         // in bounds for every agent cell: rows b-1 .. b+1 lie inside the
         // buffer and a column step off the row lands in the adjacent row).
@@ -287,23 +296,21 @@ __device__ __forceinline__ int draw_winner(const StepArgs& a, const Smem& sm, in
     return resolve(m, seed, step, uint64_t(grow) * uint64_t(a.k.W) + uint64_t(gcol));
 }
 
-__device__ __forceinline__ void set_winner(Smem& sm, int ai, int si, int j, int k) {
+__device__ __forceinline__ void set_winner(Smem& sm, int cur, int ai, int si, int j, int k) {
     const uint32_t b = 1u << j;
     if (k & 1) atomicOr(&sm.K[0][ai][si], b);
     if (k & 2) atomicOr(&sm.K[1][ai][si], b);
     if (k & 4) atomicOr(&sm.K[2][ai][si], b);
-    grant(sm, ai - 1, si, k, b);
+    grant(sm, cur, ai - 1, si, k, b);
 }
 
 // One work item: a chunk of consecutive RT-row tiles of one strip of one
-// replica, with the strip's column window.
+// replica.
 struct Item {
     int rep, strip, chunk, c0, t_first, t_end;
-    int col_lo, fill_lo, fill_hi;  // arena columns [col_lo, ...) land in staged columns [fill_lo, fill_hi)
 };
 
-__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
-                                            int W) {
+__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item) {
     Item it;
     it.rep = item / (strips * n_chunks);
     it.strip = (item / n_chunks) % strips;
@@ -311,37 +318,26 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
     it.c0 = it.strip * (NS * 32);
     it.t_first = it.chunk * tiles_per_item;
     it.t_end = min(it.t_first + tiles_per_item, n_tiles);
-    it.col_lo = max(it.c0 - HALO, 0);
-    const int col_hi = min(it.c0 + 32 * NS + HALO, W);  // 16-byte aligned: c0 % 256 == 0, W % 16 == 0
-    it.fill_lo = it.col_lo - (it.c0 - HALO);
-    it.fill_hi = col_hi - (it.c0 - HALO);
     return it;
 }
 
-// Issue the TMA loads of `nrows` staged rows (tile rows first_sr.., relative
-// to the tile at r0) of item `it` into their ring slots, completing on
-// mbarrier m; the strip's columns outside the arena and rows past the end of
-// the buffer are written as walls. Called by one full warp.
+// Issue the TMA loads of `nrows` staged plane rows (tile rows first_sr..,
+// relative to the tile at r0) of item `it` into their ring slots, completing
+// on mbarrier m; rows past the end of the buffer are written as walls. Each
+// row is one 16-byte-aligned run of SP segments (the row padding holds walls
+// beyond the grid's columns). Called by one full warp.
 __device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parity, const Item& it, int r0, int base,
                                           int first_sr, int nrows, unsigned long long* m) {
     const int lane = threadIdx.x & 31;
-    const int W = a.k.W;
-    const uint32_t* cin = a.p.cell[parity] + size_t(it.rep) * a.p.plane;
+    const uint2* src = a.p.occ[parity] + size_t(it.rep) * a.p.occ_plane + size_t(it.strip) * NS;
     const int b_first = kGhost + r0 - 3 + first_sr;
     const int nvalid = max(0, min(nrows, a.rows_buf - b_first));
-    const int ncols = it.fill_hi - it.fill_lo;
-    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(ncols) * 4u);
+    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(SP * 8));
     __syncwarp();
     for (int i = lane; i < nvalid; i += 32)
-        bulk_g2s(&sm.word[slot(base, first_sr + i)][it.fill_lo], cin + size_t(b_first + i) * W + it.col_lo,
-                 uint32_t(ncols) * 4u, m);
-    const int nfill = SW - ncols;  // wall columns at the arena's left / right edge
-    for (int i = lane; i < nvalid * nfill; i += 32) {
-        const int r = i / nfill, c = i - r * nfill;
-        sm.word[slot(base, first_sr + r)][c < it.fill_lo ? c : it.fill_hi + (c - it.fill_lo)] = kWall;
-    }
-    for (int i = nvalid; i < nrows; ++i)
-        for (int c = lane; c < SW; c += 32) sm.word[slot(base, first_sr + i)][c] = kWall;
+        bulk_g2s(&sm.pl[slot(base, first_sr + i)][0], src + size_t(b_first + i) * a.p.wsp, uint32_t(SP * 8), m);
+    for (int i = nvalid * SP + lane; i < nrows * SP; i += 32)
+        sm.pl[slot(base, first_sr + i / SP)][i % SP] = make_uint2(kWall, kWall);
 }
 
 template <bool ACO>
@@ -363,6 +359,13 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         mbar_init(&sm.mbar[1], 1);
         fence_mbar_init();
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
+        sm.qc[0][0] = sm.qc[0][1] = sm.qc[1][0] = sm.qc[1][1] = 0u;
+    }
+    for (int i = threadIdx.x; i < 2 * RT * SS; i += NT) (&sm.G[0][0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < 2 * RT; i += NT) (&sm.dirty[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < 8 * DROWS; i += NT) {  // the zero end columns of the intent planes
+        sm.D[i / DROWS][i % DROWS][0] = 0u;
+        sm.D[i / DROWS][i % DROWS][SS + 1] = 0u;
     }
     __syncthreads();
     // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         item = __shfl_sync(0xFFFFFFFFu, item, 0);
         if (lane == 0) sm.item = item;
         if (item < n_items) {
-            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
             load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
         }
     }
@@ -384,21 +387,23 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     uint32_t moved = 0, ntop = 0, nbot = 0;
     uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
     int base = 0;                               // ring slot of staged row 0 of the current tile
+    int cur = 0;                                // tile parity: G / dirty / work-list counters
+    uint32_t* const cells = a.p.cell[0];
     while (item < n_items) {
-    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
     const int rep = it.rep, c0 = it.c0;
     const uint64_t seed = __ldg(&a.rep[rep].seed);
     const int band = __ldg(&a.rep[rep].band);
     const size_t plane_base = size_t(rep) * a.p.plane;
-    uint32_t* __restrict__ cout = a.p.cell[parity ^ 1] + plane_base;
+    uint32_t* const cw = cells + plane_base;
+    uint2* const oout = a.p.occ[parity ^ 1] + size_t(rep) * a.p.occ_plane + size_t(it.strip) * NS + 2;
     const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
     double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + plane_base : nullptr;
     double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
     int next_base = 0;
 
     for (int t = it.t_first; t < it.t_end; ++t) {
-        const int k = t - it.t_first;  // tile index within the item (k == 0: full window)
-        const int r0 = t * RT;         // owned-local row of the tile
+        const int r0 = t * RT;               // owned-local row of the tile
         const uint32_t my_load = nload - 1;  // the load that brought this tile's new rows
         // Prefetch into the half of the ring this tile does not use (its
         // previous readers all passed the end-of-tile barrier): the next
@@ -414,66 +419,27 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item = nx;
                 if (kCrossPrefetch && nx < n_items) {
-                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta);
                     load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
                 }
             }
         }
-        for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[0][0])[i] = 0u;
-        if (threadIdx.x < RT) sm.dirty[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) sm.qc[0] = sm.qc[1] = 0u;
+        // Scratch of the NEXT tile (its last readers passed the previous
+        // end-of-tile barrier; its first writers come after this tile's).
+        for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[cur ^ 1][0][0])[i] = 0u;
+        if (threadIdx.x < RT) sm.dirty[cur ^ 1][threadIdx.x] = 0u;
+        if (threadIdx.x == 0) sm.qc[cur ^ 1][0] = sm.qc[cur ^ 1][1] = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
-
-        // ------------------------------------------------------------ S0
-        // Thread per new segment-row: eight 16-byte shared loads (chunk order
-        // rotated by lane, so a quarter-warp hits eight distinct bank groups),
-        // the top byte of each word packed with PRMT, bits 31 / 30 of four
-        // words gathered into a nibble by one multiply.
-        {
-            const int first = k == 0 ? 0 : 6;
-            for (int u = threadIdx.x; u < (SR - first) * SS; u += NT) {
-                const int sr = first + u / SS, si = u % SS;
-                const int rs = slot(base, sr);
-                auto nibbles = [](const uint4& q, uint32_t& n30, uint32_t& n31) {
-                    const uint32_t top =
-                        __byte_perm(__byte_perm(q.x, q.y, 0x0073), __byte_perm(q.z, q.w, 0x0073), 0x5410);
-                    n31 = ((top & 0x80808080u) * 0x00204081u) >> 28;
-                    n30 = (((top & 0x40404040u) * 0x00204081u) >> 27) & 0xFu;
-                };
-                uint32_t v30 = 0u, v31 = 0u;
-                if (si == 0 || si == SS - 1) {  // halo segment: 4 staged columns, the rest walls
-                    const bool left = si == 0;
-                    uint32_t n30, n31;
-                    nibbles(*reinterpret_cast<const uint4*>(&sm.word[rs][left ? 0 : SW - HALO]), n30, n31);
-                    v30 = left ? (0x0FFFFFFFu | n30 << 28) : (0xFFFFFFF0u | n30);
-                    v31 = left ? (0x0FFFFFFFu | n31 << 28) : (0xFFFFFFF0u | n31);
-                } else {
-                    const uint4* p = reinterpret_cast<const uint4*>(&sm.word[rs][si * 32 - WOFF]);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int c = (i + lane) & 7;
-                        uint32_t n30, n31;
-                        nibbles(p[c], n30, n31);
-                        v31 |= n31 << (4 * c);
-                        v30 |= n30 << (4 * c);
-                    }
-                }
-                sm.v30[rs][si] = v30;
-                sm.v31[rs][si] = v31;
-            }
-        }
-        __syncthreads();
 
         // ------------------------------------------------------------ S1
         // Intents for rows -2 .. RT+1, all staged segments (halo segments
         // only at the two columns next to the strip).
         for (int u = threadIdx.x; u < DROWS * SS; u += NT) {
             const int di = u / SS, si = u - di * SS;  // di = rr + 2
-            const int rs = slot(base, di + 1);
+            const uint2 p = sm.pl[slot(base, di + 1)][si + 1];
             const Around n = around(sm, base, di + 1, si);
-            const uint32_t v30 = sm.v30[rs][si], v31 = sm.v31[rs][si];
             const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
-            const uint32_t T = v30 & ~v31 & segmask, B = v31 & ~v30 & segmask;
+            const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
             uint32_t d[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) d[q] = 0u;
@@ -481,22 +447,22 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             d[1] = B & n.em;  // Bottom forward: (-1, 0)
             const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
             const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) enqueue(sm, u, slow, 0);
+            if (slow) enqueue(sm, &sm.qc[cur][0], u, slow);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sm.D[q][di][si] = d[q];
+            for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
         }
         __syncthreads();
         // Draws, spread evenly over the CTA (the barrier is skipped,
         // uniformly, when there are none).
-        if (const uint32_t nq = sm.qc[0] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[0] >> 16;
+        if (const uint32_t nq = sm.qc[cur][0] & 0xFFFFu) {
+            const uint32_t ne = sm.qc[cur][0] >> 16;
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                 int u, j;
                 list_entry(sm, ne, e, u, j);
                 const int di = u / SS, si = u - di * SS;
-                const bool bottom = bit(sm.v31[slot(base, di + 1)][si], j) != 0u;
-                const int code = draw_intent<ACO>(a, sm, base, tin, di, si, j, bottom, r0, c0, seed, step);
-                atomicOr(&sm.D[code][di][si], 1u << j);
+                const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
+                const int code = draw_intent<ACO>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
+                atomicOr(&sm.D[code][di][si + 1], 1u << j);
             }
             __syncthreads();
         }
@@ -517,23 +483,23 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
 #pragma unroll
             for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
             sm.A[ai][si] = ones;
-            if (ones && ai >= 1 && ai <= RT) sm.dirty[ai - 1] = 1u;
+            if (ones && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
             sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
             sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
             sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (win[q]) grant(sm, ai - 1, si, q, win[q]);
-            if (twos) enqueue(sm, u, twos, 1);
+                if (win[q]) grant(sm, cur, ai - 1, si, q, win[q]);
+            if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
         }
         __syncthreads();
-        if (const uint32_t nq = sm.qc[1] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[1] >> 16;
+        if (const uint32_t nq = sm.qc[cur][1] & 0xFFFFu) {
+            const uint32_t ne = sm.qc[cur][1] >> 16;
             for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                 int u, j;
                 list_entry(sm, ne, e, u, j);
                 const int ai = u / SS, si = u - ai * SS;
-                set_winner(sm, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
+                set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
             }
             __syncthreads();
         }
@@ -545,17 +511,10 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
             const int b = kGhost + lr;
             const int grow = a.row_begin + lr;
             const int rs = slot(base, rr + 3), ai = rr + 1;
-            if (!ACO && !sm.dirty[rr]) {
-                // Nothing arrives or leaves in this row: copy its 256 words
-                // with 16-byte shared loads / global stores (lane = 4 columns).
-                // (Not for ACO: the extra live registers cost it more in spills.)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int col = 128 * h + 4 * lane;
-                    if (c0 + col < W)  // W is a multiple of 16: a 4-word group is all in or all out
-                        *reinterpret_cast<uint4*>(cout + size_t(b) * W + c0 + col) =
-                            *reinterpret_cast<const uint4*>(&sm.word[rs][HALO + col]);
-                }
+            uint2* const orow = oout + size_t(b) * a.p.wsp;
+            if (!ACO && !sm.dirty[cur][rr]) {
+                // Nothing arrives or leaves in this row: its planes are copied.
+                if (lane < NS) orow[lane] = sm.pl[rs][lane + 2];
                 continue;
             }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
@@ -566,53 +525,47 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 for (int s = 0; s < NS; ++s)
                     tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
             }
+            uint2 mine = make_uint2(kWall, kWall);
 #pragma unroll
             for (int si = 1; si <= NS; ++si) {
                 const int gc = c0 + 32 * (si - 1) + lane;
                 const bool valid = gc < W;
-                const uint32_t Am = sm.A[ai][si], Gm = sm.G[rr][si];
-                const uint32_t w = sm.word[rs][si * 32 + lane - WOFF];
+                const uint32_t Am = sm.A[ai][si], Gm = sm.G[cur][rr][si];
+                uint2 np = sm.pl[rs][si + 1];
                 const size_t gi = row0 + 32 * (si - 1);
                 if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
-                    if (valid) {
-                        cout[gi] = w;
-                        if (ACO) {
-                            const double2 tt = tv[si - 1];
-                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
-                        }
+                    if (ACO && valid) {
+                        const double2 tt = tv[si - 1];
+                        tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
                     }
-                    continue;
-                }
-                uint32_t nw = w;
-                bool arrived = false;
-                uint32_t group = 0;
-                double tour_new = 0.0;
-                if (bit(Am, lane)) {
-                    const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                       bit(sm.K[2][ai][si], lane) << 2);
-                    const uint32_t sw = sm.word[slot(base, rr + 3 + kDR[kc])][si * 32 + lane + kDC[kc] - WOFF];
-                    group = sw >> 30;
-                    nw = sw;
-                    if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
-                        nw |= kCrossedBit;
-                        if (valid) {
+                } else {
+                    const bool arrived = bit(Am, lane) != 0u;
+                    uint32_t group = 0;
+                    double tour_new = 0.0;
+                    if (arrived) {
+                        const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
+                                           bit(sm.K[2][ai][si], lane) << 2);
+                        const size_t src = size_t(b + kDR[kc]) * W + (gc + kDC[kc]);
+                        const uint32_t sw = cw[src];  // occupied at step start: not written this step
+                        group = sw >> 30;
+                        uint32_t nw = sw;
+                        if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
+                            nw |= kCrossedBit;
                             if (group == 1u) ++ntop;
                             else ++nbot;
                         }
+                        ++moved;
+                        cw[gi] = nw;  // empty at step start: nobody reads it this step
+                        if (ACO) {    // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
+                            tour_new = __dadd_rn(tour[src], is_diag(kc) ? a.k.diag : 1.0);
+                            tour[gi] = tour_new;
+                        }
                     }
-                    arrived = true;
-                    if (valid) ++moved;
-                    if (ACO && valid) {  // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
-                        const size_t si_src = size_t(b + kDR[kc]) * W + (gc + kDC[kc]);
-                        tour_new = __dadd_rn(tour[si_src], is_diag(kc) ? a.k.diag : 1.0);
-                        tour[gi] = tour_new;
-                    }
-                } else if (bit(Gm, lane)) {
-                    nw = 0u;
-                }
-                if (valid) {
-                    cout[gi] = nw;
-                    if (ACO) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
+                    const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
+                    const uint32_t bot = __ballot_sync(0xFFFFFFFFu, group == 2u);
+                    np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
+                    np.y = (np.y & ~Gm) | bot;
+                    if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
                         double2 tt = tv[si - 1];
                         tt.x = __dmul_rn(tt.x, a.k.factor);
                         tt.y = __dmul_rn(tt.y, a.k.factor);
@@ -624,10 +577,13 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                         tout[gi] = tt;
                     }
                 }
+                if (lane == si - 1) mine = np;
             }
+            if (lane < NS) orow[lane] = mine;
         }
         __syncthreads();  // end of tile: the window's slots may be refilled
         base = slot(base, RT);
+        cur ^= 1;
     }
     base = next_base;
     // Counters of this item go to its replica's StepReport (src/engine.cpp:172-174).
@@ -654,7 +610,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
         // Small ring: the next item's window is loaded only now, into the
         // slots the finished item released.
         if (warp == 0) {
-            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, W);
+            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
             load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
         }
         __syncthreads();  // wall rows written by warp 0 are visible to all
@@ -662,11 +618,6 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     if (item < n_items) ++nload;
     }  // work items
 }
-
-// Three CTAs per SM must fit the 196 KB shared-memory carve-out step (1 KB
-// reserved per CTA): the next step up (228 KB) leaves 28 KB of L1 instead of
-// 60 KB, and the ACO pheromone stream then loses ~15% (measured).
-static_assert(sizeof(Smem) <= (196 * 1024) / 3 - 1024 - 64, "shared memory would cost 3 CTAs/SM their L1");
 
 int configure_step_bits() {
     const int bytes = int(sizeof(Smem));
@@ -676,6 +627,8 @@ int configure_step_bits() {
         return 1;
     return 0;
 }
+
+int bits_strip_segments() { return NS; }
 
 // Persistent grid: one CTA per (SM x 3) slot at most. Work items are chunks of
 // up to 16 consecutive RT-row tiles of one strip of one replica, sized so

@@ -171,6 +171,7 @@ struct pf_ctx {
     std::vector<int32_t> rep_aps;               // agents_per_side of each replica
     std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
+    bool bits() const { return cfg.kernel == PF_KERNEL_FUSED; }  // occupancy planes + in-place words
     size_t plane() const { return size_t(rows_buf) * size_t(cfg.width); }
     size_t total() const { return plane() * size_t(cfg.replicas); }
 };
@@ -321,8 +322,20 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     pfk::Planes& P = ctx->args.p;
     P.plane = ctx->plane();
     P.cell[0] = static_cast<uint32_t*>(alloc(n * 4));
-    P.cell[1] = static_cast<uint32_t*>(alloc(n * 4));
+    P.cell[1] = ctx->bits() ? P.cell[0] : static_cast<uint32_t*>(alloc(n * 4));
     bool ok = P.cell[0] && P.cell[1];
+    if (ctx->bits()) {
+        // Plane pitch: every strip's window (NS + 4 segments from segment
+        // strip * NS - 2) lies inside the row, and rows stay 16-byte aligned.
+        const int ns = pfk::bits_strip_segments();
+        const int strips = (cfg->width + 32 * ns - 1) / (32 * ns);
+        P.wsp = strips * ns + 4;
+        P.occ_plane = size_t(ctx->rows_buf) * size_t(P.wsp);
+        for (int i = 0; i < 2; ++i) {
+            P.occ[i] = static_cast<uint2*>(alloc(P.occ_plane * size_t(cfg->replicas) * 8));
+            ok = ok && P.occ[i];
+        }
+    }
     if (ctx->aco()) {
         P.tau[0] = static_cast<double2*>(alloc(n * 16));
         P.tau[1] = static_cast<double2*>(alloc(n * 16));
@@ -353,6 +366,8 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     }
     if (cudaMemsetAsync(P.cell[0], 0, n * 4, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(P.cell[1], 0, n * 4, ctx->stream) != cudaSuccess ||
+        (P.occ[0] && cudaMemsetAsync(P.occ[0], 0xFF, P.occ_plane * size_t(cfg->replicas) * 8, ctx->stream) != cudaSuccess) ||
+        (P.occ[1] && cudaMemsetAsync(P.occ[1], 0xFF, P.occ_plane * size_t(cfg->replicas) * 8, ctx->stream) != cudaSuccess) ||
         cudaMemsetAsync(ctx->d_step, 0, 4, ctx->stream) != cudaSuccess)
         return cleanup(fail(PF_ERR_CUDA, "cudaMemset failed"));
     if (P.intent) {
@@ -419,6 +434,31 @@ int32_t pf_replica_agents(const pf_ctx* ctx, int32_t rep) {
 // Global row of buffer row b.
 static inline int64_t grow_of(const pf_ctx* ctx, int b) { return int64_t(ctx->row_begin) - pfk::kGhost + b; }
 
+// Fused kernel: occupancy planes of both parities from the replica's words.
+static void build_occ(pf_ctx* ctx, int rep) {
+    pfk::Planes& P = ctx->args.p;
+    if (!ctx->bits()) return;
+    const size_t ooff = size_t(rep) * P.occ_plane;
+    ctx->launches += pfk::launch_build_occ(P.cell[0] + size_t(rep) * ctx->plane(), ctx->cfg.width, ctx->rows_buf,
+                                           P.wsp, P.occ[0] + ooff, P.occ[1] + ooff, ctx->stream);
+}
+
+// Fused kernel: zero the stale words of vacated cells (empty in the current
+// planes) so the word plane is the exact cell-word state; *bad counts agent
+// cells whose word disagrees with the planes.
+static void sanitize_words(pf_ctx* ctx, int rep, unsigned long long* bad) {
+    pfk::Planes& P = ctx->args.p;
+    if (!ctx->bits()) return;
+    ctx->launches += pfk::launch_sanitize_words(P.cell[0] + size_t(rep) * ctx->plane(),
+                                                P.occ[ctx->parity] + size_t(rep) * P.occ_plane, ctx->cfg.width,
+                                                ctx->rows_buf, P.wsp, bad, ctx->stream);
+}
+
+// Copy between aliased planes is a no-op.
+static cudaError_t copy_d2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+    return dst == src ? cudaSuccess : cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s);
+}
+
 // Upload one replica's buffer-row planes (cells + tour) and set the step.
 static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& words, const std::vector<double>* tour,
                           const std::vector<double2>* tau) {
@@ -427,7 +467,8 @@ static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& wor
     // One host->device copy per plane; the second ping-pong buffer is filled
     // device-side (its ghost rows must hold the same walls / halo).
     PF_CUDA(ctx->stage[0].h2d(P.cell[0] + off, words.data(), ctx->plane() * 4, ctx->stream));
-    PF_CUDA(cudaMemcpyAsync(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    PF_CUDA(copy_d2d(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, ctx->stream));
+    build_occ(ctx, rep);
     if (ctx->aco()) {
         if (tour) PF_CUDA(ctx->stage[0].h2d(P.tour + off, tour->data(), ctx->plane() * 8, ctx->stream));
         else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
@@ -586,8 +627,8 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     // Valid: both ping-pong buffers receive the state (the parity is kept).
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.cell[cur] + off, d_words, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.cell[cur ^ 1] + off, d_words, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = copy_d2d(P.cell[cur ^ 1] + off, P.cell[cur] + off, plane * 4, ctx->stream);
+    if (e == cudaSuccess) build_occ(ctx, rep);
     if (e == cudaSuccess && ctx->aco())
         e = cudaMemcpyAsync(P.tour + off, d_tour, plane * 8, cudaMemcpyDeviceToDevice, ctx->stream);
     join_side();
@@ -621,7 +662,7 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
     const pfk::Planes& P = ctx->args.p;
     IoTrace io_trace;
     auto up = up256;
-    const size_t need = up(own) + up(own * 4) + up(size_t(n_agents) * 40) + 16;
+    const size_t need = up(own) + up(own * 4) + up(size_t(n_agents) * 40) + 24;
     if (int rc = ensure_scratch(ctx, need)) return rc;
     if (!ctx->io_event) PF_CUDA(cudaEventCreateWithFlags(&ctx->io_event, cudaEventDisableTiming));
     char* s = static_cast<char*>(ctx->io_scratch);
@@ -629,8 +670,9 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
     auto* d_index = reinterpret_cast<uint32_t*>(s + up(own));
     char* d_agents = s + up(own) + up(own * 4);
     auto* d_status = reinterpret_cast<unsigned long long*>(d_agents + up(size_t(n_agents) * 40));
-    PF_CUDA(cudaMemsetAsync(d_status, 0, 16, ctx->stream));
+    PF_CUDA(cudaMemsetAsync(d_status, 0, 24, ctx->stream));
     if (agents) PF_CUDA(cudaMemsetAsync(d_agents, 0, size_t(n_agents) * 40, ctx->stream));
+    sanitize_words(ctx, rep, d_status + 2);
     ctx->launches += pfk::launch_export_state(P.cell[ctx->parity] + off, ctx->aco() ? P.tour + off : nullptr, own,
                                               uint32_t(W), uint32_t(ctx->row_begin), occ ? d_occ : nullptr,
                                               index ? d_index : nullptr, agents ? d_agents : nullptr, n_agents,
@@ -653,8 +695,8 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
             side_err = e;
         });
     }
-    unsigned long long status[2] = {0, 0};
-    cudaError_t e = ctx->stage[0].d2h(status, d_status, 16, ctx->stream);
+    unsigned long long status[3] = {0, 0, 0};
+    cudaError_t e = ctx->stage[0].d2h(status, d_status, 24, ctx->stream);
     if (e == cudaSuccess && occ) e = ctx->stage[0].d2h(occ, d_occ, own, ctx->stream);
     if (e == cudaSuccess && index) e = ctx->stage[0].d2h(index, d_index, own * 4, ctx->stream);
     if (e == cudaSuccess && agents) e = ctx->stage[0].d2h(agents, d_agents, size_t(n_agents) * 40, ctx->stream);
@@ -664,6 +706,7 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
     if (e == cudaSuccess) e = side_err;
     if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state download: ") + cudaGetErrorString(e));
     if (status[1]) return fail(PF_ERR_STATE, "state corrupt: device cell holds an out-of-range id");
+    if (status[2]) return fail(PF_ERR_STATE, "state corrupt: cell words disagree with the occupancy planes");
     if (status[0] != n_agents) return fail(PF_ERR_STATE, "state corrupt: agents on the grid disagree with the agent count");
     return PF_OK;
 }
@@ -687,6 +730,7 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
     const pfk::Planes& P = ctx->args.p;
     std::unique_ptr<uint32_t[]> words_buf(new uint32_t[own]);
     uint32_t* words = words_buf.get();
+    sanitize_words(ctx, rep, nullptr);
     PF_CUDA(ctx->stage[0].d2h(words, P.cell[ctx->parity] + off, own * 4, ctx->stream));
     const size_t g0 = size_t(ctx->row_begin) * W;
     // ACO: pheromone is de-interleaved on the device into the owned rows of
@@ -941,6 +985,13 @@ int pf_halo(pf_ctx* ctx, int32_t rep, int32_t side, int32_t recv, pf_halo_rows* 
     const pfk::Planes& P = ctx->args.p;
     out->cells = P.cell[ctx->parity] + off + size_t(first) * W;
     out->cell_bytes = size_t(G) * W * 4;
+    if (ctx->bits()) {
+        out->occ = P.occ[ctx->parity] + size_t(rep) * P.occ_plane + size_t(first) * P.wsp;
+        out->occ_bytes = size_t(G) * P.wsp * 8;
+    } else {
+        out->occ = nullptr;
+        out->occ_bytes = 0;
+    }
     if (ctx->aco()) {
         out->tau = P.tau[ctx->parity] + off + size_t(first) * W;
         out->tau_bytes = size_t(G) * W * 16;
@@ -970,6 +1021,12 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
         pf_halo(lower, r, 0, 1, &lr);
         PF_CUDA(cudaMemcpyAsync(lr.cells, us.cells, us.cell_bytes, cudaMemcpyDefault, lower->stream));
         PF_CUDA(cudaMemcpyAsync(ur.cells, ls.cells, ls.cell_bytes, cudaMemcpyDefault, lower->stream));
+        if (us.occ && ls.occ && us.occ_bytes == lr.occ_bytes) {
+            PF_CUDA(cudaMemcpyAsync(lr.occ, us.occ, us.occ_bytes, cudaMemcpyDefault, lower->stream));
+            PF_CUDA(cudaMemcpyAsync(ur.occ, ls.occ, ls.occ_bytes, cudaMemcpyDefault, lower->stream));
+        } else if (us.occ || ls.occ) {
+            return fail(PF_ERR_COMM, "shards use different kernels");
+        }
         if (us.tau) {
             PF_CUDA(cudaMemcpyAsync(lr.tau, us.tau, us.tau_bytes, cudaMemcpyDefault, lower->stream));
             PF_CUDA(cudaMemcpyAsync(ur.tau, ls.tau, ls.tau_bytes, cudaMemcpyDefault, lower->stream));
@@ -988,16 +1045,17 @@ int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
     const uint32_t n_agents = ctx->reps[size_t(rep)].n_agents;
     const size_t words = (size_t(n_agents) + 31) / 32;
     char* d = nullptr;
-    PF_CUDA(cudaMalloc(&d, words * 4 + 3 * 8));
+    PF_CUDA(cudaMalloc(&d, words * 4 + 4 * 8));
     auto* counts = reinterpret_cast<unsigned long long*>(d);
-    auto* seen = reinterpret_cast<uint32_t*>(d + 3 * 8);
-    unsigned long long h[3] = {0ull, 0ull, ~0ull};
+    auto* seen = reinterpret_cast<uint32_t*>(d + 4 * 8);
+    unsigned long long h[4] = {0ull, 0ull, ~0ull, 0ull};
     int rc = PF_OK;
     if (cudaMemcpyAsync(counts, h, sizeof h, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(seen, 0, words * 4, ctx->stream) != cudaSuccess) {
         rc = fail(PF_ERR_CUDA, "audit setup failed");
     } else {
         const size_t W = size_t(ctx->cfg.width);
+        sanitize_words(ctx, rep, counts + 3);
         ctx->launches += pfk::launch_audit(ctx->args.p.cell[ctx->parity] + size_t(rep) * ctx->plane(),
                                            size_t(pfk::kGhost) * W, size_t(ctx->rows_owned) * W, n_agents, seen,
                                            counts, ctx->stream);
@@ -1008,6 +1066,7 @@ int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
     cudaFree(d);
     if (rc) return rc;
     if (agent_cells) *agent_cells = h[0];
+    if (h[3]) return fail(PF_ERR_STATE, "state corrupt: " + std::to_string(h[3]) + " cell word(s) disagree with the occupancy planes");
     if (h[1]) {
         const size_t cell = size_t(h[2] - 1);
         const size_t W = size_t(ctx->cfg.width);

@@ -17,7 +17,15 @@ constexpr int kGhost = 3;  // == PF_GHOST_ROWS
 // plane[replica][buffer row][column]; buffer row b <-> global row
 // row_begin - kGhost + b.
 struct Planes {
-    uint32_t* cell[2];  // ping-pong cell words
+    // Cell words. PF_KERNEL_FUSED: one plane updated in place (cell[1] ==
+    // cell[0]), valid only where occ says "occupied". Other kernels: ping-pong.
+    uint32_t* cell[2];
+    // PF_KERNEL_FUSED: ping-pong occupancy bit planes, uint2 {v30, v31} per
+    // 32-cell segment, rows of wsp segments (2 wall segments of padding on
+    // each side: segment s of a row is at index s + 2). Null otherwise.
+    uint2* occ[2];
+    size_t occ_plane;   // uint2 elements per replica = rows_buf * wsp
+    int wsp;
     double2* tau[2];    // ping-pong {top, bottom} pheromone (ACO)
     double* tour;       // cell-resident tour length, updated in place (ACO)
     uint8_t* intent;    // pipeline-kernel scratch
@@ -47,6 +55,15 @@ struct StepArgs {
 // Returns the number of kernel launches issued.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s);   // PF_KERNEL_FUSED
 int configure_step_bits();
+int bits_strip_segments();  // NS: the plane pitch is a multiple of it plus 4
+// Occupancy planes of rows [0, rows) from cell words (W columns; padding
+// segments untouched); written to occ0 and, if non-null, occ1.
+int launch_build_occ(const uint32_t* words, int W, int rows, int wsp, uint2* occ0, uint2* occ1, cudaStream_t s);
+// Zero the words of cells the planes mark empty (stale ids of vacated cells)
+// over rows [0, rows); *bad (may be null) += occupied cells whose word's group
+// disagrees with the planes.
+int launch_sanitize_words(uint32_t* words, const uint2* occ, int W, int rows, int wsp, unsigned long long* bad,
+                          cudaStream_t s);
 int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s);  // PF_KERNEL_TILE
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
 // *d_step += n

@@ -524,6 +524,63 @@ int launch_gather_tour(double* per_agent, const uint32_t* words, const double* t
     return 1;
 }
 
+// --- occupancy bit planes of the fused kernel (pf_bitstep.cu) -----------
+
+// Warp per 32-cell segment, lane = column: two ballots of the word's group
+// bits; columns past W are walls (both bits set).
+__global__ void build_occ_kernel(const uint32_t* __restrict__ words, int W, int rows, int wsp, uint2* occ0,
+                                 uint2* occ1) {
+    const int lane = threadIdx.x & 31;
+    const int nseg = (W + 31) / 32;
+    const size_t units = size_t(rows) * nseg;
+    for (size_t u = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) / 32; u < units;
+         u += size_t(gridDim.x) * blockDim.x / 32) {
+        const size_t row = u / nseg;
+        const int seg = int(u % nseg), c = 32 * seg + lane;
+        const uint32_t w = c < W ? words[row * W + c] : pfdev::kWall;
+        const uint2 p = make_uint2(__ballot_sync(0xFFFFFFFFu, (w >> 30) & 1u), __ballot_sync(0xFFFFFFFFu, w >> 31));
+        if (lane == 0) {
+            occ0[row * wsp + seg + 2] = p;
+            if (occ1) occ1[row * wsp + seg + 2] = p;
+        }
+    }
+}
+
+int launch_build_occ(const uint32_t* words, int W, int rows, int wsp, uint2* occ0, uint2* occ1, cudaStream_t s) {
+    build_occ_kernel<<<148 * 8, 256, 0, s>>>(words, W, rows, wsp, occ0, occ1);
+    return 1;
+}
+
+// Thread per cell: a word under an empty plane bit is a stale id of a
+// vacated cell (the fused kernel never clears them) and becomes 0.
+__global__ void sanitize_words_kernel(uint32_t* words, const uint2* __restrict__ occ, int W, int rows, int wsp,
+                                      unsigned long long* bad) {
+    const size_t n = size_t(rows) * W;
+    unsigned nbad = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t row = i / W;
+        const int c = int(i - row * W);
+        const uint2 p = occ[row * wsp + c / 32 + 2];
+        const uint32_t g = ((p.x >> (c & 31)) & 1u) | ((p.y >> (c & 31)) & 1u) << 1;
+        const uint32_t w = words[i];
+        if (g == 0u) {
+            if (w != 0u) words[i] = 0u;
+        } else if ((w >> 30) != g || (g != 3u && (w & pfdev::kIdMask) == 0u)) {
+            ++nbad;
+        }
+    }
+    if (bad) {
+        nbad = __reduce_add_sync(0xFFFFFFFFu, nbad);
+        if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(bad, (unsigned long long)nbad);
+    }
+}
+
+int launch_sanitize_words(uint32_t* words, const uint2* occ, int W, int rows, int wsp, unsigned long long* bad,
+                          cudaStream_t s) {
+    sanitize_words_kernel<<<148 * 8, 256, 0, s>>>(words, occ, W, rows, wsp, bad);
+    return 1;
+}
+
 }  // namespace pfk
 
 namespace pfk {

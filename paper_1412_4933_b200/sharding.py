@@ -143,7 +143,8 @@ class ShardedEngine:
         out = []
         for r in range(self.ctx.replicas):
             h = self.ctx.halo(r, side, recv)
-            for ptr, nb in ((h.cells, h.cell_bytes), (h.tau, h.tau_bytes), (h.tour, h.tour_bytes)):
+            for ptr, nb in ((h.cells, h.cell_bytes), (h.occ, h.occ_bytes), (h.tau, h.tau_bytes),
+                             (h.tour, h.tour_bytes)):
                 if not nb:
                     continue
                 key = (ptr, nb)

@@ -88,9 +88,9 @@ def test_device_audit_accepts_valid_and_detects_corruption():
     # duplicate an id inside the arena (first owned rows of replica 1)
     h = ens.ctx.halo(1, 0, False)
     rows = _device_tensor(h.cells, h.cell_bytes, 0).view(torch.int32)
+    # (the audits above left the words exact: vacated cells hold 0)
     occupied = torch.nonzero(rows != 0).flatten()
-    empty = torch.nonzero(rows == 0).flatten()
-    rows[empty[0]] = rows[occupied[0]]
+    rows[occupied[1]] = rows[occupied[0]]
     torch.cuda.synchronize()
     with pytest.raises(p.StateCorrupt):
         ens.audit(1)
