@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -46,14 +48,24 @@ WORKLOADS = {
 }
 
 
-def alg_bytes(w, h, n, model, replicas):
-    """Algorithmic HBM bytes per step: LEM 8 B/cell (read +
-    write the 32-bit cell word); ACO 40 B/cell (+ two f64 pheromone fields
-    read + written) + 16 B/agent (f64 tour read + written)."""
+ALG_MODEL = ("bit-plane state (DESIGN.md §2): 0.5 B/cell (2-bit occupancy planes read + written) + 8 B/mover "
+             "(source cell word read, destination word written); ACO + 32 B/cell (two f64 pheromone fields read + "
+             "written) + 16 B/mover (f64 tour read + written)")
+
+
+def alg_bytes(w, h, model, replicas, movers):
+    """Algorithmic HBM bytes per step of the bit-plane representation
+    (SURVEY.md §8(d) counted 8 B/cell for the packed word
+    plane, which the in-place word plane no longer streams): every cell's
+    occupancy bits are read and written (2 x 2 bits), every mover's word is
+    read at its source and written at its destination; ACO adds both f64
+    pheromone fields read + written for every cell and the f64 tour read +
+    written per mover. `movers` = agents moved per step (StepReport.moved)."""
     cells = w * h * replicas
-    if model == "lem":
-        return 8 * cells
-    return 40 * cells + 16 * 2 * n * replicas
+    b = 0.5 * cells + 8 * movers
+    if model == "aco":
+        b += 32 * cells + 16 * movers
+    return b
 
 
 def measured_peak():
@@ -203,7 +215,11 @@ def run_reference_arm(args):
 # ------------------------------------------------------------------ GPU arm
 
 def secondary_runs(steps):
-    """C4/C3 (100K agents) replica-batched and single-scenario device timings."""
+    """C4/C3 (100K agents) replica-batched and single-scenario device timings,
+    and C2/C1. The window is steps 5 .. 5+steps of the run: with steps = 1000
+    (the length of the C3/C4 golden runs) it covers the approach of the two
+    crowds AND the congested regime after they meet (~step 130), which costs
+    2-3x more per step than the free-flow start."""
     import paper_1412_4933_b200 as p
 
     peak, _ = measured_peak()
@@ -212,13 +228,19 @@ def secondary_runs(steps):
         cfg, reps, desc = scenario(name)
         ens = p.Ensemble(cfg, replicas=reps)
         ens.run(5)
-        tot, ker = ens.time_steps(steps, kernel=True)
-        b = alg_bytes(cfg.width, cfg.height, cfg.agents_per_side, "lem" if cfg.model == p.Model.Lem else "aco", reps)
+        n = min(steps, 1024)
+        tot, _ = ens.time_steps(n)
+        movers = float(ens.ctx.read_reports(n)["moved"].astype(np.int64).sum()) / n
+        _, ker = ens.time_steps(min(n, 50), kernel=True)
+        model = "lem" if cfg.model == p.Model.Lem else "aco"
+        b = alg_bytes(cfg.width, cfg.height, model, reps, movers)
         out[name] = {
-            "workload": desc, "ms_per_step": tot / steps, "kernel_ms_isolated_launch_events": ker,
-            "agent_updates_per_s": 2 * cfg.agents_per_side * reps * steps / (tot / 1e3),
-            "cell_updates_per_s": cfg.width * cfg.height * reps * steps / (tot / 1e3),
-            "roofline_frac": b / (tot / steps / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
+            "workload": desc, "window": f"steps 5..{5 + n}", "ms_per_step": tot / n,
+            "kernel_ms_isolated_launch_events": ker,
+            "agent_updates_per_s": 2 * cfg.agents_per_side * reps * n / (tot / 1e3),
+            "cell_updates_per_s": cfg.width * cfg.height * reps * n / (tot / 1e3),
+            "movers_per_step": movers,
+            "roofline_frac": b / (tot / n / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
         }
         ens.close()
     return out
@@ -257,6 +279,13 @@ def run_gpu_arm(args):
             return x
         t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
     # --- device-resident throughput -----------------------------------
@@ -302,7 +331,8 @@ def run_gpu_arm(args):
 
     agents_total = 2 * n * reps
     value = agents_total * args.steps / (ms / 1e3)
-    bytes_step = alg_bytes(w, h, n, model, reps)
+    moved_all = sum_over_ranks(moved_local)
+    bytes_step = alg_bytes(w, h, model, reps, moved_all / min(args.steps, 1024))
     bytes_launch = bytes_step / world  # per rank's kernel (its shard)
     achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
 
@@ -329,7 +359,7 @@ def run_gpu_arm(args):
                          "kernel": "step_bits_kernel", "kernel_ms": kernel_ms,
                          "kernel_ms_isolated_launch_events": kernel_ms_isolated,
                          "alg_bytes_per_launch": bytes_launch,
-                         "alg_bytes_model": "LEM 8 B/cell; ACO 40 B/cell + 16 B/agent (SURVEY.md 8(d))"},
+                         "alg_bytes_model": ALG_MODEL},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "setup_s": setup_s,
@@ -345,7 +375,7 @@ def run_gpu_arm(args):
             line["cpu_baseline"] = {"value": r["value"], "unit": "agent-updates/s", "cores": r["cores"],
                                     "kind": r["kind"], "sample": r["sample"]}
         if world == 1 and not args.no_secondary:
-            line["secondary"] = secondary_runs(50)
+            line["secondary"] = secondary_runs(1000)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

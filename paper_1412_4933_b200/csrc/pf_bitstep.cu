@@ -91,6 +91,10 @@ struct Smem {
     uint32_t qu[NU];  // unit
     uint32_t qm[NU];  // its bits
     uint32_t qp[NU];  // rank of its first bit
+    // S3: per warp, the words (and ACO tours) at the sources of its row's
+    // arrivals, fetched for all segments at once by cp.async.
+    uint32_t asw[NW][NS][32];
+    double atr[NW][NS][32];
     unsigned long long mbar[2];
     uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
     int item;
@@ -132,6 +136,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity
         "}\n" ::"r"(smem_u32(m)),
         "r"(parity)
         : "memory");
+}
+
+// --- cp.async (LDGSTS) of single words into shared memory ----------------
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 // Ring slot of staged row sr (0 = tile row -3) for a window starting at base.
@@ -518,6 +531,21 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                 continue;
             }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
+            // The sources of this row's arrivals: all their loads are in
+            // flight together (one round trip per row, not one per segment).
+            // Each source is occupied at step start, so nothing writes it.
+#pragma unroll
+            for (int si = 1; si <= NS; ++si) {
+                if (bit(sm.A[ai][si], lane)) {
+                    const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
+                                       bit(sm.K[2][ai][si], lane) << 2);
+                    const size_t src = size_t(b + kDR[kc]) * W + (c0 + 32 * (si - 1) + lane + kDC[kc]);
+                    cp_async<4>(&sm.asw[warp][si - 1][lane], cw + src);
+                    if (ACO) cp_async<8>(&sm.atr[warp][si - 1][lane], tour + src);
+                }
+            }
+            cp_async_wait_all();
+            __syncwarp();
             // ACO: issue the whole row's pheromone loads before using any of them.
             double2 tv[NS];
             if (ACO) {
@@ -545,8 +573,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                     if (arrived) {
                         const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
                                            bit(sm.K[2][ai][si], lane) << 2);
-                        const size_t src = size_t(b + kDR[kc]) * W + (gc + kDC[kc]);
-                        const uint32_t sw = cw[src];  // occupied at step start: not written this step
+                        const uint32_t sw = sm.asw[warp][si - 1][lane];
                         group = sw >> 30;
                         uint32_t nw = sw;
                         if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
@@ -557,7 +584,7 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
                         ++moved;
                         cw[gi] = nw;  // empty at step start: nobody reads it this step
                         if (ACO) {    // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
-                            tour_new = __dadd_rn(tour[src], is_diag(kc) ? a.k.diag : 1.0);
+                            tour_new = __dadd_rn(sm.atr[warp][si - 1][lane], is_diag(kc) ? a.k.diag : 1.0);
                             tour[gi] = tour_new;
                         }
                     }
