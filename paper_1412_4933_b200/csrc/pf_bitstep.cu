@@ -69,6 +69,11 @@ constexpr int SS = NS + 2;       // intent / resolution segments: -1 .. NS
 constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index = si + 1)
 static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
 constexpr int NT = 256;          // threads per CTA
+// Resident CTAs per SM (register budget 65536 / (NT * CTAS)): 4 (64
+// registers) for LEM and for grids whose pheromone planes fit in L2; 3 (80
+// registers, no spills) for the HBM-streaming ACO grids, where the extra
+// warps cost more in spills than they hide (A/B: C5 ACO +2%, C5 LEM -12%).
+constexpr int kCtasHbm = 3, kCtasDefault = 4;
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
 constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
@@ -353,8 +358,8 @@ __device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parit
         sm.pl[slot(base, first_sr + i / SP)][i % SP] = make_uint2(kWall, kWall);
 }
 
-template <bool ACO>
-__global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
+template <bool ACO, int CTAS>
+__global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -646,32 +651,37 @@ __global__ void __launch_bounds__(NT, 3) step_bits_kernel(const StepArgs a, int 
     }  // work items
 }
 
+static_assert(kCtasDefault * (sizeof(Smem) + 1024) <= 228 * 1024, "shared memory must fit kCtasDefault CTAs per SM");
+
 int configure_step_bits() {
     const int bytes = int(sizeof(Smem));
-    if (cudaFuncSetAttribute(step_bits_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
-        return 1;
-    if (cudaFuncSetAttribute(step_bits_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
-        return 1;
+    for (auto f : {step_bits_kernel<false, kCtasDefault>, step_bits_kernel<true, kCtasDefault>,
+                   step_bits_kernel<true, kCtasHbm>})
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
     return 0;
 }
 
 int bits_strip_segments() { return NS; }
 
-// Persistent grid: one CTA per (SM x 3) slot at most. Work items are chunks of
+// Persistent grid: one CTA per (SM x 3 or 4) slot at most. Work items are chunks of
 // up to 16 consecutive RT-row tiles of one strip of one replica, sized so
 // there are about 4 items per CTA for load balance.
 int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
-    const long long ctas_max = (long long)a.num_sms * 3;
+    // ACO grids whose pheromone planes (32 B/cell) exceed the 126 MB L2 stream from HBM.
+    const bool hbm = a.k.model == 1 && 32.0 * double(a.k.W) * a.rows_buf * a.replicas > 126e6;
+    const int ctas = hbm ? kCtasHbm : kCtasDefault;
+    const long long ctas_max = (long long)a.num_sms * ctas;
     const long long tiles = (long long)strips * n_tiles * a.replicas;
     StepArgs b = a;
     b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
     dim3 grid(unsigned(std::min(items, ctas_max)));
     const size_t bytes = sizeof(Smem);
-    if (a.k.model == 1) step_bits_kernel<true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    else step_bits_kernel<false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    if (a.k.model == 0) step_bits_kernel<false, kCtasDefault><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    else if (hbm) step_bits_kernel<true, kCtasHbm><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    else step_bits_kernel<true, kCtasDefault><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
     return 1;
 }
 

@@ -2,6 +2,7 @@
 # A/B builds for same-box timing comparisons (dev tool):
 #   tools/debug/lib_base.so  from git REF (default HEAD)
 #   tools/debug/lib_new.so   from the working tree
+# (NEW_FLAGS="-DPF_BITS_CTAS=4" adds compile flags to lib_new)
 # then on the GPU box:  python tools/ab_time.py c5_lem c4_aco_x64 ...
 set -e
 cd "$(dirname "$0")/.."
@@ -12,7 +13,7 @@ git archive "$REF" paper_1412_4933_b200/csrc include | tar -x -C "$TMP"
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off"
 SRCS="pf_kernels.cu pf_bitstep.cu pf_context.cu pf_setup.cpp"
 nvcc $FLAGS -I "$TMP/include" -shared -o tools/debug/lib_base.so $(for s in $SRCS; do echo "$TMP/paper_1412_4933_b200/csrc/$s"; done) &
-nvcc $FLAGS -I include -shared -o tools/debug/lib_new.so $(for s in $SRCS; do echo "paper_1412_4933_b200/csrc/$s"; done) &
+nvcc $FLAGS $NEW_FLAGS -I include -shared -o tools/debug/lib_new.so $(for s in $SRCS; do echo "paper_1412_4933_b200/csrc/$s"; done) &
 wait
 rm -rf "$TMP"
 echo "built tools/debug/lib_base.so ($REF) and tools/debug/lib_new.so (working tree)"
