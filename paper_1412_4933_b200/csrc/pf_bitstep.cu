@@ -70,9 +70,10 @@ constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index 
 static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
 constexpr int NT = 256;          // threads per CTA
 // Resident CTAs per SM (register budget 65536 / (NT * CTAS)): 4 (64
-// registers) for LEM and for grids whose pheromone planes fit in L2; 3 (80
-// registers, no spills) for the HBM-streaming ACO grids, where the extra
-// warps cost more in spills than they hide (A/B: C5 ACO +2%, C5 LEM -12%).
+// registers) for LEM and for small (480^2-class, replica-batched) ACO grids;
+// 3 (80 registers, no spills) for large ACO grids, which are pure pheromone
+// streams and lose more to spills than the extra warps hide (A/B at step
+// 150: C5 ACO +2%, C4 x64 ACO -5%, C5 LEM -12%, C3 x64 LEM -11%).
 constexpr int kCtasHbm = 3, kCtasDefault = 4;
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
@@ -669,8 +670,7 @@ int bits_strip_segments() { return NS; }
 int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
-    // ACO grids whose pheromone planes (32 B/cell) exceed the 126 MB L2 stream from HBM.
-    const bool hbm = a.k.model == 1 && 32.0 * double(a.k.W) * a.rows_buf * a.replicas > 126e6;
+    const bool hbm = a.k.model == 1 && double(a.k.W) * a.rows_buf >= double(1 << 22);  // >= 4M cells per replica
     const int ctas = hbm ? kCtasHbm : kCtasDefault;
     const long long ctas_max = (long long)a.num_sms * ctas;
     const long long tiles = (long long)strips * n_tiles * a.replicas;
