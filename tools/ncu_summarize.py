@@ -81,9 +81,9 @@ def summarize(tag, specs):
     tpath = os.path.join(PROF, "ncu_traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     lines = [f"# ncu --set full summaries ({tag})", "",
-             "Captured with `ncu --set full --clock-control none --import-source on -k regex:step_bits -s 3 -c 1` "
-             "on `python tools/profile_step.py <workload> 5` (one launch, cold caches, serialised: compare shares, "
-             "not absolute times, with the bench).", ""]
+             "Captured with `ncu --set full --clock-control none --import-source on -k regex:step_bits -s S -c 1` "
+             "on `python tools/profile_step.py <workload> S+2` (one launch at step S, named in each heading; cold "
+             "caches, serialised: compare shares, not absolute times, with the bench).", ""]
     for spec in specs:
         rep, workload = spec.split(":")
         d = raw(rep)
