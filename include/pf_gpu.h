@@ -156,6 +156,31 @@ int pf_halo(pf_ctx* ctx, int32_t replica, int32_t side, int32_t recv, pf_halo_ro
  * (upper owns the rows just above lower) on the same or peer devices. */
 int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower);
 
+/* Fused halo exchange (PF_KERNEL_FUSED only): instead of a separate swap
+ * after each step, the step kernel stores this shard's PF_GHOST_ROWS boundary
+ * rows (planes, arrivals' words and tours, pheromone) straight into the ghost
+ * rows of the neighbour shards, through peer memory (NVLink P2P; CUDA IPC
+ * between processes). Each step is then bracketed on the device by a flag
+ * handshake: wait until the neighbours have completed the previous step
+ * (their stores into our ghost rows are done and they no longer read the
+ * ghost buffers we are about to write), step, then release our completion
+ * count into the neighbours' flags. No host work or collective per step, so
+ * sharded steps batch into CUDA graphs like single-GPU ones. */
+typedef struct pf_peer_desc {
+    unsigned char ipc[7][64]; /* cudaIpcMemHandle_t of: cell, occ[0], occ[1], tau[0], tau[1], tour, sync flags */
+    uint64_t ptr[7];          /* the same allocations as device pointers of the exporting process */
+    int32_t device, width, replicas, model, kernel, row_begin, rows_owned, parity;
+    uint32_t step, reserved;
+    uint64_t plane, occ_plane; /* per-replica elements of the cell / occupancy planes */
+} pf_peer_desc;
+/* Describe this context for its neighbours (pointers and IPC handles). */
+int pf_peer_export(pf_ctx* ctx, pf_peer_desc* out);
+/* Link the neighbour on `side` (0: the shard above, ending at row_begin;
+ * 1: the shard below). ipc != 0 opens the IPC handles (another process);
+ * ipc == 0 uses the pointers (same process, same or peer-capable device).
+ * Both shards must be at the same step and parity; link both directions. */
+int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* peer, int32_t ipc);
+
 /* Device-side state audit of one replica, the cell-resident form of
  * check_consistency (src/state.cpp:77-110): every agent cell holds an id in
  * [1, 2n] of the right side, no id twice, no wall inside the arena, and (for

@@ -71,6 +71,17 @@ class PfHalo(C.Structure):
     ]
 
 
+class PfPeerDesc(C.Structure):
+    """pf_peer_desc: a shard's planes for its neighbours (fused halo exchange)."""
+    _fields_ = [
+        ("ipc", (C.c_ubyte * 64) * 7), ("ptr", C.c_uint64 * 7),
+        ("device", C.c_int32), ("width", C.c_int32), ("replicas", C.c_int32), ("model", C.c_int32),
+        ("kernel", C.c_int32), ("row_begin", C.c_int32), ("rows_owned", C.c_int32), ("parity", C.c_int32),
+        ("step", C.c_uint32), ("reserved", C.c_uint32),
+        ("plane", C.c_uint64), ("occ_plane", C.c_uint64),
+    ]
+
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build the CUDA library first "
@@ -104,8 +115,12 @@ _sigs = {
     "pf_exchange_pair": (C.c_int, [_vp, _vp]),
     "pf_selftest_rng": (C.c_int, [_i32, _u32, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double, _vp, _vp, _vp]),
     "pf_audit": (C.c_int, [_vp, _i32, C.POINTER(_u64)]),
+    "pf_peer_export": (C.c_int, [_vp, C.POINTER(PfPeerDesc)]),
+    "pf_peer_attach": (C.c_int, [_vp, _i32, C.POINTER(PfPeerDesc), _i32]),
 }
 for _name, (_res, _args) in _sigs.items():
+    if os.environ.get("PEDFLOW_B200_LIB") and not hasattr(lib, _name):
+        continue  # dev A/B against an older build (tools/ab_time.py): newer entry points absent
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args
@@ -221,6 +236,17 @@ class Context:
         check(lib.pf_audit(self.h, replica, C.byref(n)))
         return n.value
 
+    def peer_desc(self) -> PfPeerDesc:
+        """This shard's planes for its neighbours (pf_peer_export)."""
+        d = PfPeerDesc()
+        check(lib.pf_peer_export(self.h, C.byref(d)))
+        return d
+
+    def attach_peer(self, side: int, desc: PfPeerDesc, ipc: bool):
+        """Link the neighbour on `side` (0 above, 1 below) for the fused halo
+        exchange (pf_peer_attach); ipc=True when it lives in another process."""
+        check(lib.pf_peer_attach(self.h, side, C.byref(desc), 1 if ipc else 0))
+
     def halo(self, replica: int, side: int, recv: bool) -> PfHalo:
         h = PfHalo()
         check(lib.pf_halo(self.h, replica, side, 1 if recv else 0, C.byref(h)))
@@ -229,6 +255,17 @@ class Context:
 
 def exchange_pair(upper: Context, lower: Context) -> None:
     check(lib.pf_exchange_pair(upper.h, lower.h))
+
+
+def link_shards(ctxs) -> None:
+    """Fused halo exchange between vertically adjacent shard contexts of ONE
+    process (ctxs in row order; same device or peer-capable devices)."""
+    descs = [c.peer_desc() for c in ctxs]
+    for i, c in enumerate(ctxs):
+        if i > 0:
+            c.attach_peer(0, descs[i - 1], ipc=False)
+        if i + 1 < len(ctxs):
+            c.attach_peer(1, descs[i + 1], ipc=False)
 
 
 def selftest_rng(seed, step, phase, entity, counter, mu=0.0, sigma=1.0, device=0):

@@ -359,7 +359,46 @@ __device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parit
         sm.pl[slot(base, first_sr + i / SP)][i % SP] = make_uint2(kWall, kWall);
 }
 
-template <bool ACO, int CTAS>
+// Fused halo exchange (linked shards only): after a tile's commit, its rows
+// that are ghost rows of a neighbour shard (this shard's first / last kGhost
+// owned rows) are copied from where the commit just wrote them (L2) into the
+// neighbour's ghost rows: occupancy planes and pheromone of the new parity,
+// words and tours in place (a stale word under an empty plane bit is as
+// harmless there as here). Called by the whole CTA after the end-of-tile
+// barrier; the system fence orders the stores before the step's completion
+// flag (launch_halo_signal).
+template <bool ACO>
+__device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int rep, int strip, int r0) {
+    const int W = a.k.W;
+    const int c0 = strip * NS * 32, ncols = min(NS * 32, W - c0);
+    const size_t pb = size_t(rep) * a.p.plane, ob = size_t(rep) * a.p.occ_plane;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const PeerRows pr = a.peer[s];
+        if (!pr.cell) continue;
+        const int lo = max(r0, s == 0 ? 0 : a.rows_owned - kGhost);
+        const int hi = min(min(r0 + RT, a.rows_owned), s == 0 ? kGhost : a.rows_owned);
+        for (int lr = lo; lr < hi; ++lr) {
+            const int b = kGhost + lr, pbr = b + pr.row_delta;
+            const size_t src = pb + size_t(b) * W + c0, dst = size_t(rep) * pr.plane + size_t(pbr) * W + c0;
+            for (int i = threadIdx.x; i < ncols; i += NT) {
+                pr.cell[dst + i] = a.p.cell[0][src + i];
+                if (ACO) {
+                    pr.tour[dst + i] = a.p.tour[src + i];
+                    pr.tau[parity ^ 1][dst + i] = a.p.tau[parity ^ 1][src + i];
+                }
+            }
+            if (threadIdx.x < NS) {
+                const size_t q = size_t(strip) * NS + 2 + threadIdx.x;
+                pr.occ[parity ^ 1][size_t(rep) * pr.occ_plane + size_t(pbr) * a.p.wsp + q] =
+                    a.p.occ[parity ^ 1][ob + size_t(b) * a.p.wsp + q];
+            }
+        }
+    }
+    __threadfence_system();
+}
+
+template <bool ACO, int CTAS, bool MIRROR>
 __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -593,6 +632,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                             tour_new = __dadd_rn(sm.atr[warp][si - 1][lane], is_diag(kc) ? a.k.diag : 1.0);
                             tour[gi] = tour_new;
                         }
+
                     }
                     const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
                     const uint32_t bot = __ballot_sync(0xFFFFFFFFu, group == 2u);
@@ -615,6 +655,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             if (lane < NS) orow[lane] = mine;
         }
         __syncthreads();  // end of tile: the window's slots may be refilled
+        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, parity, rep, it.strip, r0);
         base = slot(base, RT);
         cur ^= 1;
     }
@@ -656,8 +697,9 @@ static_assert(kCtasDefault * (sizeof(Smem) + 1024) <= 228 * 1024, "shared memory
 
 int configure_step_bits() {
     const int bytes = int(sizeof(Smem));
-    for (auto f : {step_bits_kernel<false, kCtasDefault>, step_bits_kernel<true, kCtasDefault>,
-                   step_bits_kernel<true, kCtasHbm>})
+    for (auto f : {step_bits_kernel<false, kCtasDefault, false>, step_bits_kernel<true, kCtasDefault, false>,
+                   step_bits_kernel<true, kCtasHbm, false>, step_bits_kernel<false, kCtasDefault, true>,
+                   step_bits_kernel<true, kCtasDefault, true>, step_bits_kernel<true, kCtasHbm, true>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
     return 0;
 }
@@ -679,9 +721,17 @@ int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
     dim3 grid(unsigned(std::min(items, ctas_max)));
     const size_t bytes = sizeof(Smem);
-    if (a.k.model == 0) step_bits_kernel<false, kCtasDefault><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    else if (hbm) step_bits_kernel<true, kCtasHbm><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    else step_bits_kernel<true, kCtasDefault><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
+    if (a.k.model == 0) {
+        if (mirror) step_bits_kernel<false, kCtasDefault, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        else step_bits_kernel<false, kCtasDefault, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    } else if (hbm) {
+        if (mirror) step_bits_kernel<true, kCtasHbm, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        else step_bits_kernel<true, kCtasHbm, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    } else {
+        if (mirror) step_bits_kernel<true, kCtasDefault, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        else step_bits_kernel<true, kCtasDefault, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    }
     return 1;
 }
 

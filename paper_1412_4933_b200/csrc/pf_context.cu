@@ -168,6 +168,14 @@ struct pf_ctx {
     void* io_scratch = nullptr;                 // device staging of exported SimState planes
     size_t io_scratch_bytes = 0;
     cudaEvent_t io_event = nullptr;
+    // Fused halo exchange: d_sync[side] = steps completed by the linked
+    // neighbour on that side (written by it); remote_flag[side] = the
+    // neighbour's flag for us; d_err = handshake timeout.
+    uint32_t* d_sync = nullptr;
+    uint32_t* d_err = nullptr;
+    uint32_t* remote_flag[2] = {nullptr, nullptr};
+    int linked = 0;                             // bit s: neighbour on side s
+    std::vector<void*> ipc_opened;              // peer allocations opened with cudaIpcOpenMemHandle
     std::vector<int32_t> rep_aps;               // agents_per_side of each replica
     std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
@@ -253,6 +261,7 @@ int pf_destroy(pf_ctx* ctx) {
     if (!ctx) return PF_OK;
     cudaSetDevice(ctx->cfg.device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (void* p : ctx->allocs) cudaFree(p);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -348,6 +357,9 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         ok = ok && P.intent && P.win;
     }
     ctx->d_step = static_cast<uint32_t*>(alloc(4));
+    ctx->d_sync = static_cast<uint32_t*>(alloc(8));
+    ctx->d_err = static_cast<uint32_t*>(alloc(4));
+    ok = ok && ctx->d_sync && ctx->d_err;
     auto* kc = static_cast<pfdev::StepConsts*>(alloc(sizeof(pfdev::StepConsts)));
     ok = ok && kc && cudaMemcpy(kc, &ctx->args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice) == cudaSuccess;
     ctx->args.kc = kc;
@@ -368,7 +380,9 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         cudaMemsetAsync(P.cell[1], 0, n * 4, ctx->stream) != cudaSuccess ||
         (P.occ[0] && cudaMemsetAsync(P.occ[0], 0xFF, P.occ_plane * size_t(cfg->replicas) * 8, ctx->stream) != cudaSuccess) ||
         (P.occ[1] && cudaMemsetAsync(P.occ[1], 0xFF, P.occ_plane * size_t(cfg->replicas) * 8, ctx->stream) != cudaSuccess) ||
-        cudaMemsetAsync(ctx->d_step, 0, 4, ctx->stream) != cudaSuccess)
+        cudaMemsetAsync(ctx->d_step, 0, 4, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(ctx->d_sync, 0, 8, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream) != cudaSuccess)
         return cleanup(fail(PF_ERR_CUDA, "cudaMemset failed"));
     if (P.intent) {
         ctx->launches += pfk::launch_fill_u8(P.intent, n, pfdev::kNone, ctx->stream);
@@ -487,6 +501,10 @@ static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& wor
 static void set_step(pf_ctx* ctx, uint32_t step) {
     ctx->step = step;
     cudaMemcpyAsync(ctx->d_step, &ctx->step, 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (ctx->linked) {  // linked neighbours are (re)loaded to the same step
+        const uint32_t sync[2] = {step, step};
+        cudaMemcpyAsync(ctx->d_sync, sync, 8, cudaMemcpyHostToDevice, ctx->stream);
+    }
     cudaStreamSynchronize(ctx->stream);
 }
 
@@ -817,11 +835,26 @@ static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
 }
 
 static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
+    if (ctx->linked)  // fused halo: the neighbours have completed the previous step
+        ctx->launches += pfk::launch_halo_wait(ctx->d_step, int(i), ctx->d_sync, ctx->linked, ctx->d_err, ctx->stream);
     switch (ctx->cfg.kernel) {
         case PF_KERNEL_FUSED: ctx->launches += pfk::launch_step_bits(ctx->args, int(i), parity, ctx->stream); break;
         case PF_KERNEL_TILE: ctx->launches += pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream); break;
         default: ctx->launches += pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream); break;
     }
+    if (ctx->linked)
+        ctx->launches += pfk::launch_halo_signal(ctx->d_step, int(i), ctx->remote_flag[0], ctx->remote_flag[1],
+                                                 ctx->stream);
+    return PF_OK;
+}
+
+// Steps are stream-ordered; a handshake timeout (a neighbour that never
+// completed its step) is reported at the next synchronisation.
+static int check_halo(pf_ctx* ctx) {
+    if (!ctx->linked) return PF_OK;
+    uint32_t err = 0;
+    PF_CUDA(cudaMemcpy(&err, ctx->d_err, 4, cudaMemcpyDeviceToHost));
+    if (err) return fail(PF_ERR_COMM, "fused halo exchange: a neighbour shard did not complete its step (timeout)");
     return PF_OK;
 }
 
@@ -849,7 +882,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
         it = ctx->graphs.emplace(key, ge).first;
     }
     PF_CUDA(cudaGraphLaunch(it->second, ctx->stream));
-    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1;
+    const uint32_t per_step = (ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1) + (ctx->linked ? 2 : 0);
     ctx->launches += uint64_t(n) * per_step + 1;
     ctx->parity ^= int(n & 1u);
     ctx->step += n;
@@ -892,7 +925,7 @@ int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n) {
 int pf_synchronize(pf_ctx* ctx) {
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
-    return PF_OK;
+    return check_halo(ctx);
 }
 
 int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
@@ -913,7 +946,7 @@ int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
         done += m;
     }
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
-    return PF_OK;
+    return check_halo(ctx);
 }
 
 int pf_time_steps(pf_ctx* ctx, uint32_t n, float* total_ms, float* kernel_ms) {
@@ -1035,6 +1068,91 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
         }
     }
     PF_CUDA(cudaStreamSynchronize(lower->stream));
+    return PF_OK;
+}
+
+int pf_peer_export(pf_ctx* ctx, pf_peer_desc* out) {
+    if (!ctx || !out) return fail(PF_ERR_ARG, "null argument");
+    if (!ctx->bits()) return fail(PF_ERR_CONFIG, "the fused halo exchange needs PF_KERNEL_FUSED");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    std::memset(out, 0, sizeof *out);
+    const pfk::Planes& P = ctx->args.p;
+    void* ptrs[7] = {P.cell[0], P.occ[0], P.occ[1], P.tau[0], P.tau[1], P.tour, ctx->d_sync};
+    for (int i = 0; i < 7; ++i) {
+        out->ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+        if (!ptrs[i]) continue;
+        cudaIpcMemHandle_t h;
+        PF_CUDA(cudaIpcGetMemHandle(&h, ptrs[i]));
+        static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(out->ipc[i], &h, 64);
+    }
+    out->device = ctx->cfg.device;
+    out->width = ctx->cfg.width;
+    out->replicas = ctx->cfg.replicas;
+    out->model = ctx->cfg.model;
+    out->kernel = ctx->cfg.kernel;
+    out->row_begin = ctx->row_begin;
+    out->rows_owned = ctx->rows_owned;
+    out->parity = ctx->parity;
+    out->step = ctx->step;
+    out->plane = ctx->plane();
+    out->occ_plane = P.occ_plane;
+    return PF_OK;
+}
+
+int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc) {
+    if (!ctx || !d) return fail(PF_ERR_ARG, "null argument");
+    if (side != 0 && side != 1) return fail(PF_ERR_ARG, "side must be 0 (above) or 1 (below)");
+    if (!ctx->bits() || d->kernel != PF_KERNEL_FUSED) return fail(PF_ERR_CONFIG, "the fused halo exchange needs PF_KERNEL_FUSED");
+    if (d->width != ctx->cfg.width || d->replicas != ctx->cfg.replicas || d->model != ctx->cfg.model)
+        return fail(PF_ERR_COMM, "neighbour shard has a different grid width, replica count or model");
+    const bool adjacent = side == 0 ? d->row_begin + d->rows_owned == ctx->row_begin
+                                    : ctx->row_begin + ctx->rows_owned == d->row_begin;
+    if (!adjacent) return fail(PF_ERR_COMM, "shards are not vertically adjacent");
+    if (d->step != ctx->step || d->parity != ctx->parity)
+        return fail(PF_ERR_COMM, "neighbour shard is at a different step");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    void* p[7] = {};
+    for (int i = 0; i < 7; ++i) {
+        if (!d->ptr[i]) continue;
+        if (ipc) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, d->ipc[i], 64);
+            PF_CUDA(cudaIpcOpenMemHandle(&p[i], h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_opened.push_back(p[i]);
+        } else {
+            p[i] = reinterpret_cast<void*>(d->ptr[i]);
+        }
+    }
+    if (!ipc && d->device != ctx->cfg.device) {
+        int can = 0;
+        PF_CUDA(cudaDeviceCanAccessPeer(&can, ctx->cfg.device, d->device));
+        if (!can) return fail(PF_ERR_COMM, "no peer access between the shards' devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(PF_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+    pfk::PeerRows& pr = ctx->args.peer[side];
+    pr.cell = static_cast<uint32_t*>(p[0]);
+    pr.occ[0] = static_cast<uint2*>(p[1]);
+    pr.occ[1] = static_cast<uint2*>(p[2]);
+    pr.tau[0] = static_cast<double2*>(p[3]);
+    pr.tau[1] = static_cast<double2*>(p[4]);
+    pr.tour = static_cast<double*>(p[5]);
+    pr.plane = size_t(d->plane);
+    pr.occ_plane = size_t(d->occ_plane);
+    // Our owned row r (buffer row G + r) is the upper neighbour's lower ghost
+    // row G + its rows_owned + r, and the lower neighbour's upper ghost row
+    // r - (rows_owned - G).
+    pr.row_delta = side == 0 ? d->rows_owned : -ctx->rows_owned;
+    ctx->remote_flag[side] = static_cast<uint32_t*>(p[6]) + (1 - side);
+    const uint32_t now = ctx->step;  // the neighbour has completed `step` steps
+    PF_CUDA(cudaMemcpy(ctx->d_sync + side, &now, 4, cudaMemcpyHostToDevice));
+    ctx->linked |= 1 << side;
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // recaptured with the handshake
+    ctx->graphs.clear();
     return PF_OK;
 }
 

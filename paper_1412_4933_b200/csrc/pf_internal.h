@@ -33,6 +33,19 @@ struct Planes {
     size_t plane;       // elements per replica plane = rows_buf * W
 };
 
+// A neighbouring shard's planes, for the fused halo exchange (PF_KERNEL_FUSED):
+// the step kernel mirrors this shard's 3 boundary rows straight into the
+// neighbour's ghost rows (peer memory over NVLink, or the same device).
+// Buffer row b of this shard is the neighbour's buffer row b + row_delta.
+struct PeerRows {
+    uint32_t* cell;
+    uint2* occ[2];
+    double2* tau[2];
+    double* tour;
+    size_t plane, occ_plane;  // the neighbour's per-replica plane sizes
+    int row_delta;
+};
+
 struct StepArgs {
     pfdev::StepConsts k;              // by value: hot scalars read from param space
     const pfdev::StepConsts* kc;      // device copy: tables read by the slow paths
@@ -49,6 +62,7 @@ struct StepArgs {
     uint32_t* work;         // bit kernel: per-step work-item counters, ring slot = step % report_cap
     int num_sms;
     int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
+    PeerRows peer[2];       // [0] the shard above (toward row 0), [1] below; cell == nullptr: none
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
@@ -68,6 +82,13 @@ int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s); 
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
 // *d_step += n
 int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
+// Fused halo handshake of step (*d_step + slot): wait until each linked
+// neighbour has completed that many steps (flags[side] >= step; spins with a
+// timeout that sets *err), and after the step tell the neighbours
+// (remote[side] = step + 1, system-scope release).
+int launch_halo_wait(const uint32_t* d_step, int slot, const volatile uint32_t* flags, int sides, uint32_t* err,
+                     cudaStream_t s);
+int launch_halo_signal(const uint32_t* d_step, int slot, uint32_t* remote0, uint32_t* remote1, cudaStream_t s);
 // Fill a tau plane range with {v, v}.
 int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);

@@ -16,10 +16,19 @@ cell-resident and arrives with the ghost rows. RNG keys use the agent id and
 the GLOBAL cell index, crossing uses the global row, so any shard count gives
 results bit-identical to one GPU and to the CPU oracle.
 
-The exchange code here is engine-agnostic: it moves torch tensors, so the CPU
-tests drive it with gloo and numpy-backed shards of the oracle, and the GPU
-path drives it with NCCL and tensors aliasing the library's device planes
-(via __cuda_array_interface__).
+Two exchange paths:
+
+* "p2p" (default for the fused kernel): the fused halo exchange of the C-ABI
+  (pf_peer_export / pf_peer_attach). Each rank exports CUDA IPC handles of its
+  planes, the handles are all-gathered once over the process group, and from
+  then on the step kernel itself stores the 3 boundary rows into the
+  neighbours' ghost rows over NVLink, with a device-side flag handshake per
+  step. No host work per step: n steps are one graph-batched pf_step_async.
+* "nccl" / host-staged: HaloExchanger below, a torch.distributed
+  batch_isend_irecv of the ghost-row ranges after each step's kernel. It is
+  engine-agnostic (it moves torch tensors), so the CPU tests drive it with
+  gloo and numpy-backed shards of the oracle, and the GPU path with NCCL and
+  tensors aliasing the library's device planes (__cuda_array_interface__).
 """
 from __future__ import annotations
 
@@ -115,7 +124,7 @@ class ShardedEngine:
     ghost-row exchange after every step."""
 
     def __init__(self, cfg, rank: int, world: int, *, device: int | None = None, replicas: int = 1,
-                 seed: int | None = None, kernel: str = "fused", group=None):
+                 seed: int | None = None, kernel: str = "fused", group=None, exchange: str | None = None):
         import torch
 
         from .engine import _pf_config, validate
@@ -130,14 +139,33 @@ class ShardedEngine:
                                            row_begin=0 if whole else self.lo, row_end=0 if whole else self.hi,
                                            device=self.device, kernel=kernel))
         self.ctx.init_environment()
+        if exchange is None:
+            exchange = "p2p" if kernel == "fused" else "collective"
+        if exchange not in ("p2p", "collective"):
+            raise _lib.ConfigError(f"unknown halo exchange {exchange!r} (p2p or collective)")
+        self.exchange = exchange if world > 1 else "none"
         staged = False
         if world > 1:
             import torch.distributed as dist
 
             staged = dist.get_backend(group) != "nccl"
+            if self.exchange == "p2p":
+                self._link_peers(dist, group)
         self.exchanger = HaloExchanger(rank, world, group, staged=staged)
         self._tcache: dict = {}
         self._stream = torch.cuda.ExternalStream(self.ctx.stream(), device=f"cuda:{self.device}")
+
+    def _link_peers(self, dist, group):
+        """Fused halo exchange: all-gather every rank's pf_peer_desc (CUDA IPC
+        handles of its planes) and attach the two vertical neighbours."""
+        mine = bytes(self.ctx.peer_desc())
+        descs = [None] * self.world
+        dist.all_gather_object(descs, mine, group=group)
+        for side, peer in ((0, self.rank - 1), (1, self.rank + 1)):
+            if 0 <= peer < self.world:
+                d = _lib.PfPeerDesc.from_buffer_copy(descs[peer])
+                self.ctx.attach_peer(side, d, ipc=True)
+        dist.barrier(group=group)  # no rank signals a neighbour before it has attached
 
     def _planes(self, side: int, recv: bool):
         out = []
@@ -155,9 +183,14 @@ class ShardedEngine:
         return out
 
     def step(self, n: int = 1) -> None:
-        """n steps; the halo swap is stream-ordered after each step's kernel."""
+        """n steps. p2p: one graph-batched enqueue (the kernels exchange the
+        halo themselves); collective: the halo swap is stream-ordered after
+        each step's kernel."""
         import torch
 
+        if self.exchange in ("p2p", "none"):
+            self.ctx.step_async(n)
+            return
         for _ in range(n):
             self.ctx.step_async(1)
             if self.world > 1:

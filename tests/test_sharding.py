@@ -198,7 +198,85 @@ def test_gpu_multishard_one_device(model, nshards):
             assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
 
 
-def _gpu_rank_main(rank, world, port, kw, steps, out_q):
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_gpu_fused_halo_one_device(model, nshards):
+    """Fused halo exchange (the step kernel stores its boundary rows into the
+    neighbours' ghost rows; device flag handshake per step): k linked shard
+    contexts on one GPU, stepped by graph-batched pf_step_async only (no host
+    exchange), equal the unsharded run in every plane. 300 steps = two graph
+    batches; shards of unequal height (112 rows over 3)."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
+
+    cfg = p.ScenarioConfig(width=96, height=112 if nshards == 3 else 96, agents_per_side=1500,
+                           model=p.Model.Lem if model == "lem" else p.Model.Aco, seed=21)
+    steps = 300
+    whole = p.Ensemble(cfg, replicas=2, seed=21)
+    whole_rep = whole.run(steps)
+    shards = []
+    for lo, hi in row_partition(cfg.height, nshards):
+        c = _lib.Context(_pf_config(cfg, 21, replicas=2, row_begin=lo, row_end=hi))
+        c.init_environment()
+        shards.append(c)
+    _lib.link_shards(shards)
+    for c in shards:
+        c.step_async(steps)
+    for c in shards:
+        c.synchronize()
+    tot = sum(c.read_reports(steps)["moved"].astype(np.int64) for c in shards)
+    assert (tot == whole_rep["moved"]).all()
+    for r in range(2):
+        ref = whole.state(r)
+        H, W = cfg.height, cfg.width
+        occ = np.zeros((H, W), np.uint8)
+        idx = np.zeros((H, W), np.uint32)
+        ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+        tt = np.zeros((H, W)) if model == "aco" else None
+        tb = np.zeros((H, W)) if model == "aco" else None
+        for c in shards:
+            assert c.store(r, occ, idx, ag, tt, tb) == steps
+        assert (idx == ref.index).all() and (occ == ref.occupancy).all()
+        assert (ag["tour_length"] == ref.agents["tour_length"]).all()
+        assert (ag["crossed"] == ref.agents["crossed"]).all()
+        if tt is not None:
+            assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
+        for c in shards:
+            c.audit(r)
+    for c in shards:
+        c.close()
+
+
+@pytest.mark.gpu
+def test_gpu_fused_halo_rejects_mismatched_peers():
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+
+    cfg = p.ScenarioConfig(width=96, height=96, agents_per_side=500, model=p.Model.Aco)
+    a = _lib.Context(_pf_config(cfg, 1, row_begin=0, row_end=48))
+    b = _lib.Context(_pf_config(cfg, 1, row_begin=48, row_end=96))
+    c = _lib.Context(_pf_config(cfg, 1, row_begin=0, row_end=40))
+    t = _lib.Context(_pf_config(cfg, 1, row_begin=48, row_end=96, kernel="tile"))
+    for x in (a, b, c):
+        x.init_environment()
+    with pytest.raises(_lib.CommError):
+        b.attach_peer(0, c.peer_desc(), ipc=False)  # not adjacent
+    with pytest.raises(_lib.CommError):
+        a.attach_peer(0, b.peer_desc(), ipc=False)  # wrong side
+    with pytest.raises(p.ConfigError):
+        t.peer_desc()  # the tile kernel has no fused exchange
+    a.step(1)
+    with pytest.raises(_lib.CommError):
+        b.attach_peer(0, a.peer_desc(), ipc=False)  # different step
+    for x in (a, b, c, t):
+        x.close()
+
+
+def _gpu_rank_main(rank, world, port, kw, steps, out_q, exchange=None):
     import torch
     import torch.distributed as dist
 
@@ -213,8 +291,9 @@ def _gpu_rank_main(rank, world, port, kw, steps, out_q):
     try:
         model = kw.pop("model")
         cfg = p.ScenarioConfig(model=p.Model.Lem if model == "lem" else p.Model.Aco, **kw)
-        eng = ShardedEngine(cfg, rank, world, device=0, replicas=2)
+        eng = ShardedEngine(cfg, rank, world, device=0, replicas=2, exchange=exchange)
         eng.step(steps)
+        eng.synchronize()
         rep = eng.reports(steps)
         H, W = cfg.height, cfg.width
         res = []
@@ -233,11 +312,15 @@ def _gpu_rank_main(rank, world, port, kw, steps, out_q):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["collective", "p2p"])
 @pytest.mark.parametrize("model", ["lem", "aco"])
-def test_gpu_sharded_engine_two_ranks_one_device(model):
-    """The N>1 product path (ShardedEngine: per-step halo swap through the
-    exchanger, halo ranges from pf_halo, parity handling) with 2 ranks sharing
-    cuda:0 over gloo (host-staged exchange), against the unsharded run."""
+def test_gpu_sharded_engine_two_ranks_one_device(model, exchange):
+    """The N>1 product path with 2 ranks (processes) sharing cuda:0 over gloo,
+    against the unsharded run. collective: ShardedEngine's per-step halo swap
+    through the exchanger (host-staged for gloo), halo ranges from pf_halo.
+    p2p: the fused halo exchange across processes — CUDA IPC handles of each
+    rank's planes all-gathered over gloo, the step kernels storing into each
+    other's ghost rows, the device flag handshake between processes."""
     import torch.multiprocessing as mp
 
     import paper_1412_4933_b200 as p
@@ -247,7 +330,8 @@ def test_gpu_sharded_engine_two_ranks_one_device(model):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gpu_rank_main, args=(r, world, port, dict(kw), steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_rank_main, args=(r, world, port, dict(kw), steps, q, exchange))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
