@@ -8,8 +8,9 @@ and cell-updates/s per step, achieved HBM GB/s vs peak, 1/2/4/8 GPUs).
 
 Default workload: C5 of BASELINE.json — ACO, 16384 x 16384 grid, 25,000,000
 agents per side (50M) — the largest configuration, the one the 1/2/4/8-GPU
-scaling is quoted on; at N GPUs it is row-sharded (strong scaling) with a
-3-row NCCL halo exchange per step. A step is one full StepEngine::step of the
+scaling is quoted on; at N GPUs it is row-sharded (strong scaling): the step
+kernels store their 3 boundary rows into the neighbours' ghost rows (CUDA IPC
+peer memory over NVLink) with a device-side handshake per step. A step is one full StepEngine::step of the
 whole grid. The other BASELINE configs are parity cases; the 100K-agent config
 (C4) is reported under "secondary" as a replica-batched run (64 seeds per
 launch), its single-scenario step time beside it.
@@ -257,12 +258,22 @@ def run_gpu_arm(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # Dev check of the N>1 code path on a box with fewer GPUs than ranks:
+    # PEDFLOW_BENCH_SHARE_GPU=1 maps rank -> GPU (local % count) and uses gloo
+    # (the numbers are then meaningless: ranks time-slice one GPU).
+    share = os.environ.get("PEDFLOW_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    red_dev = "cpu" if share else f"cuda:{local}"
     cfg, reps, desc = scenario(args.workload)
     if args.replicas:
         reps = args.replicas
@@ -277,14 +288,14 @@ def run_gpu_arm(args):
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -350,7 +361,7 @@ def run_gpu_arm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64+u32",
             "data": "synthetic (new_environment placement, seed 42; replica i uses seed 42+i)",
             "config": {"workload": desc, "width": w, "height": h, "agents_per_side": n, "model": model,
-                       "replicas": reps, "parallelism": f"row-shard x{world} (3-row NCCL halo/step)" if world > 1
+                       "replicas": reps, "parallelism": f"row-shard x{world} (fused 3-row P2P halo per step: peer stores + device handshake)" if world > 1
                        else "single GPU", "l2": "inputs larger than L2 (resident state >> 126 MB; no flush)"},
             "cell_updates_per_s": w * h * reps * args.steps / (ms / 1e3),
             "hbm_gbs_alg_step": bytes_step * args.steps / (ms / 1e3) / 1e9,
@@ -390,7 +401,7 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
     import paper_1412_4933_b200 as p
     from paper_1412_4933_b200 import _lib
     from paper_1412_4933_b200.engine import _pf_config
-    from paper_1412_4933_b200.sharding import HaloExchanger, row_partition
+    from paper_1412_4933_b200.sharding import row_partition
 
     state = p.new_environment(cfg, 42)  # host planes (reference layout)
     lo, hi = row_partition(cfg.height, world)[rank]
@@ -403,14 +414,14 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
     d2h = (hi - lo) * W * (1 + 4 + (16 if aco else 0)) + len(state.agents) * 40 + 16 * args.steps
     import torch
 
-    ex = HaloExchanger(rank, world)
-    stream = torch.cuda.ExternalStream(c.stream(), device=f"cuda:{local}")
-    from paper_1412_4933_b200.sharding import _device_tensor
+    if world > 1:  # fused halo exchange between the ranks' contexts (CUDA IPC, device handshake)
+        import torch.distributed as dist
 
-    def planes(side, recv):
-        hh = c.halo(0, side, recv)
-        return [_device_tensor(pt, nb, local) for pt, nb in ((hh.cells, hh.cell_bytes), (hh.occ, hh.occ_bytes),
-                                                             (hh.tau, hh.tau_bytes), (hh.tour, hh.tour_bytes)) if nb]
+        descs = [None] * world
+        dist.all_gather_object(descs, bytes(c.peer_desc()))
+        for side, peer in ((0, rank - 1), (1, rank + 1)):
+            if 0 <= peer < world:
+                c.attach_peer(side, _lib.PfPeerDesc.from_buffer_copy(descs[peer]), ipc=True)
 
     barrier()
     t0 = time.perf_counter()
@@ -418,10 +429,8 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
     if world == 1:
         rep = c.step(args.steps)
     else:
-        for _ in range(args.steps):
-            c.step_async(1)
-            with torch.cuda.stream(stream):
-                ex.exchange(planes)
+        barrier()  # every shard is loaded (and its handshake flags reset) before any steps
+        c.step_async(args.steps)
         rep = c.read_reports(min(args.steps, 1024))
     c.store(0, state._occ, state._index, state._agents, state._tau_top, state._tau_bot)
     secs = max_over_ranks(time.perf_counter() - t0)
