@@ -54,8 +54,17 @@ using namespace pfdev;
 
 namespace {
 
-constexpr int RT = 16;           // output rows per tile
-constexpr int NS = 8;            // output 32-column segments per strip
+#ifndef PF_BITS_RT
+#define PF_BITS_RT 16
+#endif
+#ifndef PF_BITS_NS
+#define PF_BITS_NS 8
+#endif
+#ifndef PF_BITS_NT
+#define PF_BITS_NT 256
+#endif
+constexpr int RT = PF_BITS_RT;   // output rows per tile
+constexpr int NS = PF_BITS_NS;   // output 32-column segments per strip
 constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
 #ifndef PF_BITS_RING
 #define PF_BITS_RING (2 * SR)
@@ -68,13 +77,13 @@ static_assert(RING >= SR + RT, "the ring must hold a window and the next tile's 
 constexpr int SS = NS + 2;       // intent / resolution segments: -1 .. NS
 constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index = si + 1)
 static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
-constexpr int NT = 256;          // threads per CTA
+constexpr int NT = PF_BITS_NT;   // threads per CTA
 // Resident CTAs per SM (register budget 65536 / (NT * CTAS)): 4 (64
 // registers) for LEM and for small (480^2-class, replica-batched) ACO grids;
 // 3 (80 registers, no spills) for large ACO grids, which are pure pheromone
 // streams and lose more to spills than the extra warps hide (A/B at step
 // 150: C5 ACO +2%, C4 x64 ACO -5%, C5 LEM -12%, C3 x64 LEM -11%).
-constexpr int kCtasHbm = 3, kCtasDefault = 4;
+constexpr int kRegCtas = NT == 256 ? 4 : 65536 / (NT * 64);
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
 constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
@@ -100,12 +109,13 @@ struct Smem {
     // S3: per warp, the words (and ACO tours) at the sources of its row's
     // arrivals, fetched for all segments at once by cp.async.
     uint32_t asw[NW][NS][32];
-    double atr[NW][NS][32];
     unsigned long long mbar[2];
     uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
     int item;
     uint32_t cnt[3];
+    double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
 };
+constexpr size_t kSmemBytes[2] = {offsetof(Smem, atr), sizeof(Smem)};  // [ACO]
 
 __device__ __forceinline__ uint32_t bit(uint32_t x, int j) { return (x >> j) & 1u; }
 
@@ -576,6 +586,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 continue;
             }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
+            // ACO: issue the whole row's pheromone loads before using any of them
+            // (and before the arrival-source fetch, so both round trips overlap).
+            double2 tv[NS];
+            if (ACO) {
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
+            }
             // The sources of this row's arrivals: all their loads are in
             // flight together (one round trip per row, not one per segment).
             // Each source is occupied at step start, so nothing writes it.
@@ -591,13 +609,6 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             }
             cp_async_wait_all();
             __syncwarp();
-            // ACO: issue the whole row's pheromone loads before using any of them.
-            double2 tv[NS];
-            if (ACO) {
-#pragma unroll
-                for (int s = 0; s < NS; ++s)
-                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
-            }
             uint2 mine = make_uint2(kWall, kWall);
 #pragma unroll
             for (int si = 1; si <= NS; ++si) {
@@ -693,38 +704,46 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     }  // work items
 }
 
-static_assert(kCtasDefault * (sizeof(Smem) + 1024) <= 228 * 1024, "shared memory must fit kCtasDefault CTAs per SM");
+// CTAs per SM: the register budget (kRegCtas), capped by shared memory (1 KB
+// reserved per CTA); one fewer (more registers) for large ACO grids.
+constexpr int smem_ctas(bool aco) { return int((228 * 1024) / (kSmemBytes[aco ? 1 : 0] + 1024)); }
+constexpr int kCtasLem = kRegCtas < smem_ctas(false) ? kRegCtas : smem_ctas(false);
+constexpr int kCtasDefault = kRegCtas < smem_ctas(true) ? kRegCtas : smem_ctas(true);
+constexpr int kCtasHbm = kCtasDefault > 1 && NT == 256 ? 3 : kCtasDefault;
+static_assert(kCtasLem >= 1 && kCtasDefault >= 1, "shared memory must fit one CTA per SM");
 
 int configure_step_bits() {
-    const int bytes = int(sizeof(Smem));
-    for (auto f : {step_bits_kernel<false, kCtasDefault, false>, step_bits_kernel<true, kCtasDefault, false>,
-                   step_bits_kernel<true, kCtasHbm, false>, step_bits_kernel<false, kCtasDefault, true>,
+    const int lem = int(kSmemBytes[0]), aco = int(kSmemBytes[1]);
+    for (auto f : {step_bits_kernel<false, kCtasLem, false>, step_bits_kernel<false, kCtasLem, true>})
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lem) != cudaSuccess) return 1;
+    for (auto f : {step_bits_kernel<true, kCtasDefault, false>, step_bits_kernel<true, kCtasHbm, false>,
                    step_bits_kernel<true, kCtasDefault, true>, step_bits_kernel<true, kCtasHbm, true>})
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, aco) != cudaSuccess) return 1;
     return 0;
 }
 
 int bits_strip_segments() { return NS; }
 
-// Persistent grid: one CTA per (SM x 3 or 4) slot at most. Work items are chunks of
-// up to 16 consecutive RT-row tiles of one strip of one replica, sized so
-// there are about 4 items per CTA for load balance.
+// Persistent grid: one CTA per resident slot (SMs x 3 or 4) at most. Work
+// items are chunks of up to 16 consecutive RT-row tiles of one strip of one
+// replica, sized so there are about 4 items per CTA for load balance.
 int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
-    const bool hbm = a.k.model == 1 && double(a.k.W) * a.rows_buf >= double(1 << 22);  // >= 4M cells per replica
-    const int ctas = hbm ? kCtasHbm : kCtasDefault;
+    const bool aco = a.k.model == 1;
+    const bool hbm = aco && double(a.k.W) * a.rows_buf >= double(1 << 22);  // >= 4M cells per replica
+    const int ctas = !aco ? kCtasLem : (hbm ? kCtasHbm : kCtasDefault);
     const long long ctas_max = (long long)a.num_sms * ctas;
     const long long tiles = (long long)strips * n_tiles * a.replicas;
     StepArgs b = a;
     b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
     dim3 grid(unsigned(std::min(items, ctas_max)));
-    const size_t bytes = sizeof(Smem);
+    const size_t bytes = kSmemBytes[aco ? 1 : 0];
     const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
-    if (a.k.model == 0) {
-        if (mirror) step_bits_kernel<false, kCtasDefault, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<false, kCtasDefault, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+    if (!aco) {
+        if (mirror) step_bits_kernel<false, kCtasLem, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        else step_bits_kernel<false, kCtasLem, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
     } else if (hbm) {
         if (mirror) step_bits_kernel<true, kCtasHbm, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
         else step_bits_kernel<true, kCtasHbm, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
