@@ -726,7 +726,8 @@ int bits_strip_segments() { return NS; }
 
 // Persistent grid: one CTA per resident slot (SMs x 3 or 4) at most. Work
 // items are chunks of up to 16 consecutive RT-row tiles of one strip of one
-// replica, sized so there are about 4 items per CTA for load balance.
+// replica, sized so there are about 32 items per CTA (a short tail at the
+// end of the step; consecutive tiles of an item share their halo rows).
 int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;

@@ -1,4 +1,7 @@
-"""Dev sweep: step time vs work items per CTA (PEDFLOW_ITEMS_PER_CTA)."""
+"""Dev sweep: step time vs work items per CTA (PEDFLOW_ITEMS_PER_CTA).
+
+    SKIP=150 python tools/sweep_items.py 2,4,8,16 c5_aco c4_aco_x64
+"""
 import os, subprocess, sys
 code = r'''
 import sys, os
@@ -6,7 +9,7 @@ sys.path.insert(0, os.getcwd())
 import bench, paper_1412_4933_b200 as p
 for name in sys.argv[1:]:
     cfg, reps, desc = bench.scenario(name)
-    e = p.Ensemble(cfg, replicas=reps); e.run(5)
+    e = p.Ensemble(cfg, replicas=reps); e.run(5 + int(os.environ.get('SKIP', '0')))
     tot, _ = e.time_steps(100)
     print(f"  {name:12s} {tot/100*1e3:8.1f} us/step", flush=True); e.close()
 '''
