@@ -1,758 +1,36 @@
-// Bit-sliced fused step kernel on occupancy bit planes (the default product
-// path, PF_KERNEL_FUSED).
+// Strip-width dispatch of the fused step kernel (pf_bitstep.cuh).
 //
-// State representation:
-//   occ[parity]  ping-pong occupancy bit planes, one uint2 {v30, v31} per
-//                32-cell row segment: bit j of v30 / v31 is bit 30 / 31 of the
-//                cell word of column 32*seg + j (Top = v30 & ~v31, Bottom =
-//                v31 & ~v30, Empty = ~(v30 | v31), wall = both). Rows are
-//                padded with two wall segments on each side, so a strip's
-//                plane window is one aligned run of NS + 4 segments.
-//   cell         the 32-bit cell words (id | crossed | group), updated IN
-//                PLACE and meaningful only where the planes say "occupied":
-//                a step reads words only at cells occupied at its start
-//                (draw keys, arrival sources) and writes them only at cells
-//                empty at its start (arrivals), so the two sets never meet
-//                and no ping-pong copy of the 4 B/cell words is needed.
-//                Vacated cells keep a stale word; state export masks words
-//                with the planes (launch_sanitize_words).
-//
-// The per-step update (StepEngine::step, src/engine.cpp:53-193) is evaluated
-// on 32-cell row segments held as 32-bit masks, so the common work costs one
-// ALU op per 32 cells; only agents that must draw (forward blocked, some slot
-// open) and destinations with >= 2 claimants fall to per-cell scalar code, and
-// those are compacted into shared-memory work lists so every lane takes one.
-//
-// Persistent column sweep: a CTA owns a strip of NS 32-column segments and a
-// run of consecutive RT-row tiles. The step-start planes of the strip live in
-// a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
-// rows); while a tile is processed, TMA bulk copies (cp.async.bulk + mbarrier,
-// one 96-byte row each) bring the next tile's RT new rows.
-//
-//   S1 intent  thread per segment-row: forward moves (F open, no draw,
-//              src/lem.cpp:23-26, src/aco.cpp:60-63) and boxed-in agents in
-//              bit logic; agents that must draw are queued, then run the
-//              scalar LEM / ACO selection one per thread with the open-slot
-//              mask built from the planes. Output: 8 intent planes D_j (bit
-//              set: the agent there moves toward row-major direction j).
-//   S2 resolve thread per segment-row: claims C_k on every destination from
-//              the shifted intent planes (the gather of src/engine.cpp:101-122,
-//              row-major contender order), at-least-two detection in bit logic;
-//              contested cells are queued for the keyed draw. Winner code
-//              planes (A, K0..K2); granted moves are OR-ed onto the sources.
-//   S3 commit  warp per row, lane = column: arrivals (source word, crossing,
-//              counters, tour), the new occupancy planes (vacates cleared,
-//              arrivals set by group ballots), ACO evaporation + deposit over
-//              every cell (src/engine.cpp:124-175).
-#include <algorithm>
-
+// A work unit of S1/S2 is one 32-cell segment-row of a tile plus the halo
+// segments on each side of its strip, and a CTA runs one unit per thread.
+// 10-segment strips (320 columns) keep 240 of the 256 threads busy in S1
+// (8-segment strips: 200) and pay 2 halo segments per 10 instead of per 8,
+// but waste whole segments when the grid width is not a multiple of 320:
+// for LEM the strip width with fewer units per row wins (A/B at step 150: C5
+// LEM -9% with 10; 480-wide grids: 8, since 10 would pad 15 segments to 20).
+// ACO, bound by its pheromone stream, keeps 8 (C5 ACO +0.4% with 10).
 #include "pf_internal.h"
 
 namespace pfk {
+namespace bits_ns8 {
+int configure();
+int launch(const StepArgs& a, int slot, int parity, cudaStream_t s);
+}  // namespace bits_ns8
+namespace bits_ns10 {
+int configure();
+int launch(const StepArgs& a, int slot, int parity, cudaStream_t s);
+}  // namespace bits_ns10
 
-using namespace pfdev;
-
-namespace {
-
-#ifndef PF_BITS_RT
-#define PF_BITS_RT 16
-#endif
-#ifndef PF_BITS_NS
-#define PF_BITS_NS 8
-#endif
-#ifndef PF_BITS_NT
-#define PF_BITS_NT 256
-#endif
-constexpr int RT = PF_BITS_RT;   // output rows per tile
-constexpr int NS = PF_BITS_NS;   // output 32-column segments per strip
-constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
-#ifndef PF_BITS_RING
-#define PF_BITS_RING (2 * SR)
-#endif
-// Ring slots: the current window + the next tile's rows, or (2 * SR) the next
-// item's whole window, prefetched during an item's last tile.
-constexpr int RING = PF_BITS_RING;
-constexpr bool kCrossPrefetch = RING >= 2 * SR;
-static_assert(RING >= SR + RT, "the ring must hold a window and the next tile's rows");
-constexpr int SS = NS + 2;       // intent / resolution segments: -1 .. NS
-constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index = si + 1)
-static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
-constexpr int NT = PF_BITS_NT;   // threads per CTA
-// Resident CTAs per SM (register budget 65536 / (NT * CTAS)): 4 (64
-// registers) for LEM and for small (480^2-class, replica-batched) ACO grids;
-// 3 (80 registers, no spills) for large ACO grids, which are pure pheromone
-// streams and lose more to spills than the extra warps hide (A/B at step
-// 150: C5 ACO +2%, C4 x64 ACO -5%, C5 LEM -12%, C3 x64 LEM -11%).
-constexpr int kRegCtas = NT == 256 ? 4 : 65536 / (NT * 64);
-constexpr int NW = NT / 32;
-constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
-constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
-constexpr int NU = DROWS * SS;   // intent units (>= resolution units AROWS * SS)
-static_assert(NU * 32 < (1 << 16), "work-list bit counts must fit 16 bits");
-
-struct Smem {
-    uint2 pl[RING][SP];             // staged {v30, v31} planes; pl[.][si + 1] = segment si
-    uint32_t D[8][DROWS][SS + 2];   // intent planes, D[.][.][si + 1]; the end columns stay 0
-    uint32_t A[AROWS][SS];
-    uint32_t K[3][AROWS][SS];
-    uint32_t G[2][RT][SS];          // grants (vacates) onto owned rows, double-buffered per tile
-    uint32_t dirty[2][RT];          // owned row has an arrival or a vacate
-    // Scalar work list (S1 draws, then reused for S2 contested cells): one
-    // entry per unit with work, in the order a packed counter handed out
-    // (entry count << 16 | bit count, one native 32-bit shared atomic; at
-    // most NU * 32 < 2^16 bits), so qp (first rank of the entry) is sorted
-    // and rank r maps to its (unit, bit) by binary search. Bounded by the
-    // unit count: it cannot overflow.
-    uint32_t qu[NU];  // unit
-    uint32_t qm[NU];  // its bits
-    uint32_t qp[NU];  // rank of its first bit
-    // S3: per warp, the words (and ACO tours) at the sources of its row's
-    // arrivals, fetched for all segments at once by cp.async.
-    uint32_t asw[NW][NS][32];
-    unsigned long long mbar[2];
-    uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
-    int item;
-    uint32_t cnt[3];
-    double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
-};
-constexpr size_t kSmemBytes[2] = {offsetof(Smem, atr), sizeof(Smem)};  // [ACO]
-
-__device__ __forceinline__ uint32_t bit(uint32_t x, int j) { return (x >> j) & 1u; }
-
-// Value of a plane at column c-1 (shift in from the left segment) / c+1.
-__device__ __forceinline__ uint32_t from_left(uint32_t x, uint32_t left) { return (x << 1) | (left >> 31); }
-__device__ __forceinline__ uint32_t from_right(uint32_t x, uint32_t right) { return (x >> 1) | (right << 31); }
-
-// --- TMA bulk copy (cp.async.bulk) + mbarrier ---------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(m))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        "  .reg .pred done;\n"
-        "WAIT_%=:\n"
-        "  mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
-        "  @!done bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(m)),
-        "r"(parity)
-        : "memory");
+int bits_strip_segments(int width, int model) {
+    if (model == 1) return 8;
+    const int ws = (width + 31) / 32;
+    auto units = [ws](int ns) { return ((ws + ns - 1) / ns) * (ns + 2); };
+    return units(10) < units(8) ? 10 : 8;
 }
 
-// --- cp.async (LDGSTS) of single words into shared memory ----------------
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
+int configure_step_bits() { return bits_ns8::configure() | bits_ns10::configure(); }
 
-// Ring slot of staged row sr (0 = tile row -3) for a window starting at base.
-__device__ __forceinline__ int slot(int base, int sr) {
-    const int s = base + sr;
-    return s >= RING ? s - RING : s;
-}
-
-__device__ __forceinline__ uint32_t empty_of(uint2 p) { return ~(p.x | p.y); }
-
-// Emptiness around one intent unit: the eight neighbour planes, shifted so
-// bit j is the neighbour of column j.
-struct Around {
-    uint32_t em, emL, emR, e0L, e0R, ep, epL, epR;
-};
-
-__device__ __forceinline__ Around around(const Smem& sm, int base, int sr, int si) {
-    const uint2* rm = sm.pl[slot(base, sr - 1)] + si + 1;
-    const uint2* r0 = sm.pl[slot(base, sr)] + si + 1;
-    const uint2* rp = sm.pl[slot(base, sr + 1)] + si + 1;
-    Around n;
-    n.em = empty_of(rm[0]);
-    n.ep = empty_of(rp[0]);
-    const uint32_t e0 = empty_of(r0[0]);
-    n.emL = from_left(n.em, empty_of(rm[-1]));
-    n.emR = from_right(n.em, empty_of(rm[1]));
-    n.e0L = from_left(e0, empty_of(r0[-1]));
-    n.e0R = from_right(e0, empty_of(r0[1]));
-    n.epL = from_left(n.ep, empty_of(rp[-1]));
-    n.epR = from_right(n.ep, empty_of(rp[1]));
-    return n;
-}
-
-// Claims on the destinations of resolution unit (row ai-1, segment si).
-__device__ __forceinline__ void claims(const Smem& sm, int ai, int si, uint32_t (&C)[8]) {
-    const int dm = ai, d0 = ai + 1, dp = ai + 2;  // intent rows of rr-1, rr, rr+1
-    auto D = [&](int k, int row, int s) -> uint32_t { return sm.D[k][row][s + 1]; };
-    C[0] = from_left(D(7, dm, si), D(7, dm, si - 1));
-    C[1] = D(6, dm, si);
-    C[2] = from_right(D(5, dm, si), D(5, dm, si + 1));
-    C[3] = from_left(D(4, d0, si), D(4, d0, si - 1));
-    C[4] = from_right(D(3, d0, si), D(3, d0, si + 1));
-    C[5] = from_left(D(2, dp, si), D(2, dp, si - 1));
-    C[6] = D(1, dp, si);
-    C[7] = from_right(D(0, dp, si), D(0, dp, si + 1));
-    const uint32_t segmask = si == 0 ? 0x80000000u : (si == SS - 1 ? 0x00000001u : 0xFFFFFFFFu);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) C[k] &= segmask;
-}
-
-// OR the source-grant bits of winners `wk` (direction k) at destination row
-// rr of segment si into G.
-__device__ __forceinline__ void grant(Smem& sm, int cur, int rr, int si, int k, uint32_t wk) {
-    const int g = rr + kDR[k];
-    if (g < 0 || g >= RT) return;
-    sm.dirty[cur][g] = 1u;
-    const int dc = kDC[k];
-    if (dc == 0) {
-        atomicOr(&sm.G[cur][g][si], wk);
-    } else if (dc < 0) {
-        atomicOr(&sm.G[cur][g][si], wk >> 1);
-        if ((wk & 1u) && si > 0) atomicOr(&sm.G[cur][g][si - 1], 0x80000000u);
-    } else {
-        atomicOr(&sm.G[cur][g][si], wk << 1);
-        if ((wk >> 31) && si + 1 < SS) atomicOr(&sm.G[cur][g][si + 1], 1u);
-    }
-}
-
-// Add unit u's bits `mask` to work list `list`.
-__device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t mask) {
-    const uint32_t old = atomicAdd(qc, (1u << 16) | uint32_t(__popc(mask)));
-    const int e = int(old >> 16);
-    sm.qu[e] = uint32_t(u);
-    sm.qm[e] = mask;
-    sm.qp[e] = old & 0xFFFFu;
-}
-
-// Position of the k-th (0-based) set bit of m.
-__device__ __forceinline__ int nth_bit(uint32_t m, int k) {
-    int pos = 0;
-#pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) {
-        const int c = __popc(m & ((1u << w) - 1u));
-        if (k >= c) {
-            k -= c;
-            m >>= w;
-            pos += w;
-        }
-    }
-    return pos;
-}
-
-// Work-list rank r -> (unit, bit), n entries.
-__device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t r, int& u, int& j) {
-    int lo = 0, hi = int(n) - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sm.qp[mid] <= r) lo = mid;
-        else hi = mid - 1;
-    }
-    u = int(sm.qu[lo]);
-    j = nth_bit(sm.qm[lo], int(r - sm.qp[lo]));
-}
-
-}  // namespace
-
-// Intent of the draw-path agent at bit j of intent unit (di, si):
-// lem_select / aco_select (src/lem.cpp:28-60, src/aco.cpp:64-92). The agent's
-// id (the selection key, src/engine.cpp:82) is read from its cell word: the
-// cell is occupied at step start, so no thread writes it during this step.
-template <bool ACO>
-__device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, int base, const uint32_t* cells,
-                                           const double2* __restrict__ tin, int di, int si, int j, bool bottom,
-                                           int r0, int c0, uint64_t seed, uint32_t step) {
-    const int sr = di + 1;
-    const int W = a.k.W;
-    const int b = kGhost + r0 + di - 2;
-    const int c = c0 + 32 * (si - 1) + j;
-    const uint32_t id = cells[size_t(b) * W + c] & kIdMask;
-    const Around n = around(sm, base, sr, si);
-    uint32_t open;  // goal-relative slots F FL FR L R B BL BR
-    if (!bottom)
-        open = bit(n.ep, j) | bit(n.epL, j) << 1 | bit(n.epR, j) << 2 | bit(n.e0L, j) << 3 | bit(n.e0R, j) << 4 |
-               bit(n.em, j) << 5 | bit(n.emL, j) << 6 | bit(n.emR, j) << 7;
-    else
-        open = bit(n.em, j) | bit(n.emR, j) << 1 | bit(n.emL, j) << 2 | bit(n.e0R, j) << 3 | bit(n.e0L, j) << 4 |
-               bit(n.ep, j) << 5 | bit(n.epR, j) << 6 | bit(n.epL, j) << 7;
-    int s;
-    if (!ACO) {
-        s = lem_choose(a.kc, open, seed, step, id);
-    } else {
-        // All eight neighbour loads are issued before any is used (they are
-        // in bounds for every agent cell: rows b-1 .. b+1 lie inside the
-        // buffer and a column step off the row lands in the adjacent row).
-        const double* t0 = reinterpret_cast<const double*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
-        double tn[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-            tn[i] = __ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code]));
-        }
-        double num[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            num[i] = (open >> i & 1u) ? __dmul_rn(pheromone_term(a.kc, tn[i]), __ldg(&a.kc->eta[i])) : 0.0;
-        s = aco_choose(num, open, seed, step, id);
-    }
-    return bottom ? 7 - kSlotCodeTop[s] : kSlotCodeTop[s];
-}
-
-// Keyed draw for a contested destination at bit j of resolution unit (ai, si):
-// the winner's row-major code (src/engine.cpp:116-120).
-__device__ __forceinline__ int draw_winner(const StepArgs& a, const Smem& sm, int ai, int si, int j, int r0, int c0,
-                                           uint64_t seed, uint32_t step) {
-    uint32_t C[8];
-    claims(sm, ai, si, C);
-    uint32_t m = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) m |= bit(C[k], j) << k;
-    const int64_t grow = int64_t(a.row_begin) + r0 + ai - 1;
-    const int gcol = c0 + 32 * (si - 1) + j;
-    return resolve(m, seed, step, uint64_t(grow) * uint64_t(a.k.W) + uint64_t(gcol));
-}
-
-__device__ __forceinline__ void set_winner(Smem& sm, int cur, int ai, int si, int j, int k) {
-    const uint32_t b = 1u << j;
-    if (k & 1) atomicOr(&sm.K[0][ai][si], b);
-    if (k & 2) atomicOr(&sm.K[1][ai][si], b);
-    if (k & 4) atomicOr(&sm.K[2][ai][si], b);
-    grant(sm, cur, ai - 1, si, k, b);
-}
-
-// One work item: a chunk of consecutive RT-row tiles of one strip of one
-// replica.
-struct Item {
-    int rep, strip, chunk, c0, t_first, t_end;
-};
-
-__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item) {
-    Item it;
-    it.rep = item / (strips * n_chunks);
-    it.strip = (item / n_chunks) % strips;
-    it.chunk = item % n_chunks;
-    it.c0 = it.strip * (NS * 32);
-    it.t_first = it.chunk * tiles_per_item;
-    it.t_end = min(it.t_first + tiles_per_item, n_tiles);
-    return it;
-}
-
-// Issue the TMA loads of `nrows` staged plane rows (tile rows first_sr..,
-// relative to the tile at r0) of item `it` into their ring slots, completing
-// on mbarrier m; rows past the end of the buffer are written as walls. Each
-// row is one 16-byte-aligned run of SP segments (the row padding holds walls
-// beyond the grid's columns). Called by one full warp.
-__device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parity, const Item& it, int r0, int base,
-                                          int first_sr, int nrows, unsigned long long* m) {
-    const int lane = threadIdx.x & 31;
-    const uint2* src = a.p.occ[parity] + size_t(it.rep) * a.p.occ_plane + size_t(it.strip) * NS;
-    const int b_first = kGhost + r0 - 3 + first_sr;
-    const int nvalid = max(0, min(nrows, a.rows_buf - b_first));
-    if (lane == 0) mbar_expect_tx(m, uint32_t(nvalid) * uint32_t(SP * 8));
-    __syncwarp();
-    for (int i = lane; i < nvalid; i += 32)
-        bulk_g2s(&sm.pl[slot(base, first_sr + i)][0], src + size_t(b_first + i) * a.p.wsp, uint32_t(SP * 8), m);
-    for (int i = nvalid * SP + lane; i < nrows * SP; i += 32)
-        sm.pl[slot(base, first_sr + i / SP)][i % SP] = make_uint2(kWall, kWall);
-}
-
-// Fused halo exchange (linked shards only): after a tile's commit, its rows
-// that are ghost rows of a neighbour shard (this shard's first / last kGhost
-// owned rows) are copied from where the commit just wrote them (L2) into the
-// neighbour's ghost rows: occupancy planes and pheromone of the new parity,
-// words and tours in place (a stale word under an empty plane bit is as
-// harmless there as here). Called by the whole CTA after the end-of-tile
-// barrier; the system fence orders the stores before the step's completion
-// flag (launch_halo_signal).
-template <bool ACO>
-__device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int rep, int strip, int r0) {
-    const int W = a.k.W;
-    const int c0 = strip * NS * 32, ncols = min(NS * 32, W - c0);
-    const size_t pb = size_t(rep) * a.p.plane, ob = size_t(rep) * a.p.occ_plane;
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        const PeerRows pr = a.peer[s];
-        if (!pr.cell) continue;
-        const int lo = max(r0, s == 0 ? 0 : a.rows_owned - kGhost);
-        const int hi = min(min(r0 + RT, a.rows_owned), s == 0 ? kGhost : a.rows_owned);
-        for (int lr = lo; lr < hi; ++lr) {
-            const int b = kGhost + lr, pbr = b + pr.row_delta;
-            const size_t src = pb + size_t(b) * W + c0, dst = size_t(rep) * pr.plane + size_t(pbr) * W + c0;
-            for (int i = threadIdx.x; i < ncols; i += NT) {
-                pr.cell[dst + i] = a.p.cell[0][src + i];
-                if (ACO) {
-                    pr.tour[dst + i] = a.p.tour[src + i];
-                    pr.tau[parity ^ 1][dst + i] = a.p.tau[parity ^ 1][src + i];
-                }
-            }
-            if (threadIdx.x < NS) {
-                const size_t q = size_t(strip) * NS + 2 + threadIdx.x;
-                pr.occ[parity ^ 1][size_t(rep) * pr.occ_plane + size_t(pbr) * a.p.wsp + q] =
-                    a.p.occ[parity ^ 1][ob + size_t(b) * a.p.wsp + q];
-            }
-        }
-    }
-    __threadfence_system();
-}
-
-template <bool ACO, int CTAS, bool MIRROR>
-__global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-
-    const int W = a.k.W;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t step = *a.d_step + uint32_t(slot_idx);
-    const int strips = (W + NS * 32 - 1) / (NS * 32);
-    const int n_tiles = (a.rows_owned + RT - 1) / RT;
-    const int n_chunks = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
-    const int n_items = strips * n_chunks * a.replicas;
-    uint32_t* work = a.work + step % uint32_t(a.report_cap);
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.mbar[0], 1);
-        mbar_init(&sm.mbar[1], 1);
-        fence_mbar_init();
-        sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
-        sm.qc[0][0] = sm.qc[0][1] = sm.qc[1][0] = sm.qc[1][1] = 0u;
-    }
-    for (int i = threadIdx.x; i < 2 * RT * SS; i += NT) (&sm.G[0][0][0])[i] = 0u;
-    for (int i = threadIdx.x; i < 2 * RT; i += NT) (&sm.dirty[0][0])[i] = 0u;
-    for (int i = threadIdx.x; i < 8 * DROWS; i += NT) {  // the zero end columns of the intent planes
-        sm.D[i / DROWS][i % DROWS][0] = 0u;
-        sm.D[i / DROWS][i % DROWS][SS + 1] = 0u;
-    }
-    __syncthreads();
-    // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
-    // taken from a per-step counter so heavy (crowded) chunks balance out.
-    // The next item is claimed during the current item's last tile and its
-    // first window is loaded into the other half of the ring meanwhile.
-    int item = 0;
-    if (warp == 0) {
-        if (lane == 0) item = int(atomicAdd(work, 1u));
-        item = __shfl_sync(0xFFFFFFFFu, item, 0);
-        if (lane == 0) sm.item = item;
-        if (item < n_items) {
-            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
-            load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
-        }
-    }
-    __syncthreads();  // item id and wall rows written by warp 0 are visible to all
-    item = sm.item;
-    uint32_t moved = 0, ntop = 0, nbot = 0;
-    uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
-    int base = 0;                               // ring slot of staged row 0 of the current tile
-    int cur = 0;                                // tile parity: G / dirty / work-list counters
-    uint32_t* const cells = a.p.cell[0];
-    while (item < n_items) {
-    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
-    const int rep = it.rep, c0 = it.c0;
-    const uint64_t seed = __ldg(&a.rep[rep].seed);
-    const int band = __ldg(&a.rep[rep].band);
-    const size_t plane_base = size_t(rep) * a.p.plane;
-    uint32_t* const cw = cells + plane_base;
-    uint2* const oout = a.p.occ[parity ^ 1] + size_t(rep) * a.p.occ_plane + size_t(it.strip) * NS + 2;
-    const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
-    double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + plane_base : nullptr;
-    double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
-    int next_base = 0;
-
-    for (int t = it.t_first; t < it.t_end; ++t) {
-        const int r0 = t * RT;               // owned-local row of the tile
-        const uint32_t my_load = nload - 1;  // the load that brought this tile's new rows
-        // Prefetch into the half of the ring this tile does not use (its
-        // previous readers all passed the end-of-tile barrier): the next
-        // tile's RT new rows, or on the last tile the next item's window.
-        if (t + 1 < it.t_end) {
-            if (warp == 0) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
-            ++nload;
-        } else {
-            next_base = kCrossPrefetch ? slot(base, SR) : 0;
-            if (warp == 0) {
-                int nx = 0;
-                if (lane == 0) nx = int(atomicAdd(work, 1u));
-                nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
-                if (lane == 0) sm.item = nx;
-                if (kCrossPrefetch && nx < n_items) {
-                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta);
-                    load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
-                }
-            }
-        }
-        // Scratch of the NEXT tile (its last readers passed the previous
-        // end-of-tile barrier; its first writers come after this tile's).
-        for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[cur ^ 1][0][0])[i] = 0u;
-        if (threadIdx.x < RT) sm.dirty[cur ^ 1][threadIdx.x] = 0u;
-        if (threadIdx.x == 0) sm.qc[cur ^ 1][0] = sm.qc[cur ^ 1][1] = 0u;
-        mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
-
-        // ------------------------------------------------------------ S1
-        // Intents for rows -2 .. RT+1, all staged segments (halo segments
-        // only at the two columns next to the strip).
-        for (int u = threadIdx.x; u < DROWS * SS; u += NT) {
-            const int di = u / SS, si = u - di * SS;  // di = rr + 2
-            const uint2 p = sm.pl[slot(base, di + 1)][si + 1];
-            const Around n = around(sm, base, di + 1, si);
-            const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
-            const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
-            uint32_t d[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) d[q] = 0u;
-            d[6] = T & n.ep;  // Top forward: (+1, 0)
-            d[1] = B & n.em;  // Bottom forward: (-1, 0)
-            const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
-            const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) enqueue(sm, &sm.qc[cur][0], u, slow);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
-        }
-        __syncthreads();
-        // Draws, spread evenly over the CTA (the barrier is skipped,
-        // uniformly, when there are none).
-        if (const uint32_t nq = sm.qc[cur][0] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[cur][0] >> 16;
-            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                int u, j;
-                list_entry(sm, ne, e, u, j);
-                const int di = u / SS, si = u - di * SS;
-                const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
-                const int code = draw_intent<ACO>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
-                atomicOr(&sm.D[code][di][si + 1], 1u << j);
-            }
-            __syncthreads();
-        }
-
-        // ------------------------------------------------------------ S2
-        // Claims, winners and grants for destinations in rows -1 .. RT.
-        for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
-            const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
-            uint32_t C[8];
-            claims(sm, ai, si, C);
-            uint32_t ones = 0u, twos = 0u;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                twos |= ones & C[q];
-                ones |= C[q];
-            }
-            uint32_t win[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
-            sm.A[ai][si] = ones;
-            if (ones && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
-            sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
-            sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
-            sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (win[q]) grant(sm, cur, ai - 1, si, q, win[q]);
-            if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
-        }
-        __syncthreads();
-        if (const uint32_t nq = sm.qc[cur][1] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[cur][1] >> 16;
-            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                int u, j;
-                list_entry(sm, ne, e, u, j);
-                const int ai = u / SS, si = u - ai * SS;
-                set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
-            }
-            __syncthreads();
-        }
-
-        // ------------------------------------------------------------ S3
-        for (int rr = warp; rr < RT; rr += NW) {
-            const int lr = r0 + rr;
-            if (lr >= a.rows_owned) break;
-            const int b = kGhost + lr;
-            const int grow = a.row_begin + lr;
-            const int rs = slot(base, rr + 3), ai = rr + 1;
-            uint2* const orow = oout + size_t(b) * a.p.wsp;
-            if (!ACO && !sm.dirty[cur][rr]) {
-                // Nothing arrives or leaves in this row: its planes are copied.
-                if (lane < NS) orow[lane] = sm.pl[rs][lane + 2];
-                continue;
-            }
-            const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
-            // ACO: issue the whole row's pheromone loads before using any of them
-            // (and before the arrival-source fetch, so both round trips overlap).
-            double2 tv[NS];
-            if (ACO) {
-#pragma unroll
-                for (int s = 0; s < NS; ++s)
-                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
-            }
-            // The sources of this row's arrivals: all their loads are in
-            // flight together (one round trip per row, not one per segment).
-            // Each source is occupied at step start, so nothing writes it.
-#pragma unroll
-            for (int si = 1; si <= NS; ++si) {
-                if (bit(sm.A[ai][si], lane)) {
-                    const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                       bit(sm.K[2][ai][si], lane) << 2);
-                    const size_t src = size_t(b + kDR[kc]) * W + (c0 + 32 * (si - 1) + lane + kDC[kc]);
-                    cp_async<4>(&sm.asw[warp][si - 1][lane], cw + src);
-                    if (ACO) cp_async<8>(&sm.atr[warp][si - 1][lane], tour + src);
-                }
-            }
-            cp_async_wait_all();
-            __syncwarp();
-            uint2 mine = make_uint2(kWall, kWall);
-#pragma unroll
-            for (int si = 1; si <= NS; ++si) {
-                const int gc = c0 + 32 * (si - 1) + lane;
-                const bool valid = gc < W;
-                const uint32_t Am = sm.A[ai][si], Gm = sm.G[cur][rr][si];
-                uint2 np = sm.pl[rs][si + 1];
-                const size_t gi = row0 + 32 * (si - 1);
-                if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
-                    if (ACO && valid) {
-                        const double2 tt = tv[si - 1];
-                        tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
-                    }
-                } else {
-                    const bool arrived = bit(Am, lane) != 0u;
-                    uint32_t group = 0;
-                    double tour_new = 0.0;
-                    if (arrived) {
-                        const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                           bit(sm.K[2][ai][si], lane) << 2);
-                        const uint32_t sw = sm.asw[warp][si - 1][lane];
-                        group = sw >> 30;
-                        uint32_t nw = sw;
-                        if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
-                            nw |= kCrossedBit;
-                            if (group == 1u) ++ntop;
-                            else ++nbot;
-                        }
-                        ++moved;
-                        cw[gi] = nw;  // empty at step start: nobody reads it this step
-                        if (ACO) {    // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
-                            tour_new = __dadd_rn(sm.atr[warp][si - 1][lane], is_diag(kc) ? a.k.diag : 1.0);
-                            tour[gi] = tour_new;
-                        }
-
-                    }
-                    const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
-                    const uint32_t bot = __ballot_sync(0xFFFFFFFFu, group == 2u);
-                    np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
-                    np.y = (np.y & ~Gm) | bot;
-                    if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
-                        double2 tt = tv[si - 1];
-                        tt.x = __dmul_rn(tt.x, a.k.factor);
-                        tt.y = __dmul_rn(tt.y, a.k.factor);
-                        if (arrived) {
-                            const double dep = __ddiv_rn(a.k.q, tour_new);
-                            if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
-                            else tt.y = __dadd_rn(tt.y, dep);
-                        }
-                        tout[gi] = tt;
-                    }
-                }
-                if (lane == si - 1) mine = np;
-            }
-            if (lane < NS) orow[lane] = mine;
-        }
-        __syncthreads();  // end of tile: the window's slots may be refilled
-        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, parity, rep, it.strip, r0);
-        base = slot(base, RT);
-        cur ^= 1;
-    }
-    base = next_base;
-    // Counters of this item go to its replica's StepReport (src/engine.cpp:172-174).
-    moved = __reduce_add_sync(0xFFFFFFFFu, moved);
-    ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);
-    nbot = __reduce_add_sync(0xFFFFFFFFu, nbot);
-    if (lane == 0 && (moved | ntop | nbot)) {
-        atomicAdd(&sm.cnt[0], moved);
-        atomicAdd(&sm.cnt[1], ntop);
-        atomicAdd(&sm.cnt[2], nbot);
-    }
-    moved = ntop = nbot = 0u;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t* rep_slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
-        if (it.strip == 0 && it.chunk == 0) rep_slot[0] = step;
-        if (sm.cnt[0]) atomicAdd(&rep_slot[1], sm.cnt[0]);
-        if (sm.cnt[1]) atomicAdd(&rep_slot[2], sm.cnt[1]);
-        if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
-        sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
-    }
-    item = sm.item;  // claimed during the last tile (visible after its barriers)
-    if (!kCrossPrefetch && item < n_items) {
-        // Small ring: the next item's window is loaded only now, into the
-        // slots the finished item released.
-        if (warp == 0) {
-            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
-            load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
-        }
-        __syncthreads();  // wall rows written by warp 0 are visible to all
-    }
-    if (item < n_items) ++nload;
-    }  // work items
-}
-
-// CTAs per SM: the register budget (kRegCtas), capped by shared memory (1 KB
-// reserved per CTA); one fewer (more registers) for large ACO grids.
-constexpr int smem_ctas(bool aco) { return int((228 * 1024) / (kSmemBytes[aco ? 1 : 0] + 1024)); }
-constexpr int kCtasLem = kRegCtas < smem_ctas(false) ? kRegCtas : smem_ctas(false);
-constexpr int kCtasDefault = kRegCtas < smem_ctas(true) ? kRegCtas : smem_ctas(true);
-constexpr int kCtasHbm = kCtasDefault > 1 && NT == 256 ? 3 : kCtasDefault;
-static_assert(kCtasLem >= 1 && kCtasDefault >= 1, "shared memory must fit one CTA per SM");
-
-int configure_step_bits() {
-    const int lem = int(kSmemBytes[0]), aco = int(kSmemBytes[1]);
-    for (auto f : {step_bits_kernel<false, kCtasLem, false>, step_bits_kernel<false, kCtasLem, true>})
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lem) != cudaSuccess) return 1;
-    for (auto f : {step_bits_kernel<true, kCtasDefault, false>, step_bits_kernel<true, kCtasHbm, false>,
-                   step_bits_kernel<true, kCtasDefault, true>, step_bits_kernel<true, kCtasHbm, true>})
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, aco) != cudaSuccess) return 1;
-    return 0;
-}
-
-int bits_strip_segments() { return NS; }
-
-// Persistent grid: one CTA per resident slot (SMs x 3 or 4) at most. Work
-// items are chunks of up to 16 consecutive RT-row tiles of one strip of one
-// replica, sized so there are about 32 items per CTA (a short tail at the
-// end of the step; consecutive tiles of an item share their halo rows).
-int launch_step_bits(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
-    const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
-    const int n_tiles = (a.rows_owned + RT - 1) / RT;
-    const bool aco = a.k.model == 1;
-    const bool hbm = aco && double(a.k.W) * a.rows_buf >= double(1 << 22);  // >= 4M cells per replica
-    const int ctas = !aco ? kCtasLem : (hbm ? kCtasHbm : kCtasDefault);
-    const long long ctas_max = (long long)a.num_sms * ctas;
-    const long long tiles = (long long)strips * n_tiles * a.replicas;
-    StepArgs b = a;
-    b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));
-    const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
-    dim3 grid(unsigned(std::min(items, ctas_max)));
-    const size_t bytes = kSmemBytes[aco ? 1 : 0];
-    const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
-    if (!aco) {
-        if (mirror) step_bits_kernel<false, kCtasLem, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<false, kCtasLem, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    } else if (hbm) {
-        if (mirror) step_bits_kernel<true, kCtasHbm, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<true, kCtasHbm, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    } else {
-        if (mirror) step_bits_kernel<true, kCtasDefault, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<true, kCtasDefault, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-    }
-    return 1;
+int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s) {
+    return a.strip_segs == 10 ? bits_ns10::launch(a, slot, parity, s) : bits_ns8::launch(a, slot, parity, s);
 }
 
 }  // namespace pfk

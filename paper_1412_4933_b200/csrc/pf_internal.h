@@ -63,13 +63,14 @@ struct StepArgs {
     int num_sms;
     int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
     PeerRows peer[2];       // [0] the shard above (toward row 0), [1] below; cell == nullptr: none
+    int strip_segs;         // bit kernel: 32-column segments per strip (bits_strip_segments)
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
 // Returns the number of kernel launches issued.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s);   // PF_KERNEL_FUSED
 int configure_step_bits();
-int bits_strip_segments();  // NS: the plane pitch is a multiple of it plus 4
+int bits_strip_segments(int width, int model);  // strip width in segments (8 or 10)
 // Occupancy planes of rows [0, rows) from cell words (W columns; padding
 // segments untouched); written to occ0 and, if non-null, occ1.
 int launch_build_occ(const uint32_t* words, int W, int rows, int wsp, uint2* occ0, uint2* occ1, cudaStream_t s);

@@ -11,9 +11,8 @@ mkdir -p tools/debug
 TMP=$(mktemp -d)
 git archive "$REF" paper_1412_4933_b200/csrc include | tar -x -C "$TMP"
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off"
-SRCS="pf_kernels.cu pf_bitstep.cu pf_context.cu pf_setup.cpp"
-nvcc $FLAGS -I "$TMP/include" -shared -o tools/debug/lib_base.so $(for s in $SRCS; do echo "$TMP/paper_1412_4933_b200/csrc/$s"; done) &
-nvcc $FLAGS $NEW_FLAGS -I include -shared -o tools/debug/lib_new.so $(for s in $SRCS; do echo "paper_1412_4933_b200/csrc/$s"; done) &
+nvcc $FLAGS -I "$TMP/include" -shared -o tools/debug/lib_base.so $(ls "$TMP"/paper_1412_4933_b200/csrc/*.cu "$TMP"/paper_1412_4933_b200/csrc/*.cpp) &
+nvcc $FLAGS $NEW_FLAGS -I include -shared -o tools/debug/lib_new.so $(ls paper_1412_4933_b200/csrc/*.cu paper_1412_4933_b200/csrc/*.cpp) &
 wait
 rm -rf "$TMP"
 echo "built tools/debug/lib_base.so ($REF) and tools/debug/lib_new.so (working tree)"
