@@ -54,6 +54,32 @@ def test_random_config_vs_oracle(kw):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kw", [
+    # LEM takes 320-column strips when they need fewer units per row: 624 = 19.5 segments
+    # (a half segment at the edge, a 2-segment last strip), 960 = 3 whole strips.
+    dict(width=624, height=96, agents_per_side=9000, model="lem", seed=77),
+    dict(width=960, height=64, agents_per_side=12000, model="lem", seed=78),
+    # the same widths with ACO (256-column strips): 624 -> a 3-segment last strip
+    dict(width=624, height=96, agents_per_side=9000, model="aco", seed=79),
+], ids=lambda kw: f"{kw['model']}{kw['width']}x{kw['height']}")
+def test_strip_widths_vs_oracle(kw):
+    """Grid widths that exercise both compiled strip widths (8 and 10
+    segments), partial last strips and a half-filled last segment."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    steps = 120
+    ora = OracleState(to_scenario(kw))
+    orep = ora.run(steps)
+    cfg = to_config(kw)
+    state = p.new_environment(cfg, kw["seed"])
+    eng = p.StepEngine(p.EngineOptions.from_config(cfg, kw["seed"]))
+    rep = eng.run_array(state, steps)
+    assert (rep == orep).all(), "per-step reports differ"
+    assert first_divergence(state, ora) == "identical"
+
+
+@pytest.mark.gpu
 def test_alpha_fractional_matches_oracle():
     """alpha not in {0,1} uses pow (tolerance-only by contract); in practice the
     trajectories and fields still agree for this scenario."""
