@@ -122,7 +122,10 @@ struct Smem {
     uint32_t asw[NW][NS][32];
     unsigned long long mbar[2];
     uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
-    int item;
+    // Next work item. Double-buffered by the parity of the item that claims it:
+    // with one-tile items the next claim can come before the slowest warp
+    // has read the previous one (no barrier in between).
+    int item[2];
     uint32_t cnt[3];
     double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
 };
@@ -455,14 +458,15 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     if (warp == 0) {
         if (lane == 0) item = int(atomicAdd(work, 1u));
         item = __shfl_sync(0xFFFFFFFFu, item, 0);
-        if (lane == 0) sm.item = item;
+        if (lane == 0) sm.item[1] = item;
         if (item < n_items) {
             const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
             load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
         }
     }
     __syncthreads();  // item id and wall rows written by warp 0 are visible to all
-    item = sm.item;
+    item = sm.item[1];
+    int ipar = 0;     // the current item's last tile claims the next one into sm.item[ipar]
     uint32_t moved = 0, ntop = 0, nbot = 0;
     uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
     int base = 0;                               // ring slot of staged row 0 of the current tile
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 int nx = 0;
                 if (lane == 0) nx = int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
-                if (lane == 0) sm.item = nx;
+                if (lane == 0) sm.item[ipar] = nx;
                 if (kCrossPrefetch && nx < n_items) {
                     const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta);
                     load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
@@ -701,7 +705,8 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
     }
-    item = sm.item;  // claimed during the last tile (visible after its barriers)
+    item = sm.item[ipar];  // claimed during the last tile (visible after its barriers)
+    ipar ^= 1;
     if (!kCrossPrefetch && item < n_items) {
         // Small ring: the next item's window is loaded only now, into the
         // slots the finished item released.

@@ -1,0 +1,41 @@
+"""Small workloads for compute-sanitizer (dev tool): every step kernel
+variant on a few small grids, including linked shards (fused halo).
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_run.py
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+    compute-sanitizer --tool synccheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1412_4933_b200 as p  # noqa: E402
+from paper_1412_4933_b200 import _lib  # noqa: E402
+from paper_1412_4933_b200.engine import _pf_config  # noqa: E402
+from paper_1412_4933_b200.sharding import row_partition  # noqa: E402
+
+steps = int(os.environ.get("STEPS", "12"))
+C = p.ScenarioConfig
+for model in (p.Model.Lem, p.Model.Aco):
+    # (the 48-replica batch gives CTAs several one-tile work items)
+    for w, h, n, reps in ((96, 96, 2000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 2000, 48)):
+        cfg = C(width=w, height=h, agents_per_side=n, model=model, seed=5)
+        for kernel in ("fused", "tile", "pipeline"):
+            e = p.Ensemble(cfg, replicas=reps, kernel=kernel)
+            e.run(steps)
+            e.state(0)
+            e.audit(0)
+            e.close()
+        shards = []
+        for lo, hi in row_partition(h, 2):
+            c = _lib.Context(_pf_config(cfg, 5, replicas=reps, row_begin=lo, row_end=hi))
+            c.init_environment()
+            shards.append(c)
+        _lib.link_shards(shards)
+        for c in shards:
+            c.step_async(steps)
+        for c in shards:
+            c.synchronize()
+            c.close()
+        print(f"ok {model.name} {w}x{h} n={n} x{reps}", flush=True)
+print("sanitize_run done")
