@@ -197,6 +197,18 @@ int pf_selftest_rng(int32_t device, uint32_t n, const uint64_t* seed, const uint
                     const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits_out,
                     double* uniform_out, double* normal_out);
 
+/* Device self-test of the selection functions the step kernels use, over n
+ * keys (seed, step, entity): kind 0 lem_select (src/lem.cpp:20-61; scores
+ * from d0's distance table, normal(mu_sel*C, sigma_sel*C)), kind 1
+ * aco_select (src/aco.cpp:59-93) with caller numerators num[8*i..8*i+7],
+ * kind 2 the movement-phase winner draw (src/engine.cpp:116-120) among the
+ * row-major contender codes set in mask[i]. mask[i] is the goal-relative
+ * open-slot mask (bit 0 = F) for kinds 0/1. out[i] = the chosen slot / code,
+ * or -1 (stay / no contender). entity = agent id (0/1) or global cell index (2). */
+int pf_selftest_select(int32_t device, int32_t kind, uint32_t n, double d0, double sel_mu, double sel_sigma,
+                       const uint8_t* mask, const double* num, const uint64_t* seed, const uint32_t* step,
+                       const uint64_t* entity, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

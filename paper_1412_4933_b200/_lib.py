@@ -115,6 +115,8 @@ _sigs = {
     "pf_exchange_pair": (C.c_int, [_vp, _vp]),
     "pf_selftest_rng": (C.c_int, [_i32, _u32, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double, _vp, _vp, _vp]),
     "pf_audit": (C.c_int, [_vp, _i32, C.POINTER(_u64)]),
+    "pf_selftest_select": (C.c_int, [_i32, _i32, _u32, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp,
+                                     _vp]),
     "pf_peer_export": (C.c_int, [_vp, C.POINTER(PfPeerDesc)]),
     "pf_peer_attach": (C.c_int, [_vp, _i32, C.POINTER(PfPeerDesc), _i32]),
 }
@@ -282,3 +284,18 @@ def selftest_rng(seed, step, phase, entity, counter, mu=0.0, sigma=1.0, device=0
     check(lib.pf_selftest_rng(device, n, ptr(seed), ptr(step), ptr(phase), ptr(entity), ptr(counter), mu, sigma,
                               ptr(bits), ptr(uni), ptr(nrm)))
     return bits, uni, nrm
+
+
+def selftest_select(kind, mask, seed, step, entity, num=None, d0=2.0, sel_mu=1.0, sel_sigma=0.5, device=0):
+    """Device lem_select (kind 0) / aco_select (1) / winner draw (2) for arrays
+    of keys (pf_selftest_select). Returns int32 slots / codes, -1 = stay."""
+    mask = np.ascontiguousarray(mask, np.uint8)
+    n = len(mask)
+    seed = np.ascontiguousarray(np.broadcast_to(seed, n), np.uint64)
+    step = np.ascontiguousarray(np.broadcast_to(step, n), np.uint32)
+    entity = np.ascontiguousarray(np.broadcast_to(entity, n), np.uint64)
+    nm = None if num is None else np.ascontiguousarray(np.broadcast_to(num, (n, 8)), np.float64)
+    out = np.zeros(n, np.int32)
+    check(lib.pf_selftest_select(device, kind, n, d0, sel_mu, sel_sigma, ptr(mask), ptr(nm), ptr(seed), ptr(step),
+                                 ptr(entity), ptr(out)))
+    return out

@@ -1198,6 +1198,54 @@ int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
     return PF_OK;
 }
 
+int pf_selftest_select(int32_t device, int32_t kind, uint32_t n, double d0, double sel_mu, double sel_sigma,
+                       const uint8_t* mask, const double* num, const uint64_t* seed, const uint32_t* step,
+                       const uint64_t* entity, int32_t* out) {
+    if (kind < 0 || kind > 2) return fail(PF_ERR_ARG, "kind must be 0 (lem), 1 (aco) or 2 (resolve)");
+    if (!mask || !seed || !step || !entity || !out || (kind == 1 && !num)) return fail(PF_ERR_ARG, "null array");
+    if (!(d0 > 1.0)) return fail(PF_ERR_CONFIG, "d0 must be > 1");
+    if (n == 0) return PF_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PF_ERR_CUDA, "no CUDA device available");
+    PF_CUDA(cudaSetDevice(device));
+    pf_ctx tmp;  // only for fill_consts: the scores / factors exactly as a context computes them
+    tmp.cfg.d0 = d0;
+    tmp.cfg.sel_mu = sel_mu;
+    tmp.cfg.sel_sigma = sel_sigma;
+    tmp.cfg.alpha = 1.0;
+    tmp.cfg.beta = 2.0;
+    tmp.cfg.rho = 0.05;
+    tmp.cfg.q = 1.0;
+    tmp.cfg.model = kind == 1 ? PF_MODEL_ACO : PF_MODEL_LEM;
+    fill_consts(&tmp);
+    const size_t bytes = sizeof(pfdev::StepConsts) + size_t(n) * (1 + 8 + 4 + 8 + 4) + (num ? size_t(n) * 64 : 0) + 64;
+    char* d = nullptr;
+    PF_CUDA(cudaMalloc(&d, bytes));
+    auto* d_kc = reinterpret_cast<pfdev::StepConsts*>(d);
+    auto* d_seed = reinterpret_cast<uint64_t*>(d + ((sizeof(pfdev::StepConsts) + 15) & ~size_t(15)));
+    uint64_t* d_ent = d_seed + n;
+    double* d_num = reinterpret_cast<double*>(d_ent + n);
+    uint32_t* d_step = reinterpret_cast<uint32_t*>(d_num + (num ? size_t(n) * 8 : 0));
+    int32_t* d_out = reinterpret_cast<int32_t*>(d_step + n);
+    uint8_t* d_mask = reinterpret_cast<uint8_t*>(d_out + n);
+    auto run = [&]() -> int {
+        PF_CUDA(cudaMemcpy(d_kc, &tmp.args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_seed, seed, n * 8, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_ent, entity, n * 8, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_step, step, n * 4, cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemcpy(d_mask, mask, n, cudaMemcpyHostToDevice));
+        if (num) PF_CUDA(cudaMemcpy(d_num, num, size_t(n) * 64, cudaMemcpyHostToDevice));
+        pfk::launch_selftest_select(kind, n, d_kc, d_mask, num ? d_num : nullptr, d_seed, d_step, d_ent, d_out, 0);
+        PF_CUDA(cudaGetLastError());
+        PF_CUDA(cudaDeviceSynchronize());
+        PF_CUDA(cudaMemcpy(out, d_out, n * 4, cudaMemcpyDeviceToHost));
+        return PF_OK;
+    };
+    const int rc = run();
+    cudaFree(d);
+    return rc;
+}
+
 int pf_selftest_rng(int32_t device, uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                     const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits_out,
                     double* uniform_out, double* normal_out) {

@@ -108,6 +108,9 @@ int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* a
 // (40-byte pf_agent, by id); status[0] += agent cells, status[1] += bad ids.
 int launch_export_state(const uint32_t* words, const double* tour, size_t n, uint32_t W, uint32_t row0, uint8_t* occ,
                         uint32_t* index, void* agents, uint32_t n_agents, unsigned long long* status, cudaStream_t s);
+int launch_selftest_select(int kind, uint32_t n, const pfdev::StepConsts* kc, const uint8_t* mask, const double* num,
+                           const uint64_t* seed, const uint32_t* step, const uint64_t* entity, int32_t* out,
+                           cudaStream_t s);
 int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                         const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
                         double* uni, double* nrm, cudaStream_t s);

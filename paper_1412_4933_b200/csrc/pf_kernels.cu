@@ -642,6 +642,39 @@ __global__ void selftest_rng_kernel(uint32_t n, const uint64_t* seed, const uint
     nrm[i] = __dadd_rn(mu, __dmul_rn(sigma, pfdev::inverse_normal_cdf(u)));
 }
 
+// Selection self-test (pf_selftest_select): the device's lem_select /
+// aco_select (forward priority + lem_choose / aco_choose) and the cell-centric
+// resolve, exactly as the step kernels call them, over arrays of keys.
+__global__ void selftest_select_kernel(int kind, uint32_t n, const pfdev::StepConsts* kc, const uint8_t* mask,
+                                       const double* num, const uint64_t* seed, const uint32_t* step,
+                                       const uint64_t* entity, int32_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t m = mask[i];
+    int r;
+    if (kind == 2) {
+        r = m ? int(pfdev::resolve(m, seed[i], step[i], entity[i])) : -1;
+    } else if (m & 1u) {
+        r = 0;  // forward open: move forward, no draw (src/lem.cpp:23-26, src/aco.cpp:60-63)
+    } else if (m == 0u) {
+        r = -1;  // boxed in: stay
+    } else if (kind == 0) {
+        r = pfdev::lem_choose(kc, m, seed[i], step[i], uint32_t(entity[i]));
+    } else {
+        double v[8];
+        for (int k = 0; k < 8; ++k) v[k] = num[size_t(i) * 8 + k];
+        r = pfdev::aco_choose(v, m, seed[i], step[i], uint32_t(entity[i]));
+    }
+    out[i] = r;
+}
+
+int launch_selftest_select(int kind, uint32_t n, const pfdev::StepConsts* kc, const uint8_t* mask, const double* num,
+                           const uint64_t* seed, const uint32_t* step, const uint64_t* entity, int32_t* out,
+                           cudaStream_t s) {
+    selftest_select_kernel<<<(n + 255) / 256, 256, 0, s>>>(kind, n, kc, mask, num, seed, step, entity, out);
+    return 1;
+}
+
 int launch_selftest_rng(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
                         const uint64_t* entity, const uint32_t* counter, double mu, double sigma, uint64_t* bits,
                         double* uni, double* nrm, cudaStream_t s) {

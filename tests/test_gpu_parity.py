@@ -153,3 +153,88 @@ def test_c5_full_grid_anchor(anchors, name):
     state, rep = _run_gpu(a["scenario"], a["steps"])
     assert int(rep["moved"].astype(np.int64).sum()) == a["sum_moved"]
     assert hex_hashes(hashes_of(state)) == a["hash"]
+
+
+def _oracle_select(lib, kind, mask, num, seed, step, ent, d0=2.0, mu=1.0, sigma=0.5):
+    """The oracle's lem_select / aco_select (goal-relative slot, -1 stay) or
+    the movement-phase winner draw (src/engine.cpp:116-120) for one key."""
+    import ctypes as C
+
+    if kind == 2:
+        k = bin(int(mask)).count("1")
+        if k == 0:
+            return -1
+        u = lib.pfo_uniform(int(seed), int(step), 3, int(ent), 0)
+        j = min(int(u * k), k - 1)
+        return [b for b in range(8) if mask >> b & 1][j]
+    op = (C.c_uint8 * 8)(*[(int(mask) >> b) & 1 for b in range(8)])
+    if kind == 0:
+        d = (C.c_double * 8)()
+        lib.pfo_distance_table(d0, d)
+        sc = (C.c_double * 8)()
+        lib.pfo_lem_scores(op, d, sc)
+        return lib.pfo_lem_select(sc, op, int(seed), int(step), int(ent), mu, sigma)
+    return lib.pfo_aco_select((C.c_double * 8)(*num), op, int(seed), int(step), int(ent))
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2], ids=["lem_select", "aco_select", "resolve"])
+def test_device_selection_matches_oracle(kind):
+    """The selection functions the step kernels use, per key, against the
+    oracle: all open masks (F open / blocked / boxed in), random keys, random
+    ACO numerators including zeros (the degenerate uniform branch)."""
+    from oracle.oracle import oracle
+    from paper_1412_4933_b200 import _lib
+
+    rng = np.random.default_rng(kind + 10)
+    n = 6000
+    mask = rng.integers(0, 256, n).astype(np.uint8)
+    seed = rng.integers(0, 2**63, n, dtype=np.uint64)
+    step = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    ent = rng.integers(1, 2**29, n, dtype=np.uint64) if kind < 2 else rng.integers(0, 2**32, n, dtype=np.uint64)
+    num = None
+    if kind == 1:
+        num = rng.random((n, 8)) * (rng.random((n, 8)) < 0.8)
+        num[rng.random(n) < 0.05] = 0.0
+    got = _lib.selftest_select(kind, mask, seed, step, ent, num=num)
+    lib = oracle()
+    exp = np.array([_oracle_select(lib, kind, mask[i], None if num is None else list(num[i]), seed[i], step[i], ent[i])
+                    for i in range(n)])
+    assert (got == exp).all(), f"{int((got != exp).sum())} of {n} selections differ"
+
+
+def test_aco_selection_frequencies_chi_square():
+    """SPEC acceptance #2 on the device: Eq. 2 frequencies (ACO, F blocked,
+    uniform tau = 0.1, beta = 2: P = num_i / sum, e.g. P(FL) = 0.29221) over
+    200,000 keyed draws, chi-square against the expected probabilities."""
+    from scipy.stats import chisquare
+
+    from paper_1412_4933_b200 import _lib
+
+    d = np.array([1, 2**0.5, 2**0.5, 5**0.5, 5**0.5, 3, 10**0.5, 10**0.5])
+    num = 0.1 * (1.0 / d) ** 2
+    num[0] = 0.0
+    p = num / num.sum()
+    assert abs(p[1] - 0.29221) < 1e-5
+    n = 200_000
+    rng = np.random.default_rng(5)
+    got = _lib.selftest_select(1, np.full(n, 0xFE, np.uint8), 42, rng.integers(0, 2**32, n, dtype=np.uint64),
+                               np.arange(1, n + 1, dtype=np.uint64), num=num)
+    counts = np.bincount(got, minlength=8)
+    assert counts[0] == 0
+    stat = chisquare(counts[1:], p[1:] * n)
+    assert stat.pvalue > 1e-3, stat
+
+
+def test_winner_draw_uniform_among_five_contenders():
+    """SPEC acceptance #3 on the device: a destination with 5 contenders picks
+    each with probability 1/5 (keyed by the global cell index)."""
+    from scipy.stats import chisquare
+
+    from paper_1412_4933_b200 import _lib
+
+    mask = 0b10110101  # contenders at row-major codes 0, 2, 4, 5, 7
+    n = 200_000
+    got = _lib.selftest_select(2, np.full(n, mask, np.uint8), 7, 123, np.arange(n, dtype=np.uint64))
+    assert set(np.unique(got)) == {0, 2, 4, 5, 7}
+    counts = np.bincount(got, minlength=8)[[0, 2, 4, 5, 7]]
+    assert chisquare(counts).pvalue > 1e-3

@@ -186,3 +186,34 @@ def test_oracle_matches_reference_library(kw):
     rr, _ = r.run(150)
     assert (ro == rr).all()
     assert o.hashes() == r.hashes()
+
+
+def test_oracle_aco_selection_chi_square():
+    """SPEC acceptance #2 (CPU, the oracle's aco_select): Eq. 2 frequencies
+    over 100,000 keyed draws match P_i = num_i / sum (chi-square)."""
+    from scipy.stats import chisquare
+
+    lib = oracle()
+    d = (C.c_double * 8)()
+    lib.pfo_distance_table(2.0, d)
+    eta = arr([(1.0 / x) ** 2.0 for x in d])
+    op = arr([0] + [1] * 7, C.c_uint8)
+    num = (C.c_double * 8)()
+    lib.pfo_aco_numerators(op, arr([0.1] * 8), 1.0, eta, num)
+    n = 100_000
+    got = np.array([lib.pfo_aco_select(num, op, 42, s % 977, s + 1) for s in range(n)])
+    counts = np.bincount(got, minlength=8)
+    p = np.array(list(num)) / sum(num)
+    assert counts[0] == 0
+    assert chisquare(counts[1:], p[1:] * n).pvalue > 1e-3
+
+
+def test_oracle_winner_draw_uniform():
+    """SPEC acceptance #3 (CPU): the keyed winner draw min(int(u*k), k-1)
+    (src/engine.cpp:118-120) picks each of 5 contenders with probability 1/5."""
+    from scipy.stats import chisquare
+
+    lib = oracle()
+    k = 5
+    idx = [min(int(lib.pfo_uniform(7, 123, 3, cell, 0) * k), k - 1) for cell in range(100_000)]
+    assert chisquare(np.bincount(idx, minlength=k)).pvalue > 1e-3
