@@ -244,6 +244,18 @@ def secondary_runs(steps):
             "roofline_frac": b / (tot / n / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
         }
         ens.close()
+    # SPEC acceptance #6: ACO <= 1.4x LEM time at 480x480, 20,480
+    # agents, 500 steps (single scenario, and as a 64-seed batch).
+    spec6 = {}
+    for reps in (1, 64):
+        t = {}
+        for model in (p.Model.Lem, p.Model.Aco):
+            cfg = p.ScenarioConfig(width=480, height=480, agents_per_side=10_240, model=model, seed=42)
+            ens = p.Ensemble(cfg, replicas=reps)
+            t[model.name.lower()], _ = ens.time_steps(500)
+            ens.close()
+        spec6[f"x{reps}"] = {"lem_ms": t["lem"], "aco_ms": t["aco"], "aco_over_lem": t["aco"] / t["lem"]}
+    out["spec6_aco_vs_lem_480_20480_500steps"] = spec6
     return out
 
 

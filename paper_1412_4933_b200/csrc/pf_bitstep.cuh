@@ -107,6 +107,7 @@ struct Smem {
     uint32_t A[AROWS][SS];
     uint32_t K[3][AROWS][SS];
     uint32_t G[2][RT][SS];          // grants (vacates) onto owned rows, double-buffered per tile
+    uint32_t rowdraw[2][DROWS];     // intent row has a drawing agent (non-forward intents), per tile parity
     uint32_t dirty[2][RT];          // owned row has an arrival or a vacate
     // Scalar work list (S1 draws, then reused for S2 contested cells): one
     // entry per unit with work, in the order a packed counter handed out
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         sm.qc[0][0] = sm.qc[0][1] = sm.qc[1][0] = sm.qc[1][1] = 0u;
     }
     for (int i = threadIdx.x; i < 2 * RT * SS; i += NT) (&sm.G[0][0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < 2 * DROWS; i += NT) (&sm.rowdraw[0][0])[i] = 0u;
     for (int i = threadIdx.x; i < 2 * RT; i += NT) (&sm.dirty[0][0])[i] = 0u;
     for (int i = threadIdx.x; i < 8 * DROWS; i += NT) {  // the zero end columns of the intent planes
         sm.D[i / DROWS][i % DROWS][0] = 0u;
@@ -510,6 +512,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // Scratch of the NEXT tile (its last readers passed the previous
         // end-of-tile barrier; its first writers come after this tile's).
         for (int i = threadIdx.x; i < RT * SS; i += NT) (&sm.G[cur ^ 1][0][0])[i] = 0u;
+        if (threadIdx.x < DROWS) sm.rowdraw[cur ^ 1][threadIdx.x] = 0u;
         if (threadIdx.x < RT) sm.dirty[cur ^ 1][threadIdx.x] = 0u;
         if (threadIdx.x == 0) sm.qc[cur ^ 1][0] = sm.qc[cur ^ 1][1] = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
@@ -530,7 +533,10 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             d[1] = B & n.em;  // Bottom forward: (-1, 0)
             const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
             const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) enqueue(sm, &sm.qc[cur][0], u, slow);
+            if (slow) {
+                enqueue(sm, &sm.qc[cur][0], u, slow);
+                sm.rowdraw[cur][di] = 1u;
+            }
 #pragma unroll
             for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
         }
@@ -554,6 +560,23 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // Claims, winners and grants for destinations in rows -1 .. RT.
         for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
             const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
+            if (!(sm.rowdraw[cur][ai] | sm.rowdraw[cur][ai + 1] | sm.rowdraw[cur][ai + 2])) {
+                // No agent in the three intent rows around these destinations
+                // drew: the only claims are forward moves, from the row above
+                // (Top, code 1) and the row below (Bottom, code 6).
+                const uint32_t segmask = si == 0 ? 0x80000000u : (si == SS - 1 ? 0x00000001u : 0xFFFFFFFFu);
+                const uint32_t c1 = sm.D[6][ai][si + 1] & segmask, c6 = sm.D[1][ai + 2][si + 1] & segmask;
+                const uint32_t twos = c1 & c6, w1 = c1 & ~twos, w6 = c6 & ~twos;
+                sm.A[ai][si] = c1 | c6;
+                if ((c1 | c6) && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
+                sm.K[0][ai][si] = w1;
+                sm.K[1][ai][si] = w6;
+                sm.K[2][ai][si] = w6;
+                if (w1) grant(sm, cur, ai - 1, si, 1, w1);
+                if (w6) grant(sm, cur, ai - 1, si, 6, w6);
+                if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
+                continue;
+            }
             uint32_t C[8];
             claims(sm, ai, si, C);
             uint32_t ones = 0u, twos = 0u;
