@@ -156,6 +156,12 @@ int pf_halo(pf_ctx* ctx, int32_t replica, int32_t side, int32_t recv, pf_halo_ro
  * (upper owns the rows just above lower) on the same or peer devices. */
 int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower);
 
+/* Page-locked host memory for SimState planes: pf_load_state / pf_store_state
+ * DMA such planes directly (pageable planes go through the library's pinned
+ * staging buffers with a multi-threaded host copy). NULL on failure. */
+void* pf_host_alloc(size_t bytes);
+int pf_host_free(void* p);
+
 /* Fused halo exchange (PF_KERNEL_FUSED only): instead of a separate swap
  * after each step, the step kernel stores this shard's PF_GHOST_ROWS boundary
  * rows (planes, arrivals' words and tours, pheromone) straight into the ghost

@@ -117,6 +117,8 @@ _sigs = {
     "pf_audit": (C.c_int, [_vp, _i32, C.POINTER(_u64)]),
     "pf_selftest_select": (C.c_int, [_i32, _i32, _u32, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp,
                                      _vp]),
+    "pf_host_alloc": (_vp, [C.c_size_t]),
+    "pf_host_free": (C.c_int, [_vp]),
     "pf_peer_export": (C.c_int, [_vp, C.POINTER(PfPeerDesc)]),
     "pf_peer_attach": (C.c_int, [_vp, _i32, C.POINTER(PfPeerDesc), _i32]),
 }
@@ -299,3 +301,49 @@ def selftest_select(kind, mask, seed, step, entity, num=None, d0=2.0, sel_mu=1.0
     check(lib.pf_selftest_select(device, kind, n, d0, sel_mu, sel_sigma, ptr(mask), ptr(nm), ptr(seed), ptr(step),
                                  ptr(entity), ptr(out)))
     return out
+
+
+class PinnedBuffer:
+    """Page-locked host memory from pf_host_alloc, freed with the object."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        self.ptr = lib.pf_host_alloc(self.nbytes)
+        if not self.ptr:
+            raise DeviceError(lib.pf_last_error().decode(errors="replace"))
+
+    def array(self, shape, dtype) -> np.ndarray:
+        """A numpy view of the buffer (keeps the buffer alive)."""
+        dtype = np.dtype(dtype)
+        count = int(np.prod(shape)) if len(shape) else 1
+        assert count * dtype.itemsize <= self.nbytes
+        raw = (C.c_char * max(1, count * dtype.itemsize)).from_address(self.ptr)
+        a = np.frombuffer(raw, dtype=dtype, count=count).reshape(shape)
+        a.setflags(write=True)
+        return _PinnedView(a, self)
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.pf_host_free(self.ptr)
+            self.ptr = None
+
+
+class _PinnedView(np.ndarray):
+    """ndarray subclass holding a reference to its PinnedBuffer."""
+
+    def __new__(cls, a, owner):
+        obj = a.view(cls)
+        obj._owner = owner
+        return obj
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+
+def pinned_array(shape, dtype) -> np.ndarray:
+    """A zeroed numpy array in page-locked memory (pf_host_alloc)."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape)) if len(shape) else 1
+    a = PinnedBuffer(count * dtype.itemsize).array(shape, dtype)
+    a[...] = 0
+    return a

@@ -69,8 +69,19 @@ class Stager {
         }
     }
 
+    // Page-locked caller memory (pf_host_alloc, cudaHostAlloc/Register) is
+    // DMA'd directly; pageable memory goes through the staging buffers.
+    static bool pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+
     cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
-        if (n < kDirect) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s);
+        if (n < kDirect || pinned(src)) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s);
         if (cudaError_t e = ready()) return e;
         const size_t nch = (n + kChunk - 1) / kChunk;
         for (size_t i = 0; i < nch; ++i) {
@@ -86,7 +97,7 @@ class Stager {
     }
 
     cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
-        if (n < kDirect) {
+        if (n < kDirect || pinned(dst)) {
             cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s);
             return e ? e : cudaStreamSynchronize(s);
         }
@@ -1069,6 +1080,21 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
         }
     }
     PF_CUDA(cudaStreamSynchronize(lower->stream));
+    return PF_OK;
+}
+
+void* pf_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        g_err = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+
+int pf_host_free(void* p) {
+    if (p) PF_CUDA(cudaFreeHost(p));
     return PF_OK;
 }
 

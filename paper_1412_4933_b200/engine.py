@@ -134,16 +134,19 @@ class SimState:
     If you modify planes in place, call touch() so the next step re-uploads.
     """
 
-    def __init__(self, width: int, height: int, model: Model, n_agents: int):
+    def __init__(self, width: int, height: int, model: Model, n_agents: int, pinned: bool = False):
         self.width = int(width)
         self.height = int(height)
         self.model = Model(model)
-        self._occ = np.zeros((height, width), np.uint8)
-        self._index = np.zeros((height, width), np.uint32)
-        self._agents = np.zeros(n_agents, AGENT_DTYPE)
+        # pinned: planes in page-locked memory (pf_host_alloc), which state
+        # upload / download DMA directly instead of staging.
+        zeros = _lib.pinned_array if pinned else np.zeros
+        self._occ = zeros((height, width), np.uint8)
+        self._index = zeros((height, width), np.uint32)
+        self._agents = zeros((n_agents,), AGENT_DTYPE)
         aco = self.model == Model.Aco
-        self._tau_top = np.zeros((height, width), np.float64) if aco else None
-        self._tau_bot = np.zeros((height, width), np.float64) if aco else None
+        self._tau_top = zeros((height, width), np.float64) if aco else None
+        self._tau_bot = zeros((height, width), np.float64) if aco else None
         self._step = 0
         self._device = None  # (engine, replica) holding a newer copy
         self._version = 0    # bumped on host-side modification
@@ -210,10 +213,11 @@ class SimState:
         return r * self.width + c
 
 
-def new_environment(cfg: ScenarioConfig, seed: int) -> SimState:
-    """new_environment (src/state.cpp:54-75), computed by the library's host C++."""
+def new_environment(cfg: ScenarioConfig, seed: int, pinned: bool = False) -> SimState:
+    """new_environment (src/state.cpp:54-75), computed by the library's host C++.
+    pinned=True puts the planes in page-locked memory (faster state transfers)."""
     validate(cfg)
-    s = SimState(cfg.width, cfg.height, cfg.model, 2 * cfg.agents_per_side)
+    s = SimState(cfg.width, cfg.height, cfg.model, 2 * cfg.agents_per_side, pinned=pinned)
     c = _pf_config(cfg, seed)
     _lib.check(_lib.lib.pf_new_environment(c, int(seed) & (2**64 - 1), s._occ.ctypes.data, s._index.ctypes.data,
                                            s._agents.ctypes.data if len(s._agents) else None,

@@ -129,6 +129,23 @@ def test_store_load_roundtrip():
     assert s.step == snap.step == 35
 
 
+def test_pinned_host_planes_match_pageable():
+    """SimState planes in page-locked memory (pf_host_alloc: direct DMA, no
+    staging) give the same trajectory as pageable planes, on a grid large
+    enough (> 4 MB planes) to take the staged path when pageable."""
+    import paper_1412_4933_b200 as p
+
+    cfg = to_config(dict(width=1024, height=1024, agents_per_side=60000, model="aco", seed=9))
+    a = p.new_environment(cfg, 9)
+    b = p.new_environment(cfg, 9, pinned=True)
+    assert hashes_of(a) == hashes_of(b)
+    for s in (a, b):
+        eng = p.StepEngine(p.EngineOptions.from_config(cfg, 9))
+        eng.run(s, 30)
+    assert hashes_of(a) == hashes_of(b)
+    assert a.step == b.step == 30
+
+
 def test_corrupt_state_rejected():
     import paper_1412_4933_b200 as p
 
