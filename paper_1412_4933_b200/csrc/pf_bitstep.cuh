@@ -352,13 +352,48 @@ __device__ __forceinline__ void set_winner(Smem& sm, int cur, int ai, int si, in
 // replica.
 struct Item {
     int rep, strip, chunk, c0, t_first, t_end;
+    int sides;  // bit 0 / 1: the item reads the upper / lower ghost rows (and writes the rows they mirror)
 };
 
-__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item) {
+// Ghost-row sides of a chunk: its first tile's window starts above row 0, or
+// its last tile's window (RT rows + 3) reaches past the last owned row. With
+// a short last tile that can be the last TWO chunks' business.
+__device__ __forceinline__ int chunk_sides(int chunk, int tiles_per_item, int n_tiles, int rows_owned) {
+    const int t0 = chunk * tiles_per_item, t1 = min(t0 + tiles_per_item, n_tiles);
+    return (t0 == 0 ? 1 : 0) | (t1 * RT + kGhost > rows_owned ? 2 : 0);
+}
+// Items per replica-strip with side s (the count signal_boundary waits for).
+__device__ __forceinline__ int side_chunks(int s, int n_chunks, int tiles_per_item, int n_tiles, int rows_owned) {
+    int n = 0;
+    for (int c = n_chunks - 1; c >= 0 && c >= n_chunks - 2; --c) n += chunk_sides(c, tiles_per_item, n_tiles, rows_owned) >> 1 & 1;
+    return s == 0 ? 1 : n;
+}
+
+// Linked shards (bfirst) number the boundary chunks of every (replica, strip)
+// first, so they are claimed early in the step: the neighbours' next steps
+// wait only for those (see wait_boundary / signal_boundary).
+__device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
+                                            int reps, bool bfirst, int rows_owned) {
     Item it;
-    it.rep = item / (strips * n_chunks);
-    it.strip = (item / n_chunks) % strips;
-    it.chunk = item % n_chunks;
+    if (bfirst) {
+        const int nb = n_chunks >= 2 ? 2 : 1, nbi = reps * strips * nb;
+        if (item < nbi) {
+            it.rep = item / (strips * nb);
+            const int r = item % (strips * nb);
+            it.strip = r / nb;
+            it.chunk = (r % nb) ? n_chunks - 1 : 0;
+        } else {
+            const int ni = n_chunks - nb, j = item - nbi;
+            it.rep = j / (strips * ni);
+            it.strip = (j / ni) % strips;
+            it.chunk = 1 + j % ni;
+        }
+    } else {
+        it.rep = item / (strips * n_chunks);
+        it.strip = (item / n_chunks) % strips;
+        it.chunk = item % n_chunks;
+    }
+    it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
     it.c0 = it.strip * (NS * 32);
     it.t_first = it.chunk * tiles_per_item;
     it.t_end = min(it.t_first + tiles_per_item, n_tiles);
@@ -384,6 +419,49 @@ __device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parit
         sm.pl[slot(base, first_sr + i / SP)][i % SP] = make_uint2(kWall, kWall);
 }
 
+// Fused halo exchange, ordering (linked shards only). A boundary item of step
+// t reads this shard's ghost rows (written by the neighbour's step t-1
+// boundary items) and writes the neighbour's ghost rows of the other parity
+// (read by the neighbour's step t-1 boundary items). Both hazards are covered
+// by waiting, before the item's rows are loaded, until the neighbour has
+// completed its step t-1 boundary items: sync_local[side] >= t. Interior
+// items never wait, so neighbouring shards overlap everything but their
+// boundary strips. Called by one lane; a 30 s timeout sets *err.
+__device__ __forceinline__ void wait_boundary(const StepArgs& a, int sides, uint32_t step) {
+    uint64_t t0 = 0;
+    for (int s = 0; s < 2; ++s) {
+        if (!(sides >> s & 1) || !a.peer[s].cell) continue;
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.sync_local + s) : "memory");
+            if (int32_t(v - step) >= 0) break;
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (!t0) t0 = now;
+            if (now - t0 > 30000000000ull) {  // the neighbour is gone
+                atomicOr(a.err, 1u);
+                return;
+            }
+            __nanosleep(200);
+        }
+    }
+}
+
+// After a boundary item (its mirror stores fenced, then a CTA barrier):
+// count it; the CTA completing the last boundary item of a side releases
+// step + 1 into that neighbour's flag. Called by one thread.
+__device__ __forceinline__ void signal_boundary(const StepArgs& a, int sides, uint32_t step, int strips, int n_chunks,
+                                                int n_tiles) {
+    for (int s = 0; s < 2; ++s) {
+        if (!(sides >> s & 1) || !a.peer[s].cell) continue;
+        const uint32_t done = atomicAdd(a.bcount + size_t(step % uint32_t(a.report_cap)) * 2 + s, 1u) + 1u;
+        if (done == uint32_t(strips * a.replicas * side_chunks(s, n_chunks, a.tiles_per_cta, n_tiles, a.rows_owned))) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.sync_remote[s]), "r"(step + 1u) : "memory");
+        }
+    }
+}
+
 // Fused halo exchange (linked shards only): after a tile's commit, its rows
 // that are ghost rows of a neighbour shard (this shard's first / last kGhost
 // owned rows) are copied from where the commit just wrote them (L2) into the
@@ -391,7 +469,7 @@ __device__ __forceinline__ void load_rows(Smem& sm, const StepArgs& a, int parit
 // words and tours in place (a stale word under an empty plane bit is as
 // harmless there as here). Called by the whole CTA after the end-of-tile
 // barrier; the system fence orders the stores before the step's completion
-// flag (launch_halo_signal).
+// flag (signal_boundary).
 template <bool ACO>
 __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int rep, int strip, int r0) {
     const int W = a.k.W;
@@ -462,7 +540,9 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         item = __shfl_sync(0xFFFFFFFFu, item, 0);
         if (lane == 0) sm.item[1] = item;
         if (item < n_items) {
-            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
+            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+            if (MIRROR && first.sides && lane == 0) wait_boundary(a, first.sides, step);
+            __syncwarp();
             load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
         }
     }
@@ -475,7 +555,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     int cur = 0;                                // tile parity: G / dirty / work-list counters
     uint32_t* const cells = a.p.cell[0];
     while (item < n_items) {
-    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
+    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
     const int rep = it.rep, c0 = it.c0;
     const uint64_t seed = __ldg(&a.rep[rep].seed);
     const int band = __ldg(&a.rep[rep].band);
@@ -504,7 +584,9 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item[ipar] = nx;
                 if (kCrossPrefetch && nx < n_items) {
-                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta);
+                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+                    if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
+                    __syncwarp();
                     load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
                 }
             }
@@ -727,6 +809,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (sm.cnt[1]) atomicAdd(&rep_slot[2], sm.cnt[1]);
         if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
+        if (MIRROR && it.sides) signal_boundary(a, it.sides, step, strips, n_chunks, n_tiles);  // after the barrier: all mirror stores fenced
     }
     item = sm.item[ipar];  // claimed during the last tile (visible after its barriers)
     ipar ^= 1;
@@ -734,7 +817,9 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // Small ring: the next item's window is loaded only now, into the
         // slots the finished item released.
         if (warp == 0) {
-            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta);
+            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+            if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
+            __syncwarp();
             load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
         }
         __syncthreads();  // wall rows written by warp 0 are visible to all

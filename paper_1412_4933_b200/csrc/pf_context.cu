@@ -371,7 +371,10 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->d_step = static_cast<uint32_t*>(alloc(4));
     ctx->d_sync = static_cast<uint32_t*>(alloc(8));
     ctx->d_err = static_cast<uint32_t*>(alloc(4));
-    ok = ok && ctx->d_sync && ctx->d_err;
+    ctx->args.bcount = static_cast<uint32_t*>(alloc(size_t(kReportCap) * 8));
+    ok = ok && ctx->d_sync && ctx->d_err && ctx->args.bcount;
+    ctx->args.sync_local = ctx->d_sync;
+    ctx->args.err = ctx->d_err;
     auto* kc = static_cast<pfdev::StepConsts*>(alloc(sizeof(pfdev::StepConsts)));
     ok = ok && kc && cudaMemcpy(kc, &ctx->args.k, sizeof(pfdev::StepConsts), cudaMemcpyHostToDevice) == cudaSuccess;
     ctx->args.kc = kc;
@@ -841,22 +844,20 @@ static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
         PF_CUDA(cudaMemset2DAsync(reinterpret_cast<char*>(ctx->d_reports) + size_t(slot) * 16, pitch, 0,
                                   size_t(m) * 16, size_t(ctx->cfg.replicas), ctx->stream));
         PF_CUDA(cudaMemsetAsync(ctx->args.work + slot, 0, size_t(m) * 4, ctx->stream));  // work-item counters
+        PF_CUDA(cudaMemsetAsync(ctx->args.bcount + size_t(slot) * 2, 0, size_t(m) * 8, ctx->stream));  // boundary items
         done += m;
     }
     return PF_OK;
 }
 
 static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
-    if (ctx->linked)  // fused halo: the neighbours have completed the previous step
-        ctx->launches += pfk::launch_halo_wait(ctx->d_step, int(i), ctx->d_sync, ctx->linked, ctx->d_err, ctx->stream);
+    // Linked shards: the step kernel itself orders its boundary items against
+    // the neighbours' (wait_boundary / signal_boundary in pf_bitstep.cuh).
     switch (ctx->cfg.kernel) {
         case PF_KERNEL_FUSED: ctx->launches += pfk::launch_step_bits(ctx->args, int(i), parity, ctx->stream); break;
         case PF_KERNEL_TILE: ctx->launches += pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream); break;
         default: ctx->launches += pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream); break;
     }
-    if (ctx->linked)
-        ctx->launches += pfk::launch_halo_signal(ctx->d_step, int(i), ctx->remote_flag[0], ctx->remote_flag[1],
-                                                 ctx->stream);
     return PF_OK;
 }
 
@@ -894,7 +895,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
         it = ctx->graphs.emplace(key, ge).first;
     }
     PF_CUDA(cudaGraphLaunch(it->second, ctx->stream));
-    const uint32_t per_step = (ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1) + (ctx->linked ? 2 : 0);
+    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1;
     ctx->launches += uint64_t(n) * per_step + 1;
     ctx->parity ^= int(n & 1u);
     ctx->step += n;
@@ -1175,6 +1176,7 @@ int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc
     // r - (rows_owned - G).
     pr.row_delta = side == 0 ? d->rows_owned : -ctx->rows_owned;
     ctx->remote_flag[side] = static_cast<uint32_t*>(p[6]) + (1 - side);
+    ctx->args.sync_remote[side] = ctx->remote_flag[side];
     const uint32_t now = ctx->step;  // the neighbour has completed `step` steps
     PF_CUDA(cudaMemcpy(ctx->d_sync + side, &now, 4, cudaMemcpyHostToDevice));
     ctx->linked |= 1 << side;

@@ -64,6 +64,14 @@ struct StepArgs {
     int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
     PeerRows peer[2];       // [0] the shard above (toward row 0), [1] below; cell == nullptr: none
     int strip_segs;         // bit kernel: 32-column segments per strip (bits_strip_segments)
+    // Fused halo ordering (linked shards): sync_local[side] = steps whose
+    // boundary items the neighbour on that side has completed (written by it);
+    // sync_remote[side] = our flag in the neighbour's memory; bcount = per-step
+    // [report_cap][2] completed boundary items per side; err = wait timeout.
+    uint32_t* sync_local;
+    uint32_t* sync_remote[2];
+    uint32_t* bcount;
+    uint32_t* err;
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
@@ -83,13 +91,6 @@ int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s); 
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
 // *d_step += n
 int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
-// Fused halo handshake of step (*d_step + slot): wait until each linked
-// neighbour has completed that many steps (flags[side] >= step; spins with a
-// timeout that sets *err), and after the step tell the neighbours
-// (remote[side] = step + 1, system-scope release).
-int launch_halo_wait(const uint32_t* d_step, int slot, const volatile uint32_t* flags, int sides, uint32_t* err,
-                     cudaStream_t s);
-int launch_halo_signal(const uint32_t* d_step, int slot, uint32_t* remote0, uint32_t* remote1, cudaStream_t s);
 // Fill a tau plane range with {v, v}.
 int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);

@@ -327,51 +327,6 @@ int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s) {
     return 1;
 }
 
-// --- fused halo handshake (one thread each) ----------------------------------
-
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-__global__ void halo_wait_kernel(const uint32_t* d_step, int slot, const volatile uint32_t* flags, int sides,
-                                 uint32_t* err) {
-    const uint32_t t = *d_step + uint32_t(slot);
-    const uint64_t t0 = globaltimer_ns();
-    for (int s = 0; s < 2; ++s) {
-        if (!(sides >> s & 1)) continue;
-        for (;;) {
-            uint32_t v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + s) : "memory");
-            if (int32_t(v - t) >= 0) break;
-            if (globaltimer_ns() - t0 > 30000000000ull) {  // 30 s: the neighbour is gone
-                atomicOr(err, 1u);
-                return;
-            }
-            __nanosleep(100);
-        }
-    }
-}
-
-__global__ void halo_signal_kernel(const uint32_t* d_step, int slot, uint32_t* r0, uint32_t* r1) {
-    const uint32_t v = *d_step + uint32_t(slot) + 1u;
-    __threadfence_system();  // the step kernel's ghost-row stores are ordered before the flag
-    if (r0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(r0), "r"(v) : "memory");
-    if (r1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(r1), "r"(v) : "memory");
-}
-
-int launch_halo_wait(const uint32_t* d_step, int slot, const volatile uint32_t* flags, int sides, uint32_t* err,
-                     cudaStream_t s) {
-    halo_wait_kernel<<<1, 1, 0, s>>>(d_step, slot, flags, sides, err);
-    return 1;
-}
-
-int launch_halo_signal(const uint32_t* d_step, int slot, uint32_t* remote0, uint32_t* remote1, cudaStream_t s) {
-    halo_signal_kernel<<<1, 1, 0, s>>>(d_step, slot, remote0, remote1);
-    return 1;
-}
-
 __global__ void fill_tau_kernel(double2* p, size_t n, double v) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         p[i] = make_double2(v, v);
