@@ -166,12 +166,13 @@ int pf_host_free(void* p);
  * after each step, the step kernel stores this shard's PF_GHOST_ROWS boundary
  * rows (planes, arrivals' words and tours, pheromone) straight into the ghost
  * rows of the neighbour shards, through peer memory (NVLink P2P; CUDA IPC
- * between processes). Each step is then bracketed on the device by a flag
- * handshake: wait until the neighbours have completed the previous step
- * (their stores into our ghost rows are done and they no longer read the
- * ghost buffers we are about to write), step, then release our completion
- * count into the neighbours' flags. No host work or collective per step, so
- * sharded steps batch into CUDA graphs like single-GPU ones. */
+ * between processes). Ordering is per boundary work item inside the kernel:
+ * an item touching the ghost rows waits until the neighbour has completed its
+ * previous step's boundary items (its stores into our ghost rows are done and
+ * it no longer reads the ghost buffers we are about to write), and the last
+ * boundary item of a side releases our count into that neighbour's flag.
+ * Interior work never waits. No host work or collective per step, so sharded
+ * steps batch into CUDA graphs like single-GPU ones. */
 typedef struct pf_peer_desc {
     unsigned char ipc[7][64]; /* cudaIpcMemHandle_t of: cell, occ[0], occ[1], tau[0], tau[1], tour, sync flags */
     uint64_t ptr[7];          /* the same allocations as device pointers of the exporting process */
