@@ -446,6 +446,7 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
         rep = c.read_reports(min(args.steps, 1024))
     c.store(0, state._occ, state._index, state._agents, state._tau_top, state._tau_bot)
     secs = max_over_ranks(time.perf_counter() - t0)
+    barrier()  # fused exchange: no rank frees its planes while a neighbour may still store into them
     c.close()
     del rep
     return {"value": 2 * cfg.agents_per_side * args.steps / secs, "unit": "agent-updates/s",

@@ -132,6 +132,7 @@ class ShardedEngine:
         validate(cfg)
         self.cfg = cfg
         self.rank, self.world = rank, world
+        self.group = group
         self.device = rank if device is None else device
         self.lo, self.hi = row_partition(cfg.height, world)[rank]
         whole = world == 1
@@ -216,4 +217,12 @@ class ShardedEngine:
         return self.ctx.store(replica, occ, index, agents, tau_top, tau_bot)
 
     def close(self):
+        """Free the shard. With the fused exchange a neighbour may still be
+        storing into this shard's ghost rows during its last step, so every
+        rank finishes its steps (synchronize + barrier) before any frees."""
+        if self.exchange == "p2p" and self.world > 1 and getattr(self.ctx, "h", None):
+            import torch.distributed as dist
+
+            self.ctx.synchronize()
+            dist.barrier(group=self.group)
         self.ctx.close()
