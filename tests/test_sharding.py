@@ -251,6 +251,53 @@ def test_gpu_fused_halo_one_device(model, nshards):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_gpu_fused_halo_minimum_shards(model):
+    """Shards of the minimum height (3 rows: every row is a ghost row of both
+    neighbours, every work item touches both sides): 16 rows over 5 linked
+    shards (3/3/3/3/4), 200 steps, equal to the unsharded run."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
+
+    cfg = p.ScenarioConfig(width=96, height=16, agents_per_side=300, model=p.Model.Lem if model == "lem" else p.Model.Aco,
+                           seed=4)
+    steps = 200
+    whole = p.Ensemble(cfg, replicas=3, seed=4)
+    whole_rep = whole.run(steps)
+    parts = row_partition(cfg.height, 5)
+    assert [hi - lo for lo, hi in parts] == [3, 3, 3, 3, 4]
+    shards = []
+    for lo, hi in parts:
+        c = _lib.Context(_pf_config(cfg, 4, replicas=3, row_begin=lo, row_end=hi))
+        c.init_environment()
+        shards.append(c)
+    _lib.link_shards(shards)
+    for c in shards:
+        c.step_async(steps)
+    for c in shards:
+        c.synchronize()
+    tot = sum(c.read_reports(steps)["moved"].astype(np.int64) for c in shards)
+    assert (tot == whole_rep["moved"]).all()
+    for r in range(3):
+        ref = whole.state(r)
+        H, W = cfg.height, cfg.width
+        idx = np.zeros((H, W), np.uint32)
+        occ = np.zeros((H, W), np.uint8)
+        ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+        tt = np.zeros((H, W)) if model == "aco" else None
+        tb = np.zeros((H, W)) if model == "aco" else None
+        for c in shards:
+            c.store(r, occ, idx, ag, tt, tb)
+        assert (idx == ref.index).all() and (occ == ref.occupancy).all()
+        if tt is not None:
+            assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
+    for c in shards:
+        c.close()
+
+
+@pytest.mark.gpu
 def test_gpu_fused_halo_rejects_mismatched_peers():
     import paper_1412_4933_b200 as p
     from paper_1412_4933_b200 import _lib
