@@ -127,6 +127,7 @@ struct Smem {
     // with one-tile items the next claim can come before the slowest warp
     // has read the previous one (no barrier in between).
     int item[2];
+    int idec[2][4];   // the same items decoded (rep, strip, chunk, sides) by warp 0: no divisions per thread
     uint32_t cnt[3];
     double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
 };
@@ -400,6 +401,25 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
     return it;
 }
 
+// An item decoded by warp 0 (Smem::idec) for the rest of the CTA.
+__device__ __forceinline__ void publish_item(int (&d)[4], const Item& it) {
+    d[0] = it.rep;
+    d[1] = it.strip;
+    d[2] = it.chunk;
+    d[3] = it.sides;
+}
+__device__ __forceinline__ Item read_item(const int (&d)[4], int n_tiles, int tiles_per_item) {
+    Item it;
+    it.rep = d[0];
+    it.strip = d[1];
+    it.chunk = d[2];
+    it.sides = d[3];
+    it.c0 = it.strip * (NS * 32);
+    it.t_first = it.chunk * tiles_per_item;
+    it.t_end = min(it.t_first + tiles_per_item, n_tiles);
+    return it;
+}
+
 // Issue the TMA loads of `nrows` staged plane rows (tile rows first_sr..,
 // relative to the tile at r0) of item `it` into their ring slots, completing
 // on mbarrier m; rows past the end of the buffer are written as walls. Each
@@ -541,6 +561,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (lane == 0) sm.item[1] = item;
         if (item < n_items) {
             const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+            if (lane == 0) publish_item(sm.idec[1], first);
             if (MIRROR && first.sides && lane == 0) wait_boundary(a, first.sides, step);
             __syncwarp();
             load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
@@ -548,6 +569,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     }
     __syncthreads();  // item id and wall rows written by warp 0 are visible to all
     item = sm.item[1];
+    int islot = 1;    // sm.idec slot of the current item
     int ipar = 0;     // the current item's last tile claims the next one into sm.item[ipar]
     uint32_t moved = 0, ntop = 0, nbot = 0;
     uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
@@ -555,7 +577,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     int cur = 0;                                // tile parity: G / dirty / work-list counters
     uint32_t* const cells = a.p.cell[0];
     while (item < n_items) {
-    const Item it = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+    const Item it = read_item(sm.idec[islot], n_tiles, a.tiles_per_cta);
     const int rep = it.rep, c0 = it.c0;
     const uint64_t seed = __ldg(&a.rep[rep].seed);
     const int band = __ldg(&a.rep[rep].band);
@@ -583,11 +605,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 if (lane == 0) nx = int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item[ipar] = nx;
-                if (kCrossPrefetch && nx < n_items) {
+                if (nx < n_items) {
                     const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
-                    if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
-                    __syncwarp();
-                    load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
+                    if (lane == 0) publish_item(sm.idec[ipar], nit);
+                    if (kCrossPrefetch) {
+                        if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
+                        __syncwarp();
+                        load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
+                    }
                 }
             }
         }
@@ -812,12 +837,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (MIRROR && it.sides) signal_boundary(a, it.sides, step, strips, n_chunks, n_tiles);  // after the barrier: all mirror stores fenced
     }
     item = sm.item[ipar];  // claimed during the last tile (visible after its barriers)
+    islot = ipar;
     ipar ^= 1;
     if (!kCrossPrefetch && item < n_items) {
         // Small ring: the next item's window is loaded only now, into the
         // slots the finished item released.
         if (warp == 0) {
-            const Item nit = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+            const Item nit = read_item(sm.idec[islot], n_tiles, a.tiles_per_cta);
             if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
             __syncwarp();
             load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
