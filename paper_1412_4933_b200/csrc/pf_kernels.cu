@@ -1,18 +1,20 @@
-// sm_100a kernels of the per-step grid update.
+// sm_100a kernels besides the product step kernel (pf_bitstep.cuh):
 //
-//   step_fused_kernel   ONE kernel per step (the product path). A CTA owns a
-//                       TH x TW tile; it stages the step-start cell words of
-//                       the tile plus a 3-cell halo in shared memory, proposes
-//                       moves for every agent within 2 cells of the tile,
-//                       scatters claims into per-destination bitmasks
-//                       (shared-memory atomicOr), resolves every destination
-//                       within 1 cell (keyed draw per contested cell), then
-//                       commits the owned cells: cell word, tour, pheromone
-//                       evaporation + deposit, crossing and counters. HBM
-//                       traffic is one read + one write of each plane.
-//   step_pipeline_*     the same semantics as three kernels (propose /
-//                       resolve / commit) through global u8 scratch planes;
-//                       kept as an independent on-device cross-check.
+//   step_fused_kernel   PF_KERNEL_TILE cross-check: ONE kernel per step on
+//                       ping-pong cell words. A CTA owns a TH x TW tile; it
+//                       stages the step-start cell words of the tile plus a
+//                       3-cell halo in shared memory, proposes moves for every
+//                       agent within 2 cells of the tile, scatters claims into
+//                       per-destination bitmasks (shared-memory atomicOr),
+//                       resolves every destination within 1 cell (keyed draw
+//                       per contested cell), then commits the owned cells.
+//   step_pipeline_*     PF_KERNEL_PIPELINE cross-check: the same semantics as
+//                       three kernels (propose / resolve / commit) through
+//                       global u8 scratch planes.
+//   state kernels       SimState import / export / audit, occupancy-plane
+//                       build and word sanitising for the product kernel,
+//                       pheromone (de)interleave, tour gather.
+//   self-tests          the device RNG and selection functions, per key.
 //
 // Reference semantics: StepEngine::step, src/engine.cpp:53-193.
 #include "pf_internal.h"
