@@ -27,7 +27,8 @@
 // run of consecutive RT-row tiles. The step-start planes of the strip live in
 // a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
 // rows); while a tile is processed, TMA bulk copies (cp.async.bulk + mbarrier,
-// one 96-byte row each) bring the next tile's RT new rows.
+// one (NS + 4) * 8-byte row each) bring the next tile's RT new rows. Warp 0
+// claims work items from a per-step counter and publishes them decoded.
 //
 //   S1 intent  thread per segment-row: forward moves (F open, no draw,
 //              src/lem.cpp:23-26, src/aco.cpp:60-63) and boxed-in agents in
@@ -44,6 +45,12 @@
 //              counters, tour), the new occupancy planes (vacates cleared,
 //              arrivals set by group ballots), ACO evaporation + deposit over
 //              every cell (src/engine.cpp:124-175).
+//
+// Linked row shards (MIRROR): boundary items are claimed first, wait for the
+// neighbour's previous-step boundary items, copy their edge rows into the
+// neighbour's ghost rows (peer memory) and count themselves toward the flag
+// that releases the neighbour's next step (wait_boundary / mirror_tile /
+// signal_boundary below).
 //
 // This file is the kernel template: it is compiled once per strip width
 // (pf_bitstep_ns8.cu: 8 segments = 256 columns, pf_bitstep_ns10.cu: 320
