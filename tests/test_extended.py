@@ -80,6 +80,29 @@ def test_strip_widths_vs_oracle(kw):
 
 
 @pytest.mark.gpu
+def test_subnormal_pheromone_regime_vs_oracle():
+    """16,000 ACO steps: the pheromone fields decay into the subnormal range
+    (most cells end below 2.2e-308, the smallest at 4e-323). fp64 on the GPU
+    keeps subnormals (no FTZ), so the fields and the trajectories stay
+    bit-identical to the oracle's (glibc, no FTZ/DAZ)."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    kw = dict(width=96, height=96, agents_per_side=256, model="aco", seed=5)
+    steps = 16_000
+    ora = OracleState(to_scenario(kw))
+    orep = ora.run(steps)
+    tau = np.asarray(ora.tau_top)
+    assert ((tau > 0) & (tau < 2.2250738585072014e-308)).sum() > 4000  # the regime is reached
+    cfg = to_config(kw)
+    state = p.new_environment(cfg, kw["seed"])
+    eng = p.StepEngine(p.EngineOptions.from_config(cfg, kw["seed"]))
+    rep = eng.run_array(state, steps)
+    assert (rep == orep).all(), "per-step reports differ"
+    assert first_divergence(state, ora) == "identical"
+
+
+@pytest.mark.gpu
 def test_alpha_fractional_matches_oracle():
     """alpha not in {0,1} uses pow (tolerance-only by contract); in practice the
     trajectories and fields still agree for this scenario."""
