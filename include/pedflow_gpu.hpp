@@ -71,6 +71,7 @@ struct SimState {
     std::vector<uint32_t> index;
     std::vector<AgentRecord> agents;
     std::vector<double> pheromone_top, pheromone_bottom;
+    std::vector<double> scores;  // CandidateScores::score by agent id, [n][8] (filled by the phase methods)
     uint32_t step = 0;
 };
 
@@ -125,10 +126,34 @@ class StepEngine {
                              s.pheromone_bottom.empty() ? nullptr : s.pheromone_bottom.data(), &s.step));
     }
 
+    // Phase-level stepping (StepEngine::score_phase .. reset_phase,
+    // src/engine.cpp:64-193); needs Options::kernel = PF_KERNEL_PIPELINE.
+    // score_phase uploads `s`; the later phases of the same step continue on
+    // the device (do not modify `s` in between); each downloads the result,
+    // so s.agents' futures and s.scores read as the reference's do.
+    void score_phase(SimState& s) {
+        upload(s);
+        phase(s, PF_PHASE_SCORE, nullptr);
+    }
+    void intention_phase(SimState& s) { phase(s, PF_PHASE_INTENTION, nullptr); }
+    StepReport movement_phase(SimState& s) {
+        StepReport r{};
+        phase(s, PF_PHASE_MOVEMENT, &r);
+        return r;
+    }
+    void reset_phase(SimState& s) { phase(s, PF_PHASE_RESET, nullptr); }
+
     const Options& options() const { return opt_; }
     pf_ctx* handle() { return ctx_; }
 
   private:
+    void phase(SimState& s, int32_t ph, StepReport* r) {
+        check(pf_phase(ctx_, ph, r));
+        download(s);
+        s.scores.resize(s.agents.size() * 8);
+        check(pf_store_scores(ctx_, 0, s.scores.data(), nullptr, uint32_t(s.agents.size())));
+    }
+
     Options opt_;
     pf_ctx* ctx_ = nullptr;
 };

@@ -128,6 +128,22 @@ int pf_store_state(pf_ctx* ctx, int32_t replica, uint8_t* occ, uint32_t* index, 
  * [replicas][n] reports. Synchronous. */
 int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out);
 
+/* Phase-level stepping, replaces: StepEngine::score_phase / intention_phase /
+ * movement_phase / reset_phase (inc/engine.hpp:55-58, src/engine.cpp:64-193).
+ * PF_KERNEL_PIPELINE contexts only (the fused kernels run all four phases in
+ * one launch). Phases run in order; a full step is SCORE, INTENTION,
+ * MOVEMENT, RESET, bit-identical to pf_step. MOVEMENT writes [replicas]
+ * reports to out (may be NULL). Between INTENTION and RESET pf_store_state
+ * exports the agents' future_row / future_col as the reference has them;
+ * pf_store_scores gives the CandidateScores after SCORE (zeros after RESET). */
+#define PF_PHASE_SCORE 0
+#define PF_PHASE_INTENTION 1
+#define PF_PHASE_MOVEMENT 2
+#define PF_PHASE_RESET 3
+int pf_phase(pf_ctx* ctx, int32_t phase, pf_step_report* out);
+/* CandidateScores (lem.hpp:14-17) of one replica by agent id: scores[(id-1)*8 + slot]
+ * in goal-relative slot order, owners[id-1] (always the id); either may be NULL. */
+int pf_store_scores(pf_ctx* ctx, int32_t replica, double* scores, uint32_t* owners, uint32_t n_agents);
 /* Asynchronous variant: enqueue n steps on the context's stream. Reports stay
  * on the device in a ring of the last 1024 steps; pf_read_reports
  * (synchronizes) returns those of steps [step - n, step) as [replicas][n]. */

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("PEDFLOW_B200_LIB") or os.path.join(HERE, "libpedflow_
 PF_OK, PF_ERR_CONFIG, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, 2, 3, 4, 5, 6
 PF_MODEL_LEM, PF_MODEL_ACO = 0, 1
 PF_KERNEL_FUSED, PF_KERNEL_PIPELINE, PF_KERNEL_TILE = 0, 1, 2
+PF_PHASE_SCORE, PF_PHASE_INTENTION, PF_PHASE_MOVEMENT, PF_PHASE_RESET = 0, 1, 2, 3
 PF_GHOST_ROWS = 3
 
 # pedflow::AgentRecord (inc/grid.hpp:84-93) == pf_agent, 40 bytes.
@@ -117,6 +118,8 @@ _sigs = {
     "pf_audit": (C.c_int, [_vp, _i32, C.POINTER(_u64)]),
     "pf_selftest_select": (C.c_int, [_i32, _i32, _u32, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp,
                                      _vp]),
+    "pf_phase": (C.c_int, [_vp, _i32, _vp]),
+    "pf_store_scores": (C.c_int, [_vp, _i32, _vp, _vp, _u32]),
     "pf_host_alloc": (_vp, [C.c_size_t]),
     "pf_host_free": (C.c_int, [_vp]),
     "pf_peer_export": (C.c_int, [_vp, C.POINTER(PfPeerDesc)]),
@@ -239,6 +242,18 @@ class Context:
         n = C.c_uint64(0)
         check(lib.pf_audit(self.h, replica, C.byref(n)))
         return n.value
+
+    def phase(self, phase: int) -> np.ndarray | None:
+        """One phase of a step (pf_phase, PF_KERNEL_PIPELINE): PF_PHASE_SCORE,
+        _INTENTION, _MOVEMENT (returns the [replicas] reports) or _RESET."""
+        out = np.zeros(self.replicas, REPORT_DTYPE) if phase == PF_PHASE_MOVEMENT else None
+        check(lib.pf_phase(self.h, phase, ptr(out)))
+        return out
+
+    def store_scores(self, replica: int, scores, owners=None):
+        """CandidateScores by agent id into scores [n, 8] (and owners [n])."""
+        n = len(scores)
+        check(lib.pf_store_scores(self.h, replica, ptr(scores), ptr(owners), n))
 
     def peer_desc(self) -> PfPeerDesc:
         """This shard's planes for its neighbours (pf_peer_export)."""

@@ -187,6 +187,11 @@ struct pf_ctx {
     uint32_t* remote_flag[2] = {nullptr, nullptr};
     int linked = 0;                             // bit s: neighbour on side s
     std::vector<void*> ipc_opened;              // peer allocations opened with cudaIpcOpenMemHandle
+    // Phase-level stepping (pf_phase, PF_KERNEL_PIPELINE): 0 between steps,
+    // else the last phase done + 1; CandidateScores by agent id.
+    int phase = 0;
+    double* d_scores = nullptr;
+    uint32_t scores_n = 0;                      // agents per replica slot of d_scores
     std::vector<int32_t> rep_aps;               // agents_per_side of each replica
     std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
@@ -279,6 +284,7 @@ int pf_destroy(pf_ctx* ctx) {
     if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
     if (ctx->io_scratch) cudaFree(ctx->io_scratch);
     if (ctx->io_event) cudaEventDestroy(ctx->io_event);
+    if (ctx->d_scores) cudaFree(ctx->d_scores);
     delete ctx;
     return PF_OK;
 }
@@ -515,6 +521,7 @@ static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& wor
 
 static void set_step(pf_ctx* ctx, uint32_t step) {
     ctx->step = step;
+    ctx->phase = 0;
     cudaMemcpyAsync(ctx->d_step, &ctx->step, 4, cudaMemcpyHostToDevice, ctx->stream);
     if (ctx->linked) {  // linked neighbours are (re)loaded to the same step
         const uint32_t sync[2] = {step, step};
@@ -706,7 +713,8 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
     PF_CUDA(cudaMemsetAsync(d_status, 0, 24, ctx->stream));
     if (agents) PF_CUDA(cudaMemsetAsync(d_agents, 0, size_t(n_agents) * 40, ctx->stream));
     sanitize_words(ctx, rep, d_status + 2);
-    ctx->launches += pfk::launch_export_state(P.cell[ctx->parity] + off, ctx->aco() ? P.tour + off : nullptr, own,
+    const uint8_t* intents = ctx->phase >= 2 ? P.intent + off : nullptr;  // futures between intention and reset
+    ctx->launches += pfk::launch_export_state(P.cell[ctx->parity] + off, ctx->aco() ? P.tour + off : nullptr, intents, own,
                                               uint32_t(W), uint32_t(ctx->row_begin), occ ? d_occ : nullptr,
                                               index ? d_index : nullptr, agents ? d_agents : nullptr, n_agents,
                                               d_status, ctx->stream);
@@ -756,6 +764,7 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         if (step) *step = ctx->step;
         return PF_OK;
     }
+    if (ctx->phase >= 2) return fail(PF_ERR_ARG, "a row shard's state cannot be stored in the middle of a phase-level step");
     IoTrace io_trace;
     const size_t W = size_t(c.width);
     const size_t own = size_t(ctx->rows_owned) * W;
@@ -905,6 +914,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
 
 int pf_step_async(pf_ctx* ctx, uint32_t n) {
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (ctx->phase) return fail(PF_ERR_ARG, "a phase-level step is in progress: finish it with PF_PHASE_RESET");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
     while (n > 0) {
         const uint32_t m = std::min<uint32_t>(n, kBatchCap);
@@ -943,6 +953,7 @@ int pf_synchronize(pf_ctx* ctx) {
 
 int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (ctx->phase) return fail(PF_ERR_ARG, "a phase-level step is in progress: finish it with PF_PHASE_RESET");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
     const int R = ctx->cfg.replicas;
     std::vector<pf_step_report> chunk;
@@ -964,6 +975,7 @@ int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
 
 int pf_time_steps(pf_ctx* ctx, uint32_t n, float* total_ms, float* kernel_ms) {
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (ctx->phase) return fail(PF_ERR_ARG, "a phase-level step is in progress: finish it with PF_PHASE_RESET");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
     cudaEvent_t e0, e1;
     PF_CUDA(cudaEventCreate(&e0));
@@ -1081,6 +1093,81 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
         }
     }
     PF_CUDA(cudaStreamSynchronize(lower->stream));
+    return PF_OK;
+}
+
+int pf_phase(pf_ctx* ctx, int32_t phase, pf_step_report* out) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (ctx->cfg.kernel != PF_KERNEL_PIPELINE)
+        return fail(PF_ERR_CONFIG, "phase-level stepping needs PF_KERNEL_PIPELINE (the fused kernels run all four phases "
+                                   "in one launch)");
+    if (phase < PF_PHASE_SCORE || phase > PF_PHASE_RESET) return fail(PF_ERR_ARG, "unknown phase");
+    if (phase != ctx->phase)
+        return fail(PF_ERR_ARG, "phases must run in order: score, intention, movement, reset");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    pfk::Planes& P = ctx->args.p;
+    const int R = ctx->cfg.replicas;
+    switch (phase) {
+        case PF_PHASE_SCORE: {  // src/engine.cpp:64-74
+            uint32_t n_max = 0;
+            for (const auto& r : ctx->reps) n_max = std::max(n_max, r.n_agents);
+            n_max = std::max(n_max, 1u);
+            if (ctx->scores_n < n_max) {
+                if (ctx->d_scores) cudaFree(ctx->d_scores);
+                ctx->d_scores = nullptr;
+                ctx->scores_n = 0;
+                PF_CUDA(cudaMalloc(&ctx->d_scores, size_t(R) * n_max * 64));
+                ctx->scores_n = n_max;
+            }
+            PF_CUDA(cudaMemsetAsync(ctx->d_scores, 0, size_t(R) * ctx->scores_n * 64, ctx->stream));
+            ctx->launches += pfk::launch_score_phase(ctx->args, ctx->parity, ctx->d_scores, nullptr, ctx->scores_n,
+                                                     ctx->stream);
+            break;
+        }
+        case PF_PHASE_INTENTION:  // src/engine.cpp:76-90
+            ctx->launches += pfk::launch_intention_phase(ctx->args, ctx->parity, ctx->stream);
+            break;
+        case PF_PHASE_MOVEMENT: {  // src/engine.cpp:92-180
+            if (int rc = zero_reports(ctx, ctx->step, 1)) return rc;
+            ctx->launches += pfk::launch_movement_phase(ctx->args, ctx->parity, ctx->stream);
+            ctx->parity ^= 1;
+            if (out) {
+                const size_t pitch = size_t(kReportCap) * 16;
+                PF_CUDA(cudaMemcpy2DAsync(out, 16, reinterpret_cast<const char*>(ctx->d_reports) +
+                                                       size_t(ctx->step % kReportCap) * 16,
+                                          pitch, 16, size_t(R), cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            break;
+        }
+        default:  // PF_PHASE_RESET, src/engine.cpp:183-193: scores zeroed, futures = positions, ++step
+            if (ctx->d_scores) PF_CUDA(cudaMemsetAsync(ctx->d_scores, 0, size_t(R) * ctx->scores_n * 64, ctx->stream));
+            ctx->launches += pfk::launch_advance_step(ctx->d_step, 1, ctx->stream);
+            ++ctx->step;
+            break;
+    }
+    PF_CUDA(cudaGetLastError());
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->phase = phase == PF_PHASE_RESET ? 0 : phase + 1;
+    return PF_OK;
+}
+
+int pf_store_scores(pf_ctx* ctx, int32_t rep, double* scores, uint32_t* owners, uint32_t n_agents) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
+    if (n_agents != ctx->reps[size_t(rep)].n_agents) return fail(PF_ERR_ARG, "agent count disagrees with the replica");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    PF_CUDA(cudaStreamSynchronize(ctx->stream));
+    // owner is always the agent's id: set by new_environment (src/state.cpp:48)
+    // and by every score_phase, never cleared (src/engine.cpp:183-193).
+    if (owners)
+        for (uint32_t i = 0; i < n_agents; ++i) owners[i] = i + 1;
+    if (!scores || !n_agents) return PF_OK;
+    if (!ctx->d_scores) {  // never scored: zeros, as new_environment leaves them
+        std::memset(scores, 0, size_t(n_agents) * 64);
+        return PF_OK;
+    }
+    PF_CUDA(cudaMemcpy(scores, ctx->d_scores + size_t(rep) * ctx->scores_n * 8, size_t(n_agents) * 64,
+                       cudaMemcpyDeviceToHost));
     return PF_OK;
 }
 

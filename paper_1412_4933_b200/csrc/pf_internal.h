@@ -107,8 +107,18 @@ int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* a
                         unsigned long long* status, cudaStream_t s);
 // Owned cell words -> reference occupancy / index planes and AgentRecords
 // (40-byte pf_agent, by id); status[0] += agent cells, status[1] += bad ids.
-int launch_export_state(const uint32_t* words, const double* tour, size_t n, uint32_t W, uint32_t row0, uint8_t* occ,
-                        uint32_t* index, void* agents, uint32_t n_agents, unsigned long long* status, cudaStream_t s);
+// intent (may be null): per-cell intended move codes (between the intention and
+// reset phases), exported as the agents' future_row / future_col.
+int launch_export_state(const uint32_t* words, const double* tour, const uint8_t* intent, size_t n, uint32_t W,
+                        uint32_t row0, uint8_t* occ, uint32_t* index, void* agents, uint32_t n_agents,
+                        unsigned long long* status, cudaStream_t s);
+// Phase-level stepping (PF_KERNEL_PIPELINE contexts): score_phase into
+// scores[replica][n_max][8] / owners[replica][n_max] by agent id; the
+// intention phase (propose kernel -> intent plane); the movement phase
+// (resolve + commit kernels, counters into the report slot of *d_step).
+int launch_score_phase(const StepArgs& a, int parity, double* scores, uint32_t* owners, uint32_t n_max, cudaStream_t s);
+int launch_intention_phase(const StepArgs& a, int parity, cudaStream_t s);
+int launch_movement_phase(const StepArgs& a, int parity, cudaStream_t s);
 int launch_selftest_select(int kind, uint32_t n, const pfdev::StepConsts* kc, const uint8_t* mask, const double* num,
                            const uint64_t* seed, const uint32_t* step, const uint64_t* entity, int32_t* out,
                            cudaStream_t s);

@@ -311,6 +311,61 @@ __global__ void __launch_bounds__(256) pipeline_commit_kernel(const StepArgs a, 
     block_count(moved, ntop, nbot, s_cnt, rep_slot, step, blockIdx.x == 0 && blockIdx.y == 0);
 }
 
+// score_phase (src/engine.cpp:64-74): every agent's CandidateScores (lem_scores
+// src/lem.cpp:8-18 or aco_numerators src/aco.cpp:39-51, goal-relative slot
+// order F FL FR L R B BL BR) by agent id; the values the selection uses.
+__global__ void __launch_bounds__(256) score_kernel(const StepArgs a, int parity, double* scores, uint32_t* owners,
+                                                    uint32_t n_max) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = kGhost + int(blockIdx.y);
+    const int rep = blockIdx.z;
+    const int W = a.k.W;
+    if (c >= W) return;
+    const size_t base = size_t(rep) * a.p.plane;
+    const uint32_t* cin = a.p.cell[parity] + base;
+    const uint32_t w = cin[size_t(b) * W + c];
+    if (w == 0u || w == kWall) return;
+    const uint32_t id = w & kIdMask;
+    if (id == 0u || id > n_max) return;
+    const bool bottom = (w >> 30) == 2u;
+    const double2* tin = a.k.model == 1 ? a.p.tau[parity] + base : nullptr;
+    double* out = scores + (size_t(rep) * n_max + (id - 1)) * 8;
+    for (int i = 0; i < 8; ++i) {
+        const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
+        const int cc = c + kDC[code];
+        const bool open = cc >= 0 && cc < W && cin[size_t(b + kDR[code]) * W + cc] == 0u;
+        double v = 0.0;
+        if (open) {
+            if (a.k.model == 0) {
+                v = a.kc->lem_score[i];
+            } else {
+                const double* t = reinterpret_cast<const double*>(tin + size_t(b + kDR[code]) * W + cc);
+                v = __dmul_rn(pheromone_term(a.kc, t[bottom ? 1 : 0]), a.kc->eta[i]);
+            }
+        }
+        out[i] = v;
+    }
+    if (owners) owners[size_t(rep) * n_max + (id - 1)] = id;
+}
+
+int launch_score_phase(const StepArgs& a, int parity, double* scores, uint32_t* owners, uint32_t n_max, cudaStream_t s) {
+    score_kernel<<<dim3((a.k.W + 255) / 256, a.rows_owned, a.replicas), 256, 0, s>>>(a, parity, scores, owners, n_max);
+    return 1;
+}
+
+int launch_intention_phase(const StepArgs& a, int parity, cudaStream_t s) {
+    pipeline_propose_kernel<<<dim3((a.k.W + 255) / 256, a.rows_owned + 4, a.replicas), 256, 0, s>>>(a, 0, parity);
+    return 1;
+}
+
+int launch_movement_phase(const StepArgs& a, int parity, cudaStream_t s) {
+    const int bx = (a.k.W + 255) / 256;
+    pipeline_resolve_kernel<<<dim3(bx, a.rows_owned + 2, a.replicas), 256, 0, s>>>(a, 0, parity);
+    if (a.k.model == 1) pipeline_commit_kernel<true><<<dim3(bx, a.rows_owned, a.replicas), 256, 0, s>>>(a, 0, parity);
+    else pipeline_commit_kernel<false><<<dim3(bx, a.rows_owned, a.replicas), 256, 0, s>>>(a, 0, parity);
+    return 2;
+}
+
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s) {
     const int bx = (a.k.W + 255) / 256;
     pipeline_propose_kernel<<<dim3(bx, a.rows_owned + 4, a.replicas), 256, 0, s>>>(a, slot, parity);
@@ -427,10 +482,11 @@ __global__ void import_state_kernel(const uint8_t* __restrict__ occ, const uint3
 // row | col << 32, future_row | future_col << 32 (= position after the
 // reset phase, src/engine.cpp:183-193), tour_length, crossed; padding zero).
 // status[0] += agent cells, status[1] += cells with an out-of-range id.
-__global__ void export_state_kernel(const uint32_t* __restrict__ words, const double* __restrict__ tour, size_t n,
-                                    uint32_t W, uint32_t row0, uint8_t* __restrict__ occ,
-                                    uint32_t* __restrict__ index, unsigned long long* __restrict__ agents,
-                                    uint32_t n_agents, unsigned long long* status) {
+__global__ void export_state_kernel(const uint32_t* __restrict__ words, const double* __restrict__ tour,
+                                    const uint8_t* __restrict__ intent, size_t n, uint32_t W, uint32_t row0,
+                                    uint8_t* __restrict__ occ, uint32_t* __restrict__ index,
+                                    unsigned long long* __restrict__ agents, uint32_t n_agents,
+                                    unsigned long long* status) {
     unsigned long long found = 0, bad = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t w = words[i];
@@ -448,7 +504,16 @@ __global__ void export_state_kernel(const uint32_t* __restrict__ words, const do
             unsigned long long* a = agents + size_t(id - 1) * 5;
             a[0] = id | (static_cast<unsigned long long>(w >> 30) << 32);
             a[1] = row | (col << 32);
-            a[2] = row | (col << 32);
+            // Between intention_phase and reset_phase the future is the intended
+            // cell (a mover's is its new cell: it arrived where no intent was).
+            const uint8_t code = intent ? intent[i] : pfdev::kNone;
+            if (code == pfdev::kNone) {
+                a[2] = row | (col << 32);
+            } else {
+                const unsigned long long fr = uint32_t(int(row) + pfdev::kDR[code]);
+                const unsigned long long fc = uint32_t(int(col) + pfdev::kDC[code]);
+                a[2] = fr | (fc << 32);
+            }
             a[3] = tour ? static_cast<unsigned long long>(__double_as_longlong(tour[i])) : 0ull;
             a[4] = (w & pfdev::kCrossedBit) ? 1ull : 0ull;
         }
@@ -515,9 +580,10 @@ int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* a
                                                 W, H, g0, g_lo, n, words, tour, status);
     return 1;
 }
-int launch_export_state(const uint32_t* words, const double* tour, size_t n, uint32_t W, uint32_t row0, uint8_t* occ,
-                        uint32_t* index, void* agents, uint32_t n_agents, unsigned long long* status, cudaStream_t s) {
-    export_state_kernel<<<148 * 8, 256, 0, s>>>(words, tour, n, W, row0, occ, index,
+int launch_export_state(const uint32_t* words, const double* tour, const uint8_t* intent, size_t n, uint32_t W,
+                        uint32_t row0, uint8_t* occ, uint32_t* index, void* agents, uint32_t n_agents,
+                        unsigned long long* status, cudaStream_t s) {
+    export_state_kernel<<<148 * 8, 256, 0, s>>>(words, tour, intent, n, W, row0, occ, index,
                                                 static_cast<unsigned long long*>(agents), n_agents, status);
     return 1;
 }

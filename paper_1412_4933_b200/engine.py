@@ -147,6 +147,7 @@ class SimState:
         aco = self.model == Model.Aco
         self._tau_top = zeros((height, width), np.float64) if aco else None
         self._tau_bot = zeros((height, width), np.float64) if aco else None
+        self._scores = np.zeros((n_agents, 8), np.float64)  # CandidateScores::score by agent id
         self._step = 0
         self._device = None  # (engine, replica) holding a newer copy
         self._version = 0    # bumped on host-side modification
@@ -172,6 +173,7 @@ class SimState:
         if self._tau_top is not None:
             s._tau_top[...] = self._tau_top
             s._tau_bot[...] = self._tau_bot
+        s._scores[...] = self._scores
         s._step = self._step
         return s
 
@@ -189,6 +191,19 @@ class SimState:
     def agents(self) -> np.ndarray:
         self._pull()
         return self._agents
+
+    @property
+    def scores(self) -> np.ndarray:
+        """CandidateScores::score (inc/pedflow/lem.hpp:14-17) by agent id,
+        [n_agents, 8] in goal-relative slot order: nonzero between
+        score_phase and reset_phase, zeros otherwise."""
+        self._pull()
+        return self._scores
+
+    @property
+    def score_owners(self) -> np.ndarray:
+        """CandidateScores::owner: always the agent's id (src/state.cpp:48)."""
+        return np.arange(1, len(self._agents) + 1, dtype=np.uint32)
 
     @property
     def pheromone_top(self) -> np.ndarray | None:
@@ -259,9 +274,10 @@ class StepEngine:
 
     ``step(state)`` advances the state by one synchronous step and returns its
     StepReport; ``run(state, n)`` is the batched fast path (one upload, n steps
-    through CUDA graphs, one lazy download). The phase methods of the reference
-    (score/intention/movement/reset) are fused into one kernel and are not
-    separately callable.
+    through CUDA graphs, one lazy download). The reference's phase methods
+    (score_phase / intention_phase / movement_phase / reset_phase) are
+    available on an engine built with ``kernel="pipeline"``; the default fused
+    kernel runs all four in one launch.
     """
 
     def __init__(self, opt: EngineOptions):
@@ -300,7 +316,33 @@ class StepEngine:
     def _download(self, state: SimState, rep: int):
         # planes are written in place by the library
         state._step = self._ctx.store(rep, state._occ, state._index, state._agents, state._tau_top, state._tau_bot)
+        if len(state._agents):
+            self._ctx.store_scores(rep, state._scores)
         self._bound = (id(state), state._version)
+
+    # --- phase-level stepping (src/engine.cpp:64-193) ------------------------
+    def _phase(self, state: SimState, phase: int):
+        self._attach(state)
+        out = self._ctx.phase(phase)
+        state._device = (self, 0)
+        return out
+
+    def score_phase(self, state: SimState) -> None:
+        """StepEngine::score_phase (src/engine.cpp:64-74): state.scores."""
+        self._phase(state, _lib.PF_PHASE_SCORE)
+
+    def intention_phase(self, state: SimState) -> None:
+        """StepEngine::intention_phase (src/engine.cpp:76-90): agents' futures."""
+        self._phase(state, _lib.PF_PHASE_INTENTION)
+
+    def movement_phase(self, state: SimState) -> StepReport:
+        """StepEngine::movement_phase (src/engine.cpp:92-180)."""
+        return StepReport.from_row(self._phase(state, _lib.PF_PHASE_MOVEMENT)[0])
+
+    def reset_phase(self, state: SimState) -> None:
+        """StepEngine::reset_phase (src/engine.cpp:183-193): scores zeroed,
+        futures re-anchored, ++step."""
+        self._phase(state, _lib.PF_PHASE_RESET)
 
     def run(self, state: SimState, n: int) -> list[StepReport]:
         """n full steps (StepEngine::step x n); returns the n StepReports."""

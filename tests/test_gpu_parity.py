@@ -255,3 +255,107 @@ def test_winner_draw_uniform_among_five_contenders():
     assert set(np.unique(got)) == {0, 2, 4, 5, 7}
     counts = np.bincount(got, minlength=8)[[0, 2, 4, 5, 7]]
     assert chisquare(counts).pvalue > 1e-3
+
+
+_TOP_OFFSETS = [(1, 0), (1, -1), (1, 1), (0, -1), (0, 1), (-1, 0), (-1, -1), (-1, 1)]  # inc/grid.hpp:19-43
+
+
+def _neighbourhood(s, a):
+    """Goal-relative slots of agent record a: (row, col) and open flag (in
+    bounds and empty at the step-start snapshot, inc/grid.hpp:109-125)."""
+    sign = 1 if a["group"] == 1 else -1
+    out = []
+    for dr, dc in _TOP_OFFSETS:
+        r, c = int(a["row"]) + sign * dr, int(a["col"]) + sign * dc
+        ok = 0 <= r < s.height and 0 <= c < s.width and s.occupancy[r, c] == 0
+        out.append((r, c, 1 if ok else 0))
+    return out
+
+
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_phase_level_api_matches_reference_phases(model):
+    """score_phase / intention_phase / movement_phase / reset_phase
+    (src/engine.cpp:64-193) one at a time on a PF_KERNEL_PIPELINE engine:
+    the scores after score_phase and the futures after intention_phase equal
+    the oracle's lem_scores / aco_numerators and lem_select / aco_select per
+    agent; movement_phase moves agents as a fused step does and leaves denied
+    agents' futures at their targets; reset_phase completes a step identical
+    to StepEngine::step; repeated phase steps equal pf_step."""
+    import ctypes as C
+
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import oracle
+
+    kw = dict(width=96, height=96, agents_per_side=1500, model=model, seed=3)
+    cfg = to_config(kw)
+    state = p.new_environment(cfg, 3)
+    eng = p.StepEngine(p.EngineOptions.from_config(cfg, 3, kernel="pipeline"))
+    eng.run(state, 40)
+    s0 = state.copy()
+    ref = s0.copy()
+    fused = p.StepEngine(p.EngineOptions.from_config(cfg, 3))
+    ref_report = fused.step(ref)
+    lib = oracle()
+    o = p.EngineOptions.from_config(cfg, 3)
+    d = (C.c_double * 8)()
+    lib.pfo_distance_table(o.d0, d)
+    eta = (C.c_double * 8)(*[(1.0 / x) ** o.beta for x in d])
+
+    eng.score_phase(state)
+    exp_scores = np.zeros((len(s0.agents), 8))
+    exp_future = np.zeros((len(s0.agents), 2), np.int64)
+    for i, a in enumerate(s0.agents):
+        nb = _neighbourhood(s0, a)
+        op = (C.c_uint8 * 8)(*[x[2] for x in nb])
+        sc = (C.c_double * 8)()
+        if model == "lem":
+            lib.pfo_lem_scores(op, d, sc)
+            slot = lib.pfo_lem_select(sc, op, 3, s0.step, int(a["index"]), o.sel_mu, o.sel_sigma)
+        else:
+            tau = s0.pheromone_top if a["group"] == 1 else s0.pheromone_bottom
+            t8 = (C.c_double * 8)(*[tau[r, c] if ok else 0.0 for r, c, ok in nb])
+            lib.pfo_aco_numerators(op, t8, o.alpha, eta, sc)
+            slot = lib.pfo_aco_select(sc, op, 3, s0.step, int(a["index"]))
+        exp_scores[i] = list(sc)
+        exp_future[i] = (nb[slot][0], nb[slot][1]) if slot >= 0 else (a["row"], a["col"])
+    assert (state.scores == exp_scores).all()
+    assert (state.score_owners == s0.agents["index"]).all()
+    assert (state.agents["future_row"] == s0.agents["row"]).all()  # no intentions yet
+
+    eng.intention_phase(state)
+    assert (state.agents["future_row"] == exp_future[:, 0]).all()
+    assert (state.agents["future_col"] == exp_future[:, 1]).all()
+    assert (state.agents["row"] == s0.agents["row"]).all()  # nobody moved yet
+    assert state.step == s0.step
+
+    report = eng.movement_phase(state)
+    assert (report.moved, report.newly_crossed_top, report.newly_crossed_bottom) == (
+        ref_report.moved, ref_report.newly_crossed_top, ref_report.newly_crossed_bottom)
+    assert (state.index == ref.index).all() and (state.occupancy == ref.occupancy).all()
+    ag = state.agents
+    assert (ag["row"] == ref.agents["row"]).all() and (ag["col"] == ref.agents["col"]).all()
+    moved = (ag["row"] != s0.agents["row"]) | (ag["col"] != s0.agents["col"])
+    assert moved.sum() == report.moved
+    # movers' futures are their new cells; denied agents keep their targets
+    assert (ag["future_row"] == exp_future[:, 0]).all() and (ag["future_col"] == exp_future[:, 1]).all()
+    assert state.step == s0.step
+
+    eng.reset_phase(state)
+    assert state.step == s0.step + 1
+    assert hashes_of(state) == hashes_of(ref)
+    assert (state.agents["future_row"] == state.agents["row"]).all()
+    assert not state.scores.any()
+
+    # phase-level steps == full steps
+    for _ in range(5):
+        eng.score_phase(state)
+        eng.intention_phase(state)
+        eng.movement_phase(state)
+        eng.reset_phase(state)
+    fused.run(ref, 5)
+    assert hashes_of(state) == hashes_of(ref)
+
+    with pytest.raises(ValueError):  # out of order (PF_ERR_ARG)
+        eng.movement_phase(state)
+    with pytest.raises(p.ConfigError):  # the fused kernel has no separate phases
+        fused.score_phase(ref)

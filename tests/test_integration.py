@@ -38,6 +38,23 @@ def test_cpp_dropin_matches_golden(anchors, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["s96_aco_900_s11", "s32_lem_200_s3"])
+def test_cpp_phase_methods_match_golden(anchors, name):
+    """The C++ shim's score_phase / intention_phase / movement_phase /
+    reset_phase (PF_KERNEL_PIPELINE), called one by one every step, land on
+    the unmodified reference's golden state."""
+    a = anchors[name]
+    sc = a["scenario"]
+    r = subprocess.run([DEMO, sc["model"], str(sc["width"]), str(sc["height"]), str(sc["agents_per_side"]),
+                        str(a["steps"]), str(sc.get("seed", 42)), "phases"], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr
+    moved, top, bot, h_index, h_occ = r.stdout.split()
+    assert (int(moved), int(top), int(bot)) == (a["sum_moved"], a["crossed_top"], a["crossed_bottom"])
+    assert (h_index, h_occ) == (a["hash"]["index"], a["hash"]["occ"])
+
+
+@pytest.mark.gpu
 def test_run_scenario_series_matches_golden(anchors):
     import paper_1412_4933_b200 as p
 

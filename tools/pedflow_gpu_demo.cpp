@@ -1,7 +1,10 @@
 // Drop-in demo: a run_scenario-style C++ caller (src/engine.cpp:195-231)
 // driving the B200 engine through include/pedflow_gpu.hpp only.
 //
-//   pedflow_gpu_demo <lem|aco> <width> <height> <agents_per_side> <steps> [seed]
+//   pedflow_gpu_demo <lem|aco> <width> <height> <agents_per_side> <steps> [seed] [phases]
+//
+// With "phases" every step is StepEngine::score_phase, intention_phase,
+// movement_phase and reset_phase called one by one (PF_KERNEL_PIPELINE).
 //
 // Prints one line: moved_sum crossed_top crossed_bottom index_fnv occ_fnv
 // (FNV-1a 64 as in tests/golden/make_golden.py) so tests can compare it with
@@ -36,10 +39,21 @@ int main(int argc, char** argv) {
         o.agents_per_side = std::atoi(argv[4]);
         const uint32_t steps = uint32_t(std::atoi(argv[5]));
         o.seed = argc > 6 ? std::strtoull(argv[6], nullptr, 10) : 42;
+        const bool phases = argc > 7 && std::strcmp(argv[7], "phases") == 0;
+        if (phases) o.kernel = PF_KERNEL_PIPELINE;
         pedflow::gpu::SimState s = pedflow::gpu::new_environment(o, o.seed);
         pedflow::gpu::StepEngine engine(o);
         std::vector<pedflow::gpu::StepReport> rep(steps);
-        engine.step_n(s, steps, rep.data());
+        if (phases) {
+            for (uint32_t i = 0; i < steps; ++i) {  // StepEngine::step, src/engine.cpp:53-62
+                engine.score_phase(s);
+                engine.intention_phase(s);
+                rep[i] = engine.movement_phase(s);
+                engine.reset_phase(s);
+            }
+        } else {
+            engine.step_n(s, steps, rep.data());
+        }
         uint64_t moved = 0, top = 0, bot = 0;
         for (const auto& r : rep) {
             moved += r.moved;
