@@ -12,10 +12,10 @@ from paper_1412_4933_b200 import _lib  # noqa: E402
 from paper_1412_4933_b200.engine import _pf_config  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5_aco"
-K = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+K = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 300
 cfg, reps, desc = bench.scenario(name)
 t = time.perf_counter()
-state = p.new_environment(cfg, 42)
+state = p.new_environment(cfg, 42, pinned="--pinned" in sys.argv)
 print(f"new_environment (host)   {time.perf_counter() - t:7.3f} s")
 c = _lib.Context(_pf_config(cfg, 42))
 for it in range(2):
