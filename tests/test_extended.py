@@ -61,6 +61,11 @@ def test_random_config_vs_oracle(kw):
     dict(width=960, height=64, agents_per_side=12000, model="lem", seed=78),
     # the same widths with ACO (256-column strips): 624 -> a 3-segment last strip
     dict(width=624, height=96, agents_per_side=9000, model="aco", seed=79),
+    # wide and flat: 52 strips of 10 segments, the last one 2 segments; one row tile
+    dict(width=16384, height=16, agents_per_side=40000, model="lem", seed=80),
+    dict(width=16384, height=16, agents_per_side=40000, model="aco", seed=81),
+    # narrow and tall: one half-filled segment, 256 row tiles
+    dict(width=16, height=4096, agents_per_side=9000, model="aco", seed=82),
 ], ids=lambda kw: f"{kw['model']}{kw['width']}x{kw['height']}")
 def test_strip_widths_vs_oracle(kw):
     """Grid widths that exercise both compiled strip widths (8 and 10
