@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (threadIdx.x == 0) sm.qc[cur ^ 1][0] = sm.qc[cur ^ 1][1] = 0u;
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
+#ifndef PF_BITS_STREAM_ONLY
         // ------------------------------------------------------------ S1
         // Intents for rows -2 .. RT+1, all staged segments (halo segments
         // only at the two columns next to the strip).
@@ -724,6 +725,12 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             __syncthreads();
         }
 
+#else
+        // Diagnostic build: no agent logic, every segment takes
+        // the no-movement path, i.e. the staged planes + the pheromone stream.
+        for (int u = threadIdx.x; u < AROWS * SS; u += NT) (&sm.A[0][0])[u] = 0u;
+        __syncthreads();
+#endif
         // ------------------------------------------------------------ S3
         for (int rr = warp; rr < RT; rr += NW) {
             const int lr = r0 + rr;
