@@ -1105,7 +1105,6 @@ int pf_phase(pf_ctx* ctx, int32_t phase, pf_step_report* out) {
     if (phase != ctx->phase)
         return fail(PF_ERR_ARG, "phases must run in order: score, intention, movement, reset");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
-    pfk::Planes& P = ctx->args.p;
     const int R = ctx->cfg.replicas;
     switch (phase) {
         case PF_PHASE_SCORE: {  // src/engine.cpp:64-74
