@@ -19,10 +19,10 @@ namespace bits_ns10 {
 int configure();
 int launch(const StepArgs& a, int slot, int parity, cudaStream_t s);
 }  // namespace bits_ns10
-namespace bits_ns8_rt8 {
+namespace bits_small {
 int configure();
 int launch(const StepArgs& a, int slot, int parity, cudaStream_t s);
-}  // namespace bits_ns8_rt8
+}  // namespace bits_small
 
 int bits_strip_segments(int width, int model) {
     if (model == 1) return 8;
@@ -31,15 +31,17 @@ int bits_strip_segments(int width, int model) {
     return units(10) < units(8) ? 10 : 8;
 }
 
-int configure_step_bits() { return bits_ns8::configure() | bits_ns10::configure() | bits_ns8_rt8::configure(); }
+int configure_step_bits() { return bits_ns8::configure() | bits_ns10::configure() | bits_small::configure(); }
 
 // Grids with fewer 16-row tiles than SMs (a single 480^2 scenario: 60 tiles)
 // run one tile per CTA on a fraction of the GPU, so their step time is one
-// tile's latency: 8-row tiles double the CTAs and halve each one's work.
+// tile's latency: they take 8-row tiles on 64-column strips (8x the CTAs,
+// pf_bitstep_small.cu). The occupancy-plane pitch (strips of 8 or 10
+// segments) also fits the 2-segment strips.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s) {
     if (a.strip_segs == 10) return bits_ns10::launch(a, slot, parity, s);
     const long long strips = (a.k.W + 255) / 256, tiles16 = strips * ((a.rows_owned + 15) / 16) * a.replicas;
-    if (tiles16 < a.num_sms) return bits_ns8_rt8::launch(a, slot, parity, s);
+    if (tiles16 < a.num_sms) return bits_small::launch(a, slot, parity, s);
     return bits_ns8::launch(a, slot, parity, s);
 }
 

@@ -9,5 +9,5 @@ cd "$(dirname "$0")/.."
 mkdir -p tools/debug
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off \
   -I include -DPF_BITS_RING=38 -shared -o tools/debug/libpedflow_b200_ring38.so \
-  paper_1412_4933_b200/csrc/pf_kernels.cu paper_1412_4933_b200/csrc/pf_bitstep.cu paper_1412_4933_b200/csrc/pf_bitstep_ns8.cu paper_1412_4933_b200/csrc/pf_bitstep_ns10.cu paper_1412_4933_b200/csrc/pf_bitstep_ns8_rt8.cu \
+  paper_1412_4933_b200/csrc/pf_kernels.cu paper_1412_4933_b200/csrc/pf_bitstep.cu paper_1412_4933_b200/csrc/pf_bitstep_ns8.cu paper_1412_4933_b200/csrc/pf_bitstep_ns10.cu paper_1412_4933_b200/csrc/pf_bitstep_small.cu \
   paper_1412_4933_b200/csrc/pf_context.cu paper_1412_4933_b200/csrc/pf_setup.cpp
