@@ -33,15 +33,17 @@ int bits_strip_segments(int width, int model) {
 
 int configure_step_bits() { return bits_ns8::configure() | bits_ns10::configure() | bits_small::configure(); }
 
-// Grids with fewer 16-row tiles than SMs (a single 480^2 scenario: 60 tiles)
-// run one tile per CTA on a fraction of the GPU, so their step time is one
-// tile's latency: they take 8-row tiles on 64-column strips (8x the CTAs,
-// pf_bitstep_small.cu). The occupancy-plane pitch (strips of 8 or 10
-// segments) also fits the 2-segment strips.
+// Grids with fewer than 2 x SMs 16-row tiles (a single 480^2 scenario: 60
+// tiles) run about one tile per CTA on a fraction of the GPU, so their step
+// time is one tile's latency: they take 8-row tiles on 64-column strips (8x
+// the CTAs, pf_bitstep_small.cu). Sweep (tools/small_tiles_sweep.py, 480^2
+// x R, 102,400 agents): x1 46 -> 17 us, x2 46 -> 28, x4 51 -> 37; x8 is
+// even (2-agent-dense LEM and sparse grids lose there). The occupancy-plane
+// pitch (strips of 8 or 10 segments) also fits the 2-segment strips.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s) {
     if (a.strip_segs == 10) return bits_ns10::launch(a, slot, parity, s);
     const long long strips = (a.k.W + 255) / 256, tiles16 = strips * ((a.rows_owned + 15) / 16) * a.replicas;
-    if (tiles16 < a.num_sms) return bits_small::launch(a, slot, parity, s);
+    if (a.small_tiles == 1 || (a.small_tiles < 0 && tiles16 < 2LL * a.num_sms)) return bits_small::launch(a, slot, parity, s);
     return bits_ns8::launch(a, slot, parity, s);
 }
 

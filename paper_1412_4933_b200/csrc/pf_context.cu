@@ -391,7 +391,9 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
         ctx->args.num_sms = sms > 0 ? sms : 148;
         const char* ipc = std::getenv("PEDFLOW_ITEMS_PER_CTA");  // tuning override (dev)
-        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : 32;  // short items: small end-of-step tail (sweep: C5 ACO -3.5%, LEM -7% vs 4)
+        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : 32;
+        const char* st = std::getenv("PEDFLOW_SMALL_TILES");  // dev: force / forbid the small-grid geometry
+        ctx->args.small_tiles = st ? (std::atoi(st) ? 1 : 0) : -1;  // short items: small end-of-step tail (sweep: C5 ACO -3.5%, LEM -7% vs 4)
     }
     if (!ok || !ctx->d_step || !ctx->d_reports || !ctx->args.work) {
         cudaGetLastError();

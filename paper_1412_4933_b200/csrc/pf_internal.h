@@ -64,6 +64,7 @@ struct StepArgs {
     int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
     PeerRows peer[2];       // [0] the shard above (toward row 0), [1] below; cell == nullptr: none
     int strip_segs;         // bit kernel: 32-column segments per strip (bits_strip_segments)
+    int small_tiles;        // bit kernel: -1 auto, 0 / 1 force the small-grid geometry (dev: PEDFLOW_SMALL_TILES)
     // Fused halo ordering (linked shards): sync_local[side] = steps whose
     // boundary items the neighbour on that side has completed (written by it);
     // sync_remote[side] = our flag in the neighbour's memory; bcount = per-step
