@@ -27,7 +27,7 @@
 // run of consecutive RT-row tiles. The step-start planes of the strip live in
 // a shared-memory ring of staged rows (tile + 3-row halo + the next tile's
 // rows); while a tile is processed, TMA bulk copies (cp.async.bulk + mbarrier,
-// one (NS + 4) * 8-byte row each) bring the next tile's RT new rows. Warp 0
+// one (NS + 4) * 8-byte row each) bring the next tile's RT new rows. One warp
 // claims work items from a per-step counter and publishes them decoded.
 //
 //   S1 intent  thread per segment-row: forward moves (F open, no draw,
@@ -106,6 +106,10 @@ constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
 constexpr int AROWS = RT + 2;    // resolution rows -1 .. RT
 constexpr int NU = DROWS * SS;   // intent units (>= resolution units AROWS * SS)
+// The warp that issues the row loads and claims work items during the tile
+// loop: the last one. S1 units fill the warps in order, so the last warp has
+// the fewest (or none) and its issue work does not delay the S1 barrier.
+constexpr int kIoWarp = NW - 1;
 static_assert(NU * 32 < (1 << 16), "work-list bit counts must fit 16 bits");
 
 struct Smem {
@@ -134,7 +138,7 @@ struct Smem {
     // with one-tile items the next claim can come before the slowest warp
     // has read the previous one (no barrier in between).
     int item[2];
-    int idec[2][4];   // the same items decoded (rep, strip, chunk, sides) by warp 0: no divisions per thread
+    int idec[2][4];   // the same items decoded (rep, strip, chunk, sides) once: no divisions per thread
     uint32_t cnt[3];
     double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
 };
@@ -408,7 +412,7 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
     return it;
 }
 
-// An item decoded by warp 0 (Smem::idec) for the rest of the CTA.
+// An item decoded by the claiming warp (Smem::idec) for the rest of the CTA.
 __device__ __forceinline__ void publish_item(int (&d)[4], const Item& it) {
     d[0] = it.rep;
     d[1] = it.strip;
@@ -603,11 +607,11 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // previous readers all passed the end-of-tile barrier): the next
         // tile's RT new rows, or on the last tile the next item's window.
         if (t + 1 < it.t_end) {
-            if (warp == 0) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
+            if (warp == kIoWarp) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
             ++nload;
         } else {
             next_base = kCrossPrefetch ? slot(base, SR) : 0;
-            if (warp == 0) {
+            if (warp == kIoWarp) {
                 int nx = 0;
                 if (lane == 0) nx = int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
@@ -856,13 +860,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     if (!kCrossPrefetch && item < n_items) {
         // Small ring: the next item's window is loaded only now, into the
         // slots the finished item released.
-        if (warp == 0) {
+        if (warp == kIoWarp) {
             const Item nit = read_item(sm.idec[islot], n_tiles, a.tiles_per_cta);
             if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
             __syncwarp();
             load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
         }
-        __syncthreads();  // wall rows written by warp 0 are visible to all
+        __syncthreads();  // wall rows written by the I/O warp are visible to all
     }
     if (item < n_items) ++nload;
     }  // work items
