@@ -51,6 +51,33 @@ def test_struct_layouts():
     assert C.sizeof(_lib.PfConfig) == 4 * 4 + 8 + 8 * 8 + 5 * 4 + 4
 
 
+def test_ctypes_layouts_match_the_header(tmp_path):
+    """Every struct the Python binding mirrors has the C header's size and
+    field offsets (compiled here with gcc against include/pf_gpu.h)."""
+    import ctypes as C
+
+    from paper_1412_4933_b200 import _lib
+
+    structs = {"pf_config": _lib.PfConfig, "pf_halo_rows": _lib.PfHalo, "pf_peer_desc": _lib.PfPeerDesc}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pf_gpu.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-std=c11", "-I", inc, "-o", str(exe), str(src)], check=True)
+    got = dict(line.rsplit(" ", 1) for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                              check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[f"{cname} sizeof"]) == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname} {fname}"]) == getattr(py, fname).offset, (cname, fname)
+
+
 @pytest.mark.parametrize("kw,msg", [
     (dict(width=100), "multiple of 16"),
     (dict(height=8), "multiple of 16"),
