@@ -41,12 +41,20 @@ def _stale(target, deps):
 
 
 def build_lib(force: bool = False, verbose_ptxas: bool = False) -> str:
+    """Compile every source to an object in parallel (the kernel template is
+    instantiated in three translation units), then link the shared library."""
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "pf_gpu.h")]
     if force or _stale(LIB, deps):
-        cmd = [NVCC] + NVFLAGS + ["-shared", "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
-        if verbose_ptxas:
-            cmd += ["-Xptxas", "-v"]
-        _run(cmd)
+        from concurrent.futures import ThreadPoolExecutor
+
+        objdir = os.path.join(PKG, "build_obj")
+        os.makedirs(objdir, exist_ok=True)
+        extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+        jobs = [(os.path.join(CSRC, src), os.path.join(objdir, src + ".o")) for src in SOURCES]
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as pool:
+            for f in [pool.submit(_run, [NVCC] + NVFLAGS + extra + ["-c", "-o", obj, src]) for src, obj in jobs]:
+                f.result()
+        _run([NVCC] + GENCODE + ["-shared", "-o", LIB] + [obj for _, obj in jobs])
     return LIB
 
 
