@@ -539,12 +539,10 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
 
     const int W = a.k.W;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t step = *a.d_step + uint32_t(slot_idx);
     const int strips = (W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
     const int n_chunks = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
     const int n_items = strips * n_chunks * a.replicas;
-    uint32_t* work = a.work + step % uint32_t(a.report_cap);
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.mbar[0], 1);
@@ -560,6 +558,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         sm.D[i / DROWS][i % DROWS][0] = 0u;
         sm.D[i / DROWS][i % DROWS][SS + 1] = 0u;
     }
+    // Launched with programmatic stream serialization: everything above only
+    // touches shared memory, so it overlaps the previous step's tail; from
+    // here on the previous step's results (planes, words, step counter) are
+    // complete and visible.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t step = *a.d_step + uint32_t(slot_idx);
+    uint32_t* work = a.work + step % uint32_t(a.report_cap);
     __syncthreads();
     // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
     // taken from a per-step counter so heavy (crowded) chunks balance out.
@@ -616,6 +621,9 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 if (lane == 0) nx = int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item[ipar] = nx;
+                // This CTA's last item: the next step's grid may be scheduled
+                // (its CTAs wait in griddepcontrol.wait until this grid ends).
+                if (nx >= n_items && lane == 0) asm volatile("griddepcontrol.launch_dependents;");
                 if (nx < n_items) {
                     const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
                     if (lane == 0) publish_item(sm.idec[ipar], nit);
@@ -895,6 +903,24 @@ int configure() {
     return 0;
 }
 
+// Launch with programmatic stream serialization (PDL): the next step's
+// kernel may be scheduled while this one finishes its last items.
+template <class Kernel>
+static void launch_pdl(Kernel kernel, dim3 grid, size_t smem, cudaStream_t s, const StepArgs& b, int slot_idx,
+                       int parity) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, b, slot_idx, parity);
+}
+
 // Persistent grid: one CTA per resident slot (SMs x 3, 4 or 5) at most. Work
 // items are chunks of up to 16 consecutive RT-row tiles of one strip of one
 // replica, sized so there are about 32 items per CTA (a short tail at the
@@ -915,17 +941,17 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const size_t bytes = kSmemBytes[aco ? 1 : 0];
     const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
     if (!aco && big) {
-        if (mirror) step_bits_kernel<false, kCtasLemBig, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<false, kCtasLemBig, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLemBig, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLemBig, false>, grid, bytes, s, b, slot_idx, parity);
     } else if (!aco) {
-        if (mirror) step_bits_kernel<false, kCtasLem, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<false, kCtasLem, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLem, false>, grid, bytes, s, b, slot_idx, parity);
     } else if (hbm) {
-        if (mirror) step_bits_kernel<true, kCtasHbm, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<true, kCtasHbm, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasHbm, false>, grid, bytes, s, b, slot_idx, parity);
     } else {
-        if (mirror) step_bits_kernel<true, kCtasDefault, true><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
-        else step_bits_kernel<true, kCtasDefault, false><<<grid, NT, bytes, s>>>(b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasDefault, false>, grid, bytes, s, b, slot_idx, parity);
     }
     return 1;
 }
