@@ -646,26 +646,54 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
 #ifndef PF_BITS_STREAM_ONLY
         // ------------------------------------------------------------ S1
         // Intents for rows -2 .. RT+1, all staged segments (halo segments
-        // only at the two columns next to the strip).
-        for (int u = threadIdx.x; u < DROWS * SS; u += NT) {
-            const int di = u / SS, si = u - di * SS;  // di = rr + 2
-            const uint2 p = sm.pl[slot(base, di + 1)][si + 1];
-            const Around n = around(sm, base, di + 1, si);
-            const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
-            const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
-            uint32_t d[8];
+        // only at the two columns next to the strip). A thread takes two
+        // vertically adjacent units: they share two of their four staged
+        // rows (12 plane loads instead of 18).
+        static_assert(DROWS % 2 == 0, "S1 pairs intent rows");
+        for (int u2 = threadIdx.x; u2 < (DROWS / 2) * SS; u2 += NT) {
+            const int dp = u2 / SS, si = u2 - dp * SS;
+            const int di0 = 2 * dp;  // intent rows di0, di0 + 1 = staged rows di0 + 1, di0 + 2
+            uint32_t E[4][3];        // emptiness of staged rows di0 .. di0 + 3 at segments si-1, si, si+1
+            uint2 P[2];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) d[q] = 0u;
-            d[6] = T & n.ep;  // Top forward: (+1, 0)
-            d[1] = B & n.em;  // Bottom forward: (-1, 0)
-            const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
-            const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-            if (slow) {
-                enqueue(sm, &sm.qc[cur][0], u, slow);
-                sm.rowdraw[cur][di] = 1u;
+            for (int r = 0; r < 4; ++r) {
+                const uint2* row = sm.pl[slot(base, di0 + r)] + si + 1;
+                const uint2 m = row[0];
+                E[r][0] = empty_of(row[-1]);
+                E[r][1] = empty_of(m);
+                E[r][2] = empty_of(row[1]);
+                if (r == 1) P[0] = m;
+                if (r == 2) P[1] = m;
             }
+            const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
+            for (int k = 0; k < 2; ++k) {
+                const int di = di0 + k, u = di * SS + si;
+                Around n;
+                n.em = E[k][1];
+                n.emL = from_left(E[k][1], E[k][0]);
+                n.emR = from_right(E[k][1], E[k][2]);
+                n.e0L = from_left(E[k + 1][1], E[k + 1][0]);
+                n.e0R = from_right(E[k + 1][1], E[k + 1][2]);
+                n.ep = E[k + 2][1];
+                n.epL = from_left(E[k + 2][1], E[k + 2][0]);
+                n.epR = from_right(E[k + 2][1], E[k + 2][2]);
+                const uint2 p = P[k];
+                const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
+                uint32_t d[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) d[q] = 0u;
+                d[6] = T & n.ep;  // Top forward: (+1, 0)
+                d[1] = B & n.em;  // Bottom forward: (-1, 0)
+                const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
+                const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
+                if (slow) {
+                    enqueue(sm, &sm.qc[cur][0], u, slow);
+                    sm.rowdraw[cur][di] = 1u;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
+            }
         }
         __syncthreads();
         // Draws, spread evenly over the CTA (the barrier is skipped,
