@@ -96,11 +96,10 @@ constexpr int SS = NS + 2;       // intent / resolution segments: -1 .. NS
 constexpr int SP = NS + 4;       // staged plane segments: -2 .. NS+1 (pl index = si + 1)
 static_assert(SP * 8 % 16 == 0, "a staged plane row must be a whole number of 16-byte TMA units");
 constexpr int NT = PF_BITS_NT;   // threads per CTA
-// Resident CTAs per SM (register budget 65536 / (NT * CTAS)): 4 (64
-// registers) for LEM and for small (480^2-class, replica-batched) ACO grids;
-// 3 (80 registers, no spills) for large ACO grids, which are pure pheromone
-// streams and lose more to spills than the extra warps hide (A/B at step
-// 150: C5 ACO +2%, C4 x64 ACO -5%, C5 LEM -12%, C3 x64 LEM -11%).
+// Resident CTAs per SM (register budget 65536 / (NT * CTAS)), chosen per
+// launch (see launch()): 4 (64 registers) for LEM and for small
+// replica-batched ACO grids; 3 (80 registers, no spills) for large ACO grids,
+// which are pure pheromone streams; 5 (48 registers) for large LEM grids.
 constexpr int kRegCtas = NT == 256 ? 4 : 65536 / (NT * 64);
 constexpr int NW = NT / 32;
 constexpr int DROWS = RT + 4;    // intent rows -2 .. RT+1
