@@ -379,6 +379,7 @@ def run_gpu_arm(args):
             "hbm_gbs_alg_step": bytes_step * args.steps / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_8tbs_spec": achieved / 8000.0,
                          "kernel": "step_bits_kernel", "kernel_ms": kernel_ms,
                          "kernel_ms_isolated_launch_events": kernel_ms_isolated,
                          "alg_bytes_per_launch": bytes_launch,
