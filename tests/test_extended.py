@@ -85,6 +85,25 @@ def test_strip_widths_vs_oracle(kw):
 
 
 @pytest.mark.gpu
+def test_wide_strip_geometry_replicas_vs_oracle():
+    """A LEM batch large enough for the regular geometry (not the small-grid
+    one) on a width that takes 320-column strips with 32-row tiles (624 =
+    19.5 segments: a 2-segment last strip, a half segment): replicas 0 and 19
+    of a 20-seed batch equal their oracle runs."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    kw = dict(width=624, height=96, agents_per_side=9000, model="lem", seed=100)
+    steps = 120
+    ens = p.Ensemble(to_config(kw), replicas=20)
+    rep = ens.run(steps)
+    for r in (0, 19):
+        ora = OracleState(to_scenario(dict(kw, seed=100 + r)))
+        assert (rep[r] == ora.run(steps)).all(), f"replica {r}: reports differ"
+        assert first_divergence(ens.state(r), ora) == "identical", f"replica {r}"
+
+
+@pytest.mark.gpu
 def test_subnormal_pheromone_regime_vs_oracle():
     """16,000 ACO steps: the pheromone fields decay into the subnormal range
     (most cells end below 2.2e-308, the smallest at 4e-323). fp64 on the GPU
