@@ -84,6 +84,9 @@ namespace {
 constexpr int RT = PF_BITS_RT;   // output rows per tile
 constexpr int NS = PF_BITS_NS;   // output 32-column segments per strip
 constexpr int SR = RT + 6;       // staged rows of one tile: -3 .. RT+2
+#ifdef PF_BITS_SMALL_RING  // debug build (tools/build_debug.sh): no cross-item prefetch
+#define PF_BITS_RING (SR + RT)
+#endif
 #ifndef PF_BITS_RING
 #define PF_BITS_RING (2 * SR)
 #endif
