@@ -17,8 +17,11 @@ from paper_1412_4933_b200.sharding import row_partition  # noqa: E402
 steps = int(os.environ.get("STEPS", "12"))
 C = p.ScenarioConfig
 for model in (p.Model.Lem, p.Model.Aco):
-    # (the 48-replica batch gives CTAs several one-tile work items)
-    for w, h, n, reps in ((96, 96, 2000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 2000, 48)):
+    # Small single grids take the small-grid geometry; the 64-replica 96^2
+    # batch the regular 256-column one (several one-tile items per CTA); the
+    # 20-replica 624-wide LEM batch the 320-column / 32-row one.
+    for w, h, n, reps in ((96, 96, 2000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 2000, 64),
+                          (624, 96, 9000, 20)):
         cfg = C(width=w, height=h, agents_per_side=n, model=model, seed=5)
         for kernel in ("fused", "tile", "pipeline"):
             e = p.Ensemble(cfg, replicas=reps, kernel=kernel)
