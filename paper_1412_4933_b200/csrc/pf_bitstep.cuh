@@ -321,15 +321,17 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
     if (!ACO) {
         s = lem_choose(a.kc, open, seed, step, id);
     } else {
-        // All eight neighbour loads are issued before any is used (they are
-        // in bounds for every agent cell: rows b-1 .. b+1 lie inside the
-        // buffer and a column step off the row lands in the adjacent row).
+        // All the open neighbours' loads are issued before any is used. Only
+        // open slots are read: an open slot is an empty cell inside the
+        // buffer, while a closed one may lie outside it (an agent in a
+        // shard's first ghost row at column 0 has its (-1,-1) neighbour
+        // before the start of the allocation).
         const double* t0 = reinterpret_cast<const double*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
         double tn[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-            tn[i] = __ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code]));
+            tn[i] = (open >> i & 1u) ? __ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code])) : 0.0;
         }
         double num[8];
 #pragma unroll

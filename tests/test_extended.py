@@ -85,6 +85,27 @@ def test_strip_widths_vs_oracle(kw):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_regular_geometry_replicas_vs_oracle(model):
+    """A batch large enough for the regular geometry (256-column strips,
+    16-row tiles, several one-tile work items per CTA: 96^2 x 64 replicas),
+    as in the bench's 480^2 x 64 configs; single small grids take the
+    small-grid geometry instead. Replicas 0, 31 and 63 equal their oracle
+    runs (seed + replica)."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    kw = dict(width=96, height=96, agents_per_side=2500, model=model, seed=200)
+    steps = 150
+    ens = p.Ensemble(to_config(kw), replicas=64)
+    rep = ens.run(steps)
+    for r in (0, 31, 63):
+        ora = OracleState(to_scenario(dict(kw, seed=200 + r)))
+        assert (rep[r] == ora.run(steps)).all(), f"replica {r}: reports differ"
+        assert first_divergence(ens.state(r), ora) == "identical", f"replica {r}"
+
+
+@pytest.mark.gpu
 def test_wide_strip_geometry_replicas_vs_oracle():
     """A LEM batch large enough for the regular geometry (not the small-grid
     one) on a width that takes 320-column strips with 32-row tiles (624 =

@@ -298,6 +298,51 @@ def test_gpu_fused_halo_minimum_shards(model):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_gpu_fused_halo_regular_geometry(model):
+    """Linked shards large enough for the regular geometry (the C5-style
+    path: 16-row tiles, boundary items claimed first, multi-tile items):
+    96 x 160 over 2 shards x 64 replicas, equal to the unsharded batch."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
+
+    cfg = p.ScenarioConfig(width=96, height=160, agents_per_side=3000, model=p.Model.Lem if model == "lem" else p.Model.Aco,
+                           seed=8)
+    steps, reps = 120, 64
+    whole = p.Ensemble(cfg, replicas=reps, seed=8)
+    whole_rep = whole.run(steps)
+    shards = []
+    for lo, hi in row_partition(cfg.height, 2):
+        c = _lib.Context(_pf_config(cfg, 8, replicas=reps, row_begin=lo, row_end=hi))
+        c.init_environment()
+        shards.append(c)
+    _lib.link_shards(shards)
+    for c in shards:
+        c.step_async(steps)
+    for c in shards:
+        c.synchronize()
+    tot = sum(c.read_reports(steps)["moved"].astype(np.int64) for c in shards)
+    assert (tot == whole_rep["moved"]).all()
+    for r in (0, 37, 63):
+        ref = whole.state(r)
+        H, W = cfg.height, cfg.width
+        idx = np.zeros((H, W), np.uint32)
+        occ = np.zeros((H, W), np.uint8)
+        ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+        tt = np.zeros((H, W)) if model == "aco" else None
+        tb = np.zeros((H, W)) if model == "aco" else None
+        for c in shards:
+            c.store(r, occ, idx, ag, tt, tb)
+        assert (idx == ref.index).all() and (occ == ref.occupancy).all()
+        if tt is not None:
+            assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
+    for c in shards:
+        c.close()
+
+
+@pytest.mark.gpu
 def test_gpu_fused_halo_rejects_mismatched_peers():
     import paper_1412_4933_b200 as p
     from paper_1412_4933_b200 import _lib
