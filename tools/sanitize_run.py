@@ -1,5 +1,5 @@
 """Small workloads for compute-sanitizer (dev tool): every step kernel
-variant on a few small grids, including linked shards (fused halo).
+variant on a few small grids, including 4 linked shards (fused halo).
 
     compute-sanitizer --tool memcheck  python tools/sanitize_run.py
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
@@ -20,7 +20,9 @@ for model in (p.Model.Lem, p.Model.Aco):
     # Small single grids take the small-grid geometry; the 64-replica 96^2
     # batch the regular 256-column one (several one-tile items per CTA); the
     # 20-replica 624-wide LEM batch the 320-column / 32-row one.
-    for w, h, n, reps in ((96, 96, 2000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 2000, 64),
+    # Dense bands (96^2 with 3000 per side: 32 rows) put agents in the ghost
+    # rows of the 4-way shard split from step 0.
+    for w, h, n, reps in ((96, 96, 3000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 3000, 64),
                           (624, 96, 9000, 20)):
         cfg = C(width=w, height=h, agents_per_side=n, model=model, seed=5)
         for kernel in ("fused", "tile", "pipeline"):
@@ -30,7 +32,7 @@ for model in (p.Model.Lem, p.Model.Aco):
             e.audit(0)
             e.close()
         shards = []
-        for lo, hi in row_partition(h, 2):
+        for lo, hi in row_partition(h, 4):
             c = _lib.Context(_pf_config(cfg, 5, replicas=reps, row_begin=lo, row_end=hi))
             c.init_environment()
             shards.append(c)
