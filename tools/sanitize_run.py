@@ -3,7 +3,7 @@ variant on a few small grids, including 4 linked shards (fused halo).
 
     compute-sanitizer --tool memcheck  python tools/sanitize_run.py
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
-    compute-sanitizer --tool synccheck python tools/sanitize_run.py
+    SANITIZE_NO_LINK=1 compute-sanitizer --tool synccheck python tools/sanitize_run.py
 """
 import os
 import sys
@@ -31,6 +31,11 @@ for model in (p.Model.Lem, p.Model.Aco):
             e.state(0)
             e.audit(0)
             e.close()
+        if os.environ.get("SANITIZE_NO_LINK"):
+            # synccheck runs kernels one at a time; linked shards on one GPU
+            # wait inside their kernels for each other and need them concurrent.
+            print(f"ok {model.name} {w}x{h} n={n} x{reps} (unlinked)", flush=True)
+            continue
         shards = []
         for lo, hi in row_partition(h, 4):
             c = _lib.Context(_pf_config(cfg, 5, replicas=reps, row_begin=lo, row_end=hi))
