@@ -964,7 +964,10 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const bool big = double(a.k.W) * a.rows_buf >= double(1 << 22);  // >= 4M cells per replica
     const bool hbm = aco && big;
     const int ctas = !aco ? (big ? kCtasLemBig : kCtasLem) : (hbm ? kCtasHbm : kCtasDefault);
-    const long long ctas_max = (long long)a.num_sms * ctas;
+    // A linked neighbour on the same GPU (tests, development) needs resident
+    // slots for its own boundary items while ours wait for them in-kernel:
+    // take at most half of them. (One shard per GPU never shares.)
+    const long long ctas_max = (long long)a.num_sms * ctas / (a.peer_same_device ? 2 : 1);
     const long long tiles = (long long)strips * n_tiles * a.replicas;
     StepArgs b = a;
     b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));

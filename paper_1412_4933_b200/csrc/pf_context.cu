@@ -391,9 +391,10 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
         ctx->args.num_sms = sms > 0 ? sms : 148;
         const char* ipc = std::getenv("PEDFLOW_ITEMS_PER_CTA");  // tuning override (dev)
+        // ~32 short items per CTA: a small end-of-step tail (sweep: C5 ACO -3.5%, LEM -7% vs 4)
         ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : 32;
         const char* st = std::getenv("PEDFLOW_SMALL_TILES");  // dev: force / forbid the small-grid geometry
-        ctx->args.small_tiles = st ? (std::atoi(st) ? 1 : 0) : -1;  // short items: small end-of-step tail (sweep: C5 ACO -3.5%, LEM -7% vs 4)
+        ctx->args.small_tiles = st ? (std::atoi(st) ? 1 : 0) : -1;
     }
     if (!ok || !ctx->d_step || !ctx->d_reports || !ctx->args.work) {
         cudaGetLastError();
@@ -1265,6 +1266,7 @@ int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc
     pr.row_delta = side == 0 ? d->rows_owned : -ctx->rows_owned;
     ctx->remote_flag[side] = static_cast<uint32_t*>(p[6]) + (1 - side);
     ctx->args.sync_remote[side] = ctx->remote_flag[side];
+    if (d->device == ctx->cfg.device) ctx->args.peer_same_device = 1;
     const uint32_t now = ctx->step;  // the neighbour has completed `step` steps
     PF_CUDA(cudaMemcpy(ctx->d_sync + side, &now, 4, cudaMemcpyHostToDevice));
     ctx->linked |= 1 << side;

@@ -73,6 +73,7 @@ struct StepArgs {
     uint32_t* sync_remote[2];
     uint32_t* bcount;
     uint32_t* err;
+    int peer_same_device;   // a linked neighbour shares this GPU: leave it resident slots (no in-kernel wait deadlock)
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
