@@ -391,8 +391,10 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
         ctx->args.num_sms = sms > 0 ? sms : 148;
         const char* ipc = std::getenv("PEDFLOW_ITEMS_PER_CTA");  // tuning override (dev)
-        // ~32 short items per CTA: a small end-of-step tail (sweep: C5 ACO -3.5%, LEM -7% vs 4)
-        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : 32;
+        // Short items per CTA keep the end-of-step tail small; longer ones reuse
+        // the halo rows of consecutive tiles (sweeps: C5 ACO best at 32, C5 LEM
+        // with 32-row tiles best at 16, -5.5% against 32).
+        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : (cfg->model == PF_MODEL_LEM ? 16 : 32);
         const char* st = std::getenv("PEDFLOW_SMALL_TILES");  // dev: force / forbid the small-grid geometry
         ctx->args.small_tiles = st ? (std::atoi(st) ? 1 : 0) : -1;
     }
