@@ -783,9 +783,21 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             const int grow = a.row_begin + lr;
             const int rs = slot(base, rr + 3), ai = rr + 1;
             uint2* const orow = oout + size_t(b) * a.p.wsp;
-            if (!ACO && !sm.dirty[cur][rr]) {
-                // Nothing arrives or leaves in this row: its planes are copied.
+            if (!sm.dirty[cur][rr]) {
+                // Nothing arrives or leaves in this row: its planes are copied
+                // (and for ACO its pheromone only evaporates).
                 if (lane < NS) orow[lane] = sm.pl[rs][lane + 2];
+                if (ACO) {
+                    const size_t r0c = size_t(b) * W + c0 + lane;
+                    double2 tc[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        tc[s] = (c0 + 32 * s + lane < W) ? tin[r0c + 32 * s] : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        if (c0 + 32 * s + lane < W)
+                            tout[r0c + 32 * s] = make_double2(__dmul_rn(tc[s].x, a.k.factor), __dmul_rn(tc[s].y, a.k.factor));
+                }
                 continue;
             }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
