@@ -562,22 +562,26 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         sm.D[i / DROWS][i % DROWS][0] = 0u;
         sm.D[i / DROWS][i % DROWS][SS + 1] = 0u;
     }
-    // Launched with programmatic stream serialization: everything above only
-    // touches shared memory, so it overlaps the previous step's tail; from
-    // here on the previous step's results (planes, words, step counter) are
-    // complete and visible.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t step = *a.d_step + uint32_t(slot_idx);
-    uint32_t* work = a.work + step % uint32_t(a.report_cap);
-    __syncthreads();
     // Work item = (replica, strip, chunk of tiles_per_cta consecutive tiles),
-    // taken from a per-step counter so heavy (crowded) chunks balance out.
+    // taken from a per-launch counter so heavy (crowded) chunks balance out.
     // The next item is claimed during the current item's last tile and its
     // first window is loaded into the other half of the ring meanwhile.
+    // The counter of batch slot slot_idx is zeroed before the batch and no
+    // other launch touches it, so the first claim needs no ordering.
+    uint32_t* const work = a.work + slot_idx;
     int item = 0;
     if (warp == 0) {
         if (lane == 0) item = int(atomicAdd(work, 1u));
         item = __shfl_sync(0xFFFFFFFFu, item, 0);
+    }
+    // Launched with programmatic stream serialization: everything above only
+    // touches shared memory and this launch's own counter, so it overlaps the
+    // previous step's tail; from here on the previous step's results (planes,
+    // words, step counter) are complete and visible.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t step = *a.d_step + uint32_t(slot_idx);
+    __syncthreads();
+    if (warp == 0) {
         if (lane == 0) sm.item[1] = item;
         if (item < n_items) {
             const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);

@@ -857,10 +857,12 @@ static int zero_reports(pf_ctx* ctx, uint32_t first, uint32_t n) {
         const uint32_t m = std::min<uint32_t>(n - done, kReportCap - slot);
         PF_CUDA(cudaMemset2DAsync(reinterpret_cast<char*>(ctx->d_reports) + size_t(slot) * 16, pitch, 0,
                                   size_t(m) * 16, size_t(ctx->cfg.replicas), ctx->stream));
-        PF_CUDA(cudaMemsetAsync(ctx->args.work + slot, 0, size_t(m) * 4, ctx->stream));  // work-item counters
         PF_CUDA(cudaMemsetAsync(ctx->args.bcount + size_t(slot) * 2, 0, size_t(m) * 8, ctx->stream));  // boundary items
         done += m;
     }
+    // Work-item counters, one per batch slot (step_bits_kernel claims its
+    // first item before griddepcontrol.wait, so they are not per step).
+    PF_CUDA(cudaMemsetAsync(ctx->args.work, 0, size_t(std::min<uint32_t>(n, kBatchCap)) * 4, ctx->stream));
     return PF_OK;
 }
 

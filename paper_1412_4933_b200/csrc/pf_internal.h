@@ -59,7 +59,7 @@ struct StepArgs {
     int rows_buf;           // rows_owned + 2 * kGhost
     int replicas;
     int tiles_per_cta;      // bit kernel: consecutive row tiles per work item (set at launch)
-    uint32_t* work;         // bit kernel: per-step work-item counters, ring slot = step % report_cap
+    uint32_t* work;         // bit kernel: work-item counters, one per batch slot (zeroed per batch)
     int num_sms;
     int items_per_cta;      // bit kernel: target work items per resident CTA (load balance vs row reuse)
     PeerRows peer[2];       // [0] the shard above (toward row 0), [1] below; cell == nullptr: none
