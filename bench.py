@@ -46,6 +46,11 @@ WORKLOADS = {
     "c3_lem": (480, 480, 51_200, "lem", 1, "C3: LEM 480x480, 51,200 agents/side (102,400), seed 42"),
     "c2_aco": (480, 480, 1_024, "aco", 1, "C2: ACO 480x480, 1,024 agents/side, seed 42"),
     "c1_lem": (480, 480, 1_024, "lem", 1, "C1: LEM 480x480, 1,024 agents/side, seed 42"),
+    "c2_aco_x64": (480, 480, 1_024, "aco", 64, "C2 x64: ACO 480x480, 1,024 agents/side, 64 seeds per launch"),
+    "c1_lem_x64": (480, 480, 1_024, "lem", 64, "C1 x64: LEM 480x480, 1,024 agents/side, 64 seeds per launch"),
+    # The paper's smallest density point (SURVEY.md 8(d) notes).
+    "c2_aco_1280": (480, 480, 1_280, "aco", 1, "C2 @1,280/side: ACO 480x480, 1,280 agents/side, seed 42"),
+    "c1_lem_1280": (480, 480, 1_280, "lem", 1, "C1 @1,280/side: LEM 480x480, 1,280 agents/side, seed 42"),
 }
 
 
@@ -217,7 +222,7 @@ def run_reference_arm(args):
 
 def secondary_runs(steps):
     """C4/C3 (100K agents) replica-batched and single-scenario device timings,
-    and C2/C1. The window is steps 5 .. 5+steps of the run: with steps = 1000
+    and C2/C1 (single, 64-seed batches, and the paper's 1,280/side point). The window is steps 5 .. 5+steps of the run: with steps = 1000
     (the length of the C3/C4 golden runs) it covers the approach of the two
     crowds AND the congested regime after they meet (~step 130), which costs
     2-3x more per step than the free-flow start."""
@@ -225,7 +230,8 @@ def secondary_runs(steps):
 
     peak, _ = measured_peak()
     out = {}
-    for name in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem"):
+    for name in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem", "c2_aco_x64", "c1_lem_x64",
+                 "c2_aco_1280", "c1_lem_1280"):
         cfg, reps, desc = scenario(name)
         ens = p.Ensemble(cfg, replicas=reps)
         ens.run(5)
