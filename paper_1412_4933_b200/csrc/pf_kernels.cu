@@ -592,7 +592,7 @@ int launch_gather_tour(double* per_agent, const uint32_t* words, const double* t
     return 1;
 }
 
-// --- occupancy bit planes of the fused kernel (pf_bitstep.cu) -----------
+// --- occupancy bit planes of the fused kernel (pf_bitstep.cuh) ----------
 
 // Warp per 32-cell segment, lane = column: two ballots of the word's group
 // bits; columns past W are walls (both bits set).
