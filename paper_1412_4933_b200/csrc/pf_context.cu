@@ -391,10 +391,12 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
         ctx->args.num_sms = sms > 0 ? sms : 148;
         const char* ipc = std::getenv("PEDFLOW_ITEMS_PER_CTA");  // tuning override (dev)
-        // Short items per CTA keep the end-of-step tail small; longer ones reuse
-        // the halo rows of consecutive tiles (sweeps: C5 ACO best at 32, C5 LEM
-        // with 32-row tiles best at 16, -5.5% against 32).
-        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : (cfg->model == PF_MODEL_LEM ? 16 : 32);
+        // Short items keep the end-of-step tail small; longer ones save item
+        // claims and reuse the staged halo rows of consecutive tiles. Sweeps on
+        // the final kernel: C5 LEM (32-row tiles) best at 16 items per CTA
+        // (2 tiles per item); C5 ACO best with one tile per item (-1.2% against
+        // 4), which 256 items per CTA gives for any grid up to ~110K tiles.
+        ctx->args.items_per_cta = ipc ? std::max(1, std::atoi(ipc)) : (cfg->model == PF_MODEL_LEM ? 16 : 256);
         const char* st = std::getenv("PEDFLOW_SMALL_TILES");  // dev: force / forbid the small-grid geometry
         ctx->args.small_tiles = st ? (std::atoi(st) ? 1 : 0) : -1;
     }

@@ -106,6 +106,30 @@ def test_regular_geometry_replicas_vs_oracle(model):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model", ["lem", "aco"])
+@pytest.mark.parametrize("items_per_cta", ["1", "256"])
+def test_tiles_per_item_vs_oracle(model, items_per_cta, monkeypatch):
+    """Work items of many tiles (1 item per CTA: up to 16 consecutive tiles,
+    staged rows carried tile to tile) and of one tile (256 items per CTA, the
+    ACO default) on a batch with enough tiles for both (1024^2 x 16: 2048+
+    tiles over 592 CTA slots, so one item per CTA is 3-6 tiles), against the
+    oracle. The default item size differs per model, so each model runs both."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    monkeypatch.setenv("PEDFLOW_ITEMS_PER_CTA", items_per_cta)
+    kw = dict(width=1024, height=1024, agents_per_side=60000, model=model, seed=300)
+    steps = 80
+    ens = p.Ensemble(to_config(kw), replicas=16)
+    rep = ens.run(steps)
+    for r in (0, 15):
+        ora = OracleState(to_scenario(dict(kw, seed=300 + r)))
+        assert (rep[r] == ora.run(steps)).all(), f"replica {r}: reports differ"
+        assert first_divergence(ens.state(r), ora) == "identical", f"replica {r}"
+    ens.close()
+
+
+@pytest.mark.gpu
 def test_wide_strip_geometry_replicas_vs_oracle():
     """A LEM batch large enough for the regular geometry (not the small-grid
     one) on a width that takes 320-column strips with 32-row tiles (624 =
