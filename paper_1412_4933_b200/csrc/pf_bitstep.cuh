@@ -971,8 +971,8 @@ static void launch_pdl(Kernel kernel, dim3 grid, size_t smem, cudaStream_t s, co
 
 // Persistent grid: one CTA per resident slot (SMs x 3, 4 or 5) at most. Work
 // items are chunks of up to 16 consecutive RT-row tiles of one strip of one
-// replica, sized so there are about 32 items per CTA (a short tail at the
-// end of the step; consecutive tiles of an item share their halo rows).
+// replica, about items_per_cta items per CTA (pf_context.cu: one tile per
+// item for ACO, two for C5 LEM; a short tail at the end of the step).
 int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const int strips = (a.k.W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
