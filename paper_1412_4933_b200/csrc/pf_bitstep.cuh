@@ -385,9 +385,15 @@ __device__ __forceinline__ int side_chunks(int s, int n_chunks, int tiles_per_it
     return s == 0 ? 1 : n;
 }
 
-// Linked shards (bfirst) number the boundary chunks of every (replica, strip)
-// first, so they are claimed early in the step: the neighbours' next steps
-// wait only for those (see wait_boundary / signal_boundary).
+// Items are numbered strip-fastest: the CTAs in flight at any moment work on
+// a band of whole rows rather than on a few hundred tiles down one strip.
+// The stream then covers full rows of every plane: C5 ACO's DRAM bytes fall
+// to the algorithmic 8.8 GB (neighbouring tiles' halo and draw reads hit in
+// L2) and, mostly, the achieved DRAM bandwidth rises (the step runs 7.8%
+// faster than with chunk-fastest numbering). Linked shards (bfirst) number the
+// boundary chunks of every (replica, strip) first, so they are claimed early
+// in the step: the neighbours' next steps wait only for those (see
+// wait_boundary / signal_boundary).
 __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
                                             int reps, bool bfirst, int rows_owned) {
     Item it;
@@ -401,13 +407,13 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
         } else {
             const int ni = n_chunks - nb, j = item - nbi;
             it.rep = j / (strips * ni);
-            it.strip = (j / ni) % strips;
-            it.chunk = 1 + j % ni;
+            it.strip = j % strips;
+            it.chunk = 1 + (j / strips) % ni;
         }
     } else {
         it.rep = item / (strips * n_chunks);
-        it.strip = (item / n_chunks) % strips;
-        it.chunk = item % n_chunks;
+        it.strip = item % strips;
+        it.chunk = (item / strips) % n_chunks;
     }
     it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
     it.c0 = it.strip * (NS * 32);
