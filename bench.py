@@ -395,6 +395,10 @@ def run_gpu_arm(args):
             "setup_s": setup_s,
             "moved_in_window_rank0": moved_local,
         }
+        if achieved > peak:
+            line["roofline"]["peak_note"] = ("achieved exceeds the driver's measured peak, a torch copy_ of 2 GiB "
+                                             "(MEASURED_PEAKS.json 'how'), which is not the HBM ceiling; "
+                                             "frac_of_8tbs_spec is the fraction of the B200 spec bandwidth")
         if e2e:
             line["e2e"] = e2e
     if dist is not None:
