@@ -385,8 +385,11 @@ __device__ __forceinline__ int side_chunks(int s, int n_chunks, int tiles_per_it
     return s == 0 ? 1 : n;
 }
 
-// Items are numbered strip-fastest: the CTAs in flight at any moment work on
-// a band of whole rows rather than on a few hundred tiles down one strip.
+// Items are numbered strip-fastest, then replica, then chunk: the CTAs in
+// flight at any moment work on a band of whole rows (of every replica of a
+// batch) rather than on a few hundred tiles down one strip. For batches,
+// replica before chunk takes the 480^2 x64 configs 9-16% faster than
+// replica-major numbering.
 // The stream then covers full rows of every plane: C5 ACO's DRAM bytes fall
 // to the algorithmic 8.8 GB (neighbouring tiles' halo and draw reads hit in
 // L2) and, mostly, the achieved DRAM bandwidth rises (the step runs 7.8%
@@ -405,15 +408,15 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
             it.strip = r / nb;
             it.chunk = (r % nb) ? n_chunks - 1 : 0;
         } else {
-            const int ni = n_chunks - nb, j = item - nbi;
-            it.rep = j / (strips * ni);
+            const int j = item - nbi;
             it.strip = j % strips;
-            it.chunk = 1 + (j / strips) % ni;
+            it.rep = (j / strips) % reps;
+            it.chunk = 1 + j / (strips * reps);
         }
     } else {
-        it.rep = item / (strips * n_chunks);
         it.strip = item % strips;
-        it.chunk = (item / strips) % n_chunks;
+        it.rep = (item / strips) % reps;
+        it.chunk = item / (strips * reps);
     }
     it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
     it.c0 = it.strip * (NS * 32);
