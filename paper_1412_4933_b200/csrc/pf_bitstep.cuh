@@ -397,6 +397,11 @@ __device__ __forceinline__ int side_chunks(int s, int n_chunks, int tiles_per_it
 // boundary chunks of every (replica, strip) first, so they are claimed early
 // in the step: the neighbours' next steps wait only for those (see
 // wait_boundary / signal_boundary).
+// The k-th row band of chunks, taken alternately from the top and the bottom
+// of the grid (0, n-1, 1, n-2, ...): the crowded bands at both ends start
+// early and are spread over the step (C5 LEM -5.8%, C3 x64 -4.2%, ACO -1%).
+__device__ __forceinline__ int two_ended(int k, int n) { return (k & 1) ? n - 1 - (k >> 1) : (k >> 1); }
+
 __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
                                             int reps, bool bfirst, int rows_owned) {
     Item it;
@@ -411,12 +416,12 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
             const int j = item - nbi;
             it.strip = j % strips;
             it.rep = (j / strips) % reps;
-            it.chunk = 1 + j / (strips * reps);
+            it.chunk = 1 + two_ended(j / (strips * reps), n_chunks - nb);
         }
     } else {
         it.strip = item % strips;
         it.rep = (item / strips) % reps;
-        it.chunk = item / (strips * reps);
+        it.chunk = two_ended(item / (strips * reps), n_chunks);
     }
     it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
     it.c0 = it.strip * (NS * 32);
