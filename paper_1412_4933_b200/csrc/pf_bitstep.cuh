@@ -400,10 +400,11 @@ __device__ __forceinline__ int side_chunks(int s, int n_chunks, int tiles_per_it
 // The k-th row band of chunks, taken alternately from the top and the bottom
 // of the grid (0, n-1, 1, n-2, ...): the crowded bands at both ends start
 // early and are spread over the step (C5 LEM -5.8%, C3 x64 -4.2%, ACO -1%).
+// Used when there are more items than CTAs (decode_item's `spread`).
 __device__ __forceinline__ int two_ended(int k, int n) { return (k & 1) ? n - 1 - (k >> 1) : (k >> 1); }
 
 __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, int n_tiles, int tiles_per_item,
-                                            int reps, bool bfirst, int rows_owned) {
+                                            int reps, bool bfirst, int rows_owned, bool spread) {
     Item it;
     if (bfirst) {
         const int nb = n_chunks >= 2 ? 2 : 1, nbi = reps * strips * nb;
@@ -416,12 +417,12 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
             const int j = item - nbi;
             it.strip = j % strips;
             it.rep = (j / strips) % reps;
-            it.chunk = 1 + two_ended(j / (strips * reps), n_chunks - nb);
+            it.chunk = 1 + (spread ? two_ended(j / (strips * reps), n_chunks - nb) : j / (strips * reps));
         }
     } else {
         it.strip = item % strips;
         it.rep = (item / strips) % reps;
-        it.chunk = two_ended(item / (strips * reps), n_chunks);
+        it.chunk = spread ? two_ended(item / (strips * reps), n_chunks) : item / (strips * reps);
     }
     it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
     it.c0 = it.strip * (NS * 32);
@@ -561,6 +562,10 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
     const int n_chunks = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
     const int n_items = strips * n_chunks * a.replicas;
+    // Two-ended row bands only pay when items queue up; when every item has
+    // its own CTA (small grids), plain order keeps neighbouring tiles on
+    // neighbouring CTAs.
+    const bool spread = n_items > int(gridDim.x);
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.mbar[0], 1);
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     if (warp == 0) {
         if (lane == 0) sm.item[1] = item;
         if (item < n_items) {
-            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread);
             if (lane == 0) publish_item(sm.idec[1], first);
             if (MIRROR && first.sides && lane == 0) wait_boundary(a, first.sides, step);
             __syncwarp();
@@ -647,7 +652,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 // (its CTAs wait in griddepcontrol.wait until this grid ends).
                 if (nx >= n_items && lane == 0) asm volatile("griddepcontrol.launch_dependents;");
                 if (nx < n_items) {
-                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned);
+                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread);
                     if (lane == 0) publish_item(sm.idec[ipar], nit);
                     if (kCrossPrefetch) {
                         if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
