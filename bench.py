@@ -54,24 +54,59 @@ WORKLOADS = {
 }
 
 
-ALG_MODEL = ("bit-plane state (DESIGN.md §2): 0.5 B/cell (2-bit occupancy planes read + written) + 8 B/mover "
-             "(source cell word read, destination word written); ACO + 32 B/cell (two f64 pheromone fields read + "
-             "written) + 16 B/mover (f64 tour read + written)")
+SURVEY_MODEL = ("SURVEY.md §8(d): LEM 8 B/cell (one packed u32 cell word read + written); ACO 40 B/cell "
+                "(word 8 + two f64 pheromone fields read + written 32) + 16 B/agent (f64 tour read + written)")
+BITPLANE_MODEL = ("bit-plane state actually streamed (DESIGN.md §2): 0.5 B/cell (2-bit occupancy planes read + "
+                  "written) + 8 B/mover (source cell word read, destination word written); ACO + 32 B/cell (two f64 "
+                  "pheromone fields read + written) + 16 B/mover (f64 tour read + written)")
 
 
-def alg_bytes(w, h, model, replicas, movers):
+def alg_bytes_survey(w, h, model, replicas, agents_per_side):
+    """SURVEY.md §8(d)'s per-unit figure x the units of one launch: 8 B/cell
+    (LEM), 40 B/cell + 16 B/agent (ACO). Its 8 B/cell assumes a ping-pong word
+    plane; the in-place word plane of this design streams 0.5 B/cell + 8 B per
+    mover instead (alg_bytes_bitplane), so fractions on this model can exceed
+    1 without any work being skipped."""
+    cells = w * h * replicas
+    if model == "aco":
+        return 40 * cells + 16 * 2 * agents_per_side * replicas
+    return 8 * cells
+
+
+def alg_bytes_bitplane(w, h, model, replicas, movers):
     """Algorithmic HBM bytes per step of the bit-plane representation
-    (SURVEY.md §8(d) counted 8 B/cell for the packed word
-    plane, which the in-place word plane no longer streams): every cell's
-    occupancy bits are read and written (2 x 2 bits), every mover's word is
-    read at its source and written at its destination; ACO adds both f64
-    pheromone fields read + written for every cell and the f64 tour read +
-    written per mover. `movers` = agents moved per step (StepReport.moved)."""
+    (DESIGN.md §2-3): every cell's occupancy bits are read and written
+    (2 x 2 bits), every mover's word is read at its source and written at its
+    destination; ACO adds both f64 pheromone fields read + written for every
+    cell and the f64 tour read + written per mover. `movers` = agents moved
+    per step (StepReport.moved). ncu's DRAM bytes per launch match this."""
     cells = w * h * replicas
     b = 0.5 * cells + 8 * movers
     if model == "aco":
         b += 32 * cells + 16 * movers
     return b
+
+
+def roofline_pair(w, h, model, reps, aps, movers, kernel_ms, peak, world=1):
+    """Both byte models for one launch of the step kernel (its shard at N>1)."""
+    out = {}
+    for key, b in (("survey", alg_bytes_survey(w, h, model, reps, aps)),
+                   ("bitplane", alg_bytes_bitplane(w, h, model, reps, movers))):
+        b /= world
+        ach = b / (kernel_ms / 1e3) / 1e9
+        out[key] = {"alg_bytes_per_launch": b, "achieved": ach, "frac": ach / peak}
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def measured_peak():
@@ -156,10 +191,13 @@ def scenario(name):
 
 # ------------------------------------------------------------------ CPU arms
 
-def cpu_reference_run(name, steps, warmup, budget_s):
+def cpu_reference_run(name, steps, warmup, budget_s, sequential_steps=1):
     """The reference CPU implementation on this host: oracle/_ref (the
     reference library built from its own sources) when present, else the C
-    oracle port. Parallel executor with every host thread. Returns a dict."""
+    oracle port. The Parallel executor with every host thread is timed first,
+    then (same placement, continuing) the Sequential executor on one core, as
+    the reference's own `bench` compares them (tools/pedflow.cpp:191-225).
+    Returns a dict; value = the Parallel rate."""
     from oracle.oracle import OracleState, Reference, Scenario
 
     w, h, n, model, reps, desc = WORKLOADS[name]
@@ -191,18 +229,31 @@ def cpu_reference_run(name, steps, warmup, budget_s):
         if secs + spent > budget_s:
             break
     agents = 2 * n
-    return {"value": agents * done / secs, "secs": secs, "steps": done, "kind": kind, "cores": cores,
-            "setup_s": setup, "cells": w * h,
-            "sample": f"{desc}; steps {warmup}..{warmup + done - 1} timed after new_environment "
-                      f"({setup:.1f}s untimed setup), {'Parallel executor' if kind == 'reference' else 'sequential C port'}, "
-                      f"{cores} thread(s)"}
+    out = {"value": agents * done / secs, "secs": secs, "steps": done, "kind": kind, "cores": cores,
+           "setup_s": setup, "cells": w * h, "cpu_model": cpu_model(), "logical_cpus": os.cpu_count(),
+           "sample": f"{desc}; steps {warmup}..{warmup + done - 1} timed after new_environment "
+                     f"({setup:.1f}s untimed setup), {'Parallel executor' if kind == 'reference' else 'sequential C port'}, "
+                     f"{cores} thread(s), {cpu_model()}"}
+    if kind == "reference" and sequential_steps > 0:
+        eng.set_executor(0)  # Sequential, same state
+        first = warmup + done
+        sq, sd = 0.0, 0
+        while sd < sequential_steps:
+            sq += one()
+            sd += 1
+            if sq > budget_s:
+                break
+        out["sequential"] = {"value": agents * sd / sq, "unit": "agent-updates/s", "cores": 1,
+                             "ms_per_step": 1e3 * sq / sd,
+                             "sample": f"steps {first}..{first + sd - 1}, Sequential executor, 1 thread"}
+    return out
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # only rank 0 times the CPU reference
-    r = cpu_reference_run(args.workload, args.steps, args.warmup, args.ref_budget)
+    r = cpu_reference_run(args.workload, args.steps, args.warmup, args.ref_budget, sequential_steps=0)
     w, h, n, model, reps, desc = WORKLOADS[args.workload]
     line = {
         "impl": "reference", "metric": "agent-updates/sec", "value": r["value"], "unit": "agent-updates/s",
@@ -212,7 +263,7 @@ def run_reference_arm(args):
         "config": {"workload": desc, "width": w, "height": h, "agents_per_side": n, "model": model, "replicas": 1},
         "cell_updates_per_s": w * h * r["steps"] / r["secs"],
         "cpu_baseline": {"value": r["value"], "unit": "agent-updates/s", "cores": r["cores"], "kind": r["kind"],
-                         "sample": r["sample"]},
+                         "sample": r["sample"], "cpu_model": r["cpu_model"]},
         "e2e": {"value": r["value"], "unit": "agent-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -221,35 +272,91 @@ def run_reference_arm(args):
 # ------------------------------------------------------------------ GPU arm
 
 def secondary_runs(steps):
-    """C4/C3 (100K agents) replica-batched and single-scenario device timings,
-    and C2/C1 (single, 64-seed batches, and the paper's 1,280/side point). The window is steps 5 .. 5+steps of the run: with steps = 1000
-    (the length of the C3/C4 golden runs) it covers the approach of the two
-    crowds AND the congested regime after they meet (~step 130), which costs
-    2-3x more per step than the free-flow start."""
+    """Device timings beside the headline:
+
+    * C4/C3 (the north star's "100K-pedestrian step loop") as 64-seed
+      replica batches and single scenarios; C2/C1 single, x64 and at the
+      paper's 1,280/side point. The window is steps 5 .. 5+steps: with
+      steps = 1000 (the length of the C3/C4 golden runs) it covers the
+      approach of the two crowds AND the congested regime after they meet
+      (~step 130), which costs 2-3x more per step than the free-flow start.
+    * C5 LEM (16384^2, 50M agents), steps 5..305.
+    * C5 ACO as 2 and 4 linked row shards on this ONE GPU (fused halo
+      exchange, same process): all shards share the device, so the ideal is
+      the unsharded step time; the difference is the per-step boundary
+      ordering + mirroring cost (not a scaling measurement).
+    """
+    import torch
+
     import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
 
     peak, _ = measured_peak()
     out = {}
     for name in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem", "c2_aco_x64", "c1_lem_x64",
-                 "c2_aco_1280", "c1_lem_1280"):
+                 "c2_aco_1280", "c1_lem_1280", "c5_lem"):
         cfg, reps, desc = scenario(name)
         ens = p.Ensemble(cfg, replicas=reps)
         ens.run(5)
-        n = min(steps, 1024)
+        n = min(steps if not name.startswith("c5") else 300, 1024)
+        ens.ctx.prepare_steps(n)
         tot, _ = ens.time_steps(n)
         movers = float(ens.ctx.read_reports(n)["moved"].astype(np.int64).sum()) / n
         _, ker = ens.time_steps(min(n, 50), kernel=True)
         model = "lem" if cfg.model == p.Model.Lem else "aco"
-        b = alg_bytes(cfg.width, cfg.height, model, reps, movers)
+        rl = roofline_pair(cfg.width, cfg.height, model, reps, cfg.agents_per_side, movers, tot / n, peak)
         out[name] = {
             "workload": desc, "window": f"steps 5..{5 + n}", "ms_per_step": tot / n,
             "kernel_ms_isolated_launch_events": ker,
             "agent_updates_per_s": 2 * cfg.agents_per_side * reps * n / (tot / 1e3),
             "cell_updates_per_s": cfg.width * cfg.height * reps * n / (tot / 1e3),
             "movers_per_step": movers,
-            "roofline_frac": b / (tot / n / 1e3) / 1e9 / peak, "alg_bytes_per_step": b,
+            "roofline_frac": rl["survey"]["frac"], "roofline_frac_bitplane": rl["bitplane"]["frac"],
+            "alg_bytes_per_step": rl["survey"]["alg_bytes_per_launch"],
+            "alg_bytes_per_step_bitplane": rl["bitplane"]["alg_bytes_per_launch"],
+            "traffic": ncu_traffic(name),
         }
         ens.close()
+    # C5 ACO as linked shards on this one GPU
+    cfg, reps, desc = scenario("c5_aco")
+    shard = {}
+    for k in (1, 2, 4):
+        ctxs = []
+        for lo, hi in row_partition(cfg.height, k):
+            c = _lib.Context(_pf_config(cfg, 42, row_begin=0 if k == 1 else lo, row_end=0 if k == 1 else hi))
+            c.init_environment()
+            ctxs.append(c)
+        if k > 1:
+            _lib.link_shards(ctxs)
+        for c in ctxs:
+            c.step_async(5)
+        for c in ctxs:
+            c.synchronize()
+            c.prepare_steps(100)
+        torch.cuda.synchronize()
+        ev = []
+        for c in ctxs:  # events on each shard's own stream; span = first start .. last end
+            st = torch.cuda.ExternalStream(c.stream())
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record(st)
+            c.step_async(100)
+            e[1].record(st)
+            ev.append(e)
+        for c in ctxs:
+            c.synchronize()
+        span = max(ev[0][0].elapsed_time(e[1]) for e in ev)
+        shard[f"shards{k}"] = {"ms_per_step": span / 100, "window": "steps 5..105"}
+        for c in ctxs:
+            c.close()
+        torch.cuda.empty_cache()
+    for k in (2, 4):
+        shard[f"shards{k}"]["overhead_vs_unsharded"] = shard[f"shards{k}"]["ms_per_step"] / shard["shards1"]["ms_per_step"] - 1
+    shard["note"] = ("C5 ACO split into k linked row shards (fused P2P halo: boundary rows stored into the "
+                     "neighbours' ghost rows + device flag handshake per step) all on ONE GPU: measures ordering and "
+                     "mirroring overhead, not multi-GPU scaling")
+    out["c5_aco_linked_shards_one_gpu"] = shard
     # SPEC acceptance #6 (SPEC:536): ACO <= 1.4x LEM time at 480x480, 20,480
     # agents, 500 steps (single scenario, and as a 64-seed batch).
     spec6 = {}
@@ -269,7 +376,6 @@ def run_gpu_arm(args):
     import torch
 
     import paper_1412_4933_b200 as p
-    from paper_1412_4933_b200 import _lib
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -323,16 +429,17 @@ def run_gpu_arm(args):
     t_setup = time.perf_counter()
     eng = ShardedEngine(cfg, rank, world, device=local, replicas=reps)
     setup_s = time.perf_counter() - t_setup
-    eng.step(args.warmup)
-    eng.synchronize()
-    barrier()
     stream = torch.cuda.ExternalStream(eng.ctx.stream(), device=f"cuda:{local}")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = eng.ctx.launches
     with ClockSampler(local) as clocks:
         time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
-        eng.step(max(1, args.warmup))  # keep the GPU busy while the sampler spins up
+        eng.step(args.warmup)  # the W untimed warm-up steps (also keep the GPU busy for the sampler)
+        eng.synchronize()
+        if world == 1:
+            eng.ctx.prepare_steps(args.steps)  # graph capture stays outside the timed region
+        barrier()
         torch.cuda.synchronize()
+        launches0 = eng.ctx.launches
         e0.record(stream)
         if world == 1:
             eng.ctx.step_async(args.steps)  # CUDA-graph batches
@@ -341,8 +448,8 @@ def run_gpu_arm(args):
         e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
+        launches = eng.ctx.launches - launches0
     barrier()
-    launches = eng.ctx.launches - launches0
     ms = max_over_ranks(e0.elapsed_time(e1))
     rep = eng.reports(min(args.steps, 1024))
     moved_local = int(rep["moved"].sum())
@@ -361,14 +468,13 @@ def run_gpu_arm(args):
     agents_total = 2 * n * reps
     value = agents_total * args.steps / (ms / 1e3)
     moved_all = sum_over_ranks(moved_local)
-    bytes_step = alg_bytes(w, h, model, reps, moved_all / min(args.steps, 1024))
-    bytes_launch = bytes_step / world  # per rank's kernel (its shard)
-    achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
+    movers = moved_all / min(args.steps, 1024)
+    rl = roofline_pair(w, h, model, reps, n, movers, kernel_ms, peak, world)
 
-    # --- end to end through the C-ABI with host buffers ----------------
+    # --- end to end with host buffers ----------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks)
+        e2e = e2e_runs(args, cfg, reps, rank, world, local, barrier, max_over_ranks)
 
     line = None
     if rank == 0:
@@ -382,23 +488,25 @@ def run_gpu_arm(args):
                        "replicas": reps, "parallelism": f"row-shard x{world} (fused 3-row P2P halo per step: peer stores + device handshake)" if world > 1
                        else "single GPU", "l2": "inputs larger than L2 (resident state >> 126 MB; no flush)"},
             "cell_updates_per_s": w * h * reps * args.steps / (ms / 1e3),
-            "hbm_gbs_alg_step": bytes_step * args.steps / (ms / 1e3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "frac_of_8tbs_spec": achieved / 8000.0,
+            "roofline": {"bound": "hbm", "achieved": rl["survey"]["achieved"], "peak": peak, "unit": "GB/s",
+                         "frac": rl["survey"]["frac"], "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": rl["survey"]["alg_bytes_per_launch"], "alg_bytes_model": SURVEY_MODEL,
                          "kernel": "step_bits_kernel", "kernel_ms": kernel_ms,
                          "kernel_ms_isolated_launch_events": kernel_ms_isolated,
-                         "alg_bytes_per_launch": bytes_launch,
-                         "alg_bytes_model": ALG_MODEL},
+                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                           "(profiles/ncu_traffic.json, captured at step 150 of the same workload)",
+                         "note": "frac > 1 on the §8(d) model: it counts 8 B/cell of word-plane traffic that the "
+                                 "in-place word plane does not stream (DESIGN.md §2); bitplane below counts the "
+                                 "bytes actually moved, which ncu's DRAM traffic matches"},
+            "roofline_bitplane": {"achieved": rl["bitplane"]["achieved"], "peak": peak, "unit": "GB/s",
+                                  "frac": rl["bitplane"]["frac"], "frac_of_8tbs_spec": rl["bitplane"]["achieved"] / 8000.0,
+                                  "alg_bytes_per_launch": rl["bitplane"]["alg_bytes_per_launch"],
+                                  "alg_bytes_model": BITPLANE_MODEL, "movers_per_step": movers},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "setup_s": setup_s,
             "moved_in_window_rank0": moved_local,
         }
-        if achieved > peak:
-            line["roofline"]["peak_note"] = ("achieved exceeds the driver's measured peak, a torch copy_ of 2 GiB "
-                                             "(MEASURED_PEAKS.json 'how'), which is not the HBM ceiling; "
-                                             "frac_of_8tbs_spec is the fraction of the B200 spec bandwidth")
         if e2e:
             line["e2e"] = e2e
     if dist is not None:
@@ -407,7 +515,9 @@ def run_gpu_arm(args):
         if world == 1 and not args.no_cpu_baseline:
             r = cpu_reference_run(args.workload, args.cpu_steps, 0, args.cpu_budget)
             line["cpu_baseline"] = {"value": r["value"], "unit": "agent-updates/s", "cores": r["cores"],
-                                    "kind": r["kind"], "sample": r["sample"]}
+                                    "kind": r["kind"], "sample": r["sample"], "cpu_model": r["cpu_model"]}
+            if "sequential" in r:
+                line["cpu_baseline"]["sequential"] = r["sequential"]
         if world == 1 and not args.no_secondary:
             line["secondary"] = secondary_runs(1000)
         print(json.dumps(line), flush=True)
@@ -415,31 +525,74 @@ def run_gpu_arm(args):
         dist.destroy_process_group()
 
 
-def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
-    """Same metric through the reference-facing API with HOST buffers: upload a
-    host SimState (pf_load_state), K steps with reports read back to the host,
-    download the SimState (pf_store_state) — all inside the timed region."""
-    import numpy as np
+def cpp_step_loop(args, cfg):
+    """The C++ drop-in (include/pedflow_gpu.hpp) as the reference's own
+    run_scenario loop calls it: `report = engine.step(state)` K times
+    (src/engine.cpp:216-221) on a reference-layout SimState of pageable
+    std::vectors, then state.sync(). The state stays on the device between
+    calls; the timed region holds the upload, K steps each with its 16-byte
+    report read back, and the download (tools/pedflow_gpu_demo, mode step)."""
+    demo = os.path.join(ROOT, "tools", "pedflow_gpu_demo")
+    model = "lem" if int(cfg.model) == 0 else "aco"
+    r = subprocess.run([demo, model, str(cfg.width), str(cfg.height), str(cfg.agents_per_side), str(args.steps),
+                        "42", "step"], capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        raise RuntimeError(f"pedflow_gpu_demo failed: {r.stderr[-500:]}")
+    return json.loads(r.stderr.strip().splitlines()[-1])
 
+
+def e2e_runs(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
+    """The same metric with host buffers, host<->device copies inside the
+    timed region. Headline (N=1): the C++ drop-in per-step loop on pageable
+    planes (cpp_step_loop). Beside it the C-ABI batch path (pf_load_state ->
+    pf_step(K) with reports -> pf_store_state) on page-locked and on pageable
+    numpy planes. At N>1 each rank runs the C-ABI path on its row shard."""
+    aco = cfg.model == 1
+    H, W = cfg.height, cfg.width
+    planes = H * W * (1 + 4 + (16 if aco else 0)) + 2 * cfg.agents_per_side * 40
+    agents = 2 * cfg.agents_per_side
+    variants = {}
+    if world == 1:
+        if rank == 0:
+            t = cpp_step_loop(args, cfg)
+            variants["cpp_step_loop_pageable"] = {
+                "value": agents * args.steps / t["run_s"], "seconds": t["run_s"], "setup_s": t["setup_s"],
+                "uploads": t["uploads"], "downloads": t["downloads"],
+                "path": "C++ shim: engine.step(state) x K (lazy, state stays on device) + state.sync(); "
+                        "std::vector planes"}
+        for pinned in (True, False):
+            secs = capi_batch(args, cfg, rank, world, local, barrier, max_over_ranks, pinned)
+            variants["capi_batch_" + ("pinned" if pinned else "pageable")] = {
+                "value": agents * args.steps / secs, "seconds": secs,
+                "path": "pf_load_state -> pf_step(K) (+reports) -> pf_store_state, "
+                        + ("page-locked numpy planes (pf_host_alloc)" if pinned else "pageable numpy planes")}
+        head = variants["cpp_step_loop_pageable"]
+    else:
+        from paper_1412_4933_b200.sharding import row_partition
+
+        secs = capi_batch(args, cfg, rank, world, local, barrier, max_over_ranks, False)
+        lo, hi = row_partition(H, world)[rank]
+        head = {"value": agents * args.steps / secs, "seconds": secs,
+                "path": "per rank: pf_load_state -> pf_step_async(K) -> reports -> pf_store_state of its row shard, "
+                        "pageable planes"}
+        variants["capi_sharded_pageable"] = head
+    return {"value": head["value"], "unit": "agent-updates/s",
+            "h2d_bytes_per_step": planes // args.steps, "d2h_bytes_per_step": planes // args.steps + 16,
+            "seconds": head["seconds"], "path": head["path"], "steps": args.steps,
+            "note": "transfer-bound at small K: about 2 x %.1f GB of reference-layout planes per run" % (planes / 1e9),
+            "variants": variants}
+
+
+def capi_batch(args, cfg, rank, world, local, barrier, max_over_ranks, pinned):
     import paper_1412_4933_b200 as p
     from paper_1412_4933_b200 import _lib
     from paper_1412_4933_b200.engine import _pf_config
     from paper_1412_4933_b200.sharding import row_partition
 
-    # Host planes in the reference layout, page-locked at N=1 (direct DMA). Each
-    # rank holds the whole grid's planes, so at N>1 they stay pageable (8 ranks
-    # x 7.6 GB of pinned memory at C5 is more than a host should lock).
-    state = p.new_environment(cfg, 42, pinned=world == 1)
+    state = p.new_environment(cfg, 42, pinned=pinned)
     lo, hi = row_partition(cfg.height, world)[rank]
     c = _lib.Context(_pf_config(cfg, 42, row_begin=0 if world == 1 else lo, row_end=0 if world == 1 else hi,
                                 device=local))
-    aco = cfg.model == p.Model.Aco
-    H, W = cfg.height, cfg.width
-    rows = (min(H, hi + 3) - max(0, lo - 3))
-    h2d = rows * W * (1 + 4 + (16 if aco else 0)) + len(state.agents) * 40
-    d2h = (hi - lo) * W * (1 + 4 + (16 if aco else 0)) + len(state.agents) * 40 + 16 * args.steps
-    import torch
-
     if world > 1:  # fused halo exchange between the ranks' contexts (CUDA IPC, device handshake)
         import torch.distributed as dist
 
@@ -448,7 +601,6 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
         for side, peer in ((0, rank - 1), (1, rank + 1)):
             if 0 <= peer < world:
                 c.attach_peer(side, _lib.PfPeerDesc.from_buffer_copy(descs[peer]), ipc=True)
-
     barrier()
     t0 = time.perf_counter()
     c.load(0, state.occupancy, state.index, state.agents, state.pheromone_top, state.pheromone_bottom, 0)
@@ -462,11 +614,8 @@ def e2e_run(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
     secs = max_over_ranks(time.perf_counter() - t0)
     barrier()  # fused exchange: no rank frees its planes while a neighbour may still store into them
     c.close()
-    del rep
-    return {"value": 2 * cfg.agents_per_side * args.steps / secs, "unit": "agent-updates/s",
-            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-            "seconds": secs, "path": "pf_load_state -> pf_step(K) (+reports) -> pf_store_state, "
-                    + ("pinned host planes (pf_host_alloc)" if world == 1 else "pageable host planes (staged)")}
+    del rep, state
+    return secs
 
 
 def main():

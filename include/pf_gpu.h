@@ -148,6 +148,10 @@ int pf_store_scores(pf_ctx* ctx, int32_t replica, double* scores, uint32_t* owne
  * on the device in a ring of the last 1024 steps; pf_read_reports
  * (synchronizes) returns those of steps [step - n, step) as [replicas][n]. */
 int pf_step_async(pf_ctx* ctx, uint32_t n);
+/* Capture and instantiate (without launching) the CUDA graphs that
+ * pf_step_async(n) / pf_step(n) will replay from the current step, so a timed
+ * region does not include graph capture. Optional. */
+int pf_prepare_steps(pf_ctx* ctx, uint32_t n);
 int pf_read_reports(pf_ctx* ctx, pf_step_report* out, uint32_t n);
 int pf_synchronize(pf_ctx* ctx);
 

@@ -212,6 +212,7 @@ class Reference:
             lib.ref_create.argtypes = [C.POINTER(_Cfg), C.c_int]
             lib.ref_destroy.argtypes = [vp]
             lib.ref_step.argtypes = [vp, u32, vp, C.POINTER(d)]
+            lib.ref_set_executor.argtypes = [vp, C.c_int]
             lib.ref_agent_count.restype = u32
             lib.ref_agent_count.argtypes = [vp]
             lib.ref_export.argtypes = [vp, vp, vp, vp, vp, vp, vp]
@@ -248,6 +249,11 @@ class Reference:
         if rc:
             raise RuntimeError(self.lib().ref_last_error().decode())
         return rep, secs.value
+
+    def set_executor(self, threads: int) -> None:
+        """Sequential (threads <= 0) or Parallel(threads), same state."""
+        if self.lib().ref_set_executor(self._h, int(threads)):
+            raise RuntimeError(self.lib().ref_last_error().decode())
 
     def export(self):
         H, W = self.sc.height, self.sc.width

@@ -77,6 +77,26 @@ void* ref_create(const ref_cfg* c, int threads) {
 
 void ref_destroy(void* p) { delete static_cast<RefHandle*>(p); }
 
+// Switches the executor of an existing handle (threads <= 0: Sequential,
+// else Parallel with that many threads) by rebuilding its StepEngine from the
+// config (EngineOptions::from_config, src/engine.cpp:35-46); the SimState and
+// its step counter are kept, so Sequential and Parallel can be timed on one
+// placement (the reference's `bench` compares the two executors the same way,
+// tools/pedflow.cpp:191-225).
+int ref_set_executor(void* p, int threads) {
+    try {
+        auto* h = static_cast<RefHandle*>(p);
+        h->cfg.executor = threads > 0 ? pedflow::ExecutorKind::Parallel : pedflow::ExecutorKind::Sequential;
+        h->cfg.threads = threads > 0 ? threads : 0;
+        pedflow::EngineOptions opt = pedflow::EngineOptions::from_config(h->cfg, h->cfg.seed);
+        h->engine = std::make_unique<pedflow::StepEngine>(std::move(opt));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
 // Runs n steps; reports is n*4 u32 (StepReport layout) or null. *seconds gets
 // the wall time of the step loop alone.
 int ref_step(void* p, uint32_t n, uint32_t* reports, double* seconds) {

@@ -106,6 +106,7 @@ _sigs = {
     "pf_store_state": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _u32, _vp, _vp, C.POINTER(_u32)]),
     "pf_step": (C.c_int, [_vp, _u32, _vp]),
     "pf_step_async": (C.c_int, [_vp, _u32]),
+    "pf_prepare_steps": (C.c_int, [_vp, _u32]),
     "pf_read_reports": (C.c_int, [_vp, _vp, _u32]),
     "pf_synchronize": (C.c_int, [_vp]),
     "pf_time_steps": (C.c_int, [_vp, _u32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
@@ -194,11 +195,41 @@ class Context:
     def init_environment(self):
         check(lib.pf_init_environment(self.h))
 
+    def _check_planes(self, replica, occ, index, agents, tau_top, tau_bot, need_all: bool):
+        """The C-ABI reads/writes width*height cells per plane and the whole
+        agent table through raw pointers: reject anything that does not match
+        this context's grid instead of letting it run out of bounds."""
+        if not 0 <= int(replica) < self.replicas:
+            raise ConfigError(f"replica {replica} out of range [0, {self.replicas})")
+        shape = (int(self.cfg.height), int(self.cfg.width))
+        planes = [("occupancy", occ, np.uint8), ("index", index, np.uint32)]
+        if self.aco:
+            planes += [("pheromone_top", tau_top, np.float64), ("pheromone_bottom", tau_bot, np.float64)]
+        elif tau_top is not None or tau_bot is not None:
+            raise ConfigError("pheromone planes given for a LEM context")
+        for name, a, dt in planes:
+            if a is None:
+                if need_all:
+                    raise ConfigError(f"{name} plane missing")
+                continue
+            if not isinstance(a, np.ndarray) or a.dtype != dt or a.shape != shape or not a.flags.c_contiguous:
+                got = (type(a).__name__, getattr(a, "dtype", None), getattr(a, "shape", None))
+                raise ConfigError(f"{name} must be a C-contiguous {np.dtype(dt).name} array of shape {shape}, got {got}")
+            if not need_all and not a.flags.writeable:
+                raise ConfigError(f"{name} is read-only")
+        n = 2 * self.replica_agents(replica)
+        if (not isinstance(agents, np.ndarray) or agents.dtype != AGENT_DTYPE or agents.ndim != 1
+                or not agents.flags.c_contiguous or len(agents) != n):
+            raise ConfigError(f"agents must be a C-contiguous AgentRecord array of length {n}, got "
+                              f"{getattr(agents, 'dtype', type(agents).__name__)} x {getattr(agents, 'shape', None)}")
+
     def load(self, replica, occ, index, agents, tau_top, tau_bot, step):
+        self._check_planes(replica, occ, index, agents, tau_top, tau_bot, need_all=True)
         check(lib.pf_load_state(self.h, replica, ptr(occ), ptr(index), ptr(agents) if len(agents) else None,
                                 len(agents), ptr(tau_top), ptr(tau_bot), step))
 
     def store(self, replica, occ, index, agents, tau_top, tau_bot) -> int:
+        self._check_planes(replica, occ, index, agents, tau_top, tau_bot, need_all=False)
         step = C.c_uint32(0)
         check(lib.pf_store_state(self.h, replica, ptr(occ), ptr(index), ptr(agents) if len(agents) else None,
                                  len(agents), ptr(tau_top), ptr(tau_bot), C.byref(step)))
@@ -211,6 +242,10 @@ class Context:
 
     def step_async(self, n: int):
         check(lib.pf_step_async(self.h, n))
+
+    def prepare_steps(self, n: int):
+        """Instantiate the CUDA graphs step_async(n) will replay (no launch)."""
+        check(lib.pf_prepare_steps(self.h, n))
 
     def read_reports(self, n: int) -> np.ndarray:
         out = np.zeros((self.replicas, n), REPORT_DTYPE)

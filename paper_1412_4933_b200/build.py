@@ -65,7 +65,7 @@ def build_demo(force: bool = False) -> str:
     if not os.path.exists(src):
         return ""
     if force or _stale(out, [src, hdr, LIB]):
-        _run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), "-o", out, src,
+        _run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-o", out, src,
               f"-L{PKG}", "-lpedflow_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../paper_1412_4933_b200"])
     return out
 

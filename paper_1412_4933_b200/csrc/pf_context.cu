@@ -487,13 +487,18 @@ static void build_occ(pf_ctx* ctx, int rep) {
 
 // Fused kernel: zero the stale words of vacated cells (empty in the current
 // planes) so the word plane is the exact cell-word state; *bad counts agent
-// cells whose word disagrees with the planes.
+// cells whose word disagrees with the planes. Owned rows only: on a linked
+// row shard the neighbour's step kernel may still be storing words and plane
+// bits into this shard's ghost rows (its stream is not ordered with ours), and
+// every reader (export, audit) reads owned rows only.
 static void sanitize_words(pf_ctx* ctx, int rep, unsigned long long* bad) {
     pfk::Planes& P = ctx->args.p;
     if (!ctx->bits()) return;
-    ctx->launches += pfk::launch_sanitize_words(P.cell[0] + size_t(rep) * ctx->plane(),
-                                                P.occ[ctx->parity] + size_t(rep) * P.occ_plane, ctx->cfg.width,
-                                                ctx->rows_buf, P.wsp, bad, ctx->stream);
+    const size_t W = size_t(ctx->cfg.width);
+    ctx->launches += pfk::launch_sanitize_words(
+        P.cell[0] + size_t(rep) * ctx->plane() + size_t(pfk::kGhost) * W,
+        P.occ[ctx->parity] + size_t(rep) * P.occ_plane + size_t(pfk::kGhost) * P.wsp, ctx->cfg.width,
+        ctx->rows_owned, P.wsp, bad, ctx->stream);
 }
 
 // Copy between aliased planes is a no-op.
@@ -896,23 +901,46 @@ static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
     return PF_OK;
 }
 
-static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
-    if (int rc = zero_reports(ctx, ctx->step, n)) return rc;
-    const auto key = std::make_pair(n, ctx->parity);
+// The cached graph of n steps starting at the given parity (captured and
+// instantiated on first use).
+static int batch_graph(pf_ctx* ctx, uint32_t n, int parity, cudaGraphExec_t* out) {
+    const auto key = std::make_pair(n, parity);
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
         const uint64_t before = ctx->launches;
         PF_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_direct(ctx, n, ctx->parity);
+        enqueue_direct(ctx, n, parity);
         PF_CUDA(cudaStreamEndCapture(ctx->stream, &g));
         ctx->launches = before;  // counted when replayed
         PF_CUDA(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
         it = ctx->graphs.emplace(key, ge).first;
     }
-    PF_CUDA(cudaGraphLaunch(it->second, ctx->stream));
+    *out = it->second;
+    return PF_OK;
+}
+
+int pf_prepare_steps(pf_ctx* ctx, uint32_t n) {
+    if (!ctx) return fail(PF_ERR_ARG, "null ctx");
+    PF_CUDA(cudaSetDevice(ctx->cfg.device));
+    int parity = ctx->parity;
+    while (n > 0) {
+        const uint32_t m = std::min<uint32_t>(n, kBatchCap);
+        cudaGraphExec_t ge = nullptr;
+        if (int rc = batch_graph(ctx, m, parity, &ge)) return rc;
+        parity ^= int(m & 1u);
+        n -= m;
+    }
+    return PF_OK;
+}
+
+static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
+    if (int rc = zero_reports(ctx, ctx->step, n)) return rc;
+    cudaGraphExec_t ge = nullptr;
+    if (int rc = batch_graph(ctx, n, ctx->parity, &ge)) return rc;
+    PF_CUDA(cudaGraphLaunch(ge, ctx->stream));
     const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1;
     ctx->launches += uint64_t(n) * per_step + 1;
     ctx->parity ^= int(n & 1u);

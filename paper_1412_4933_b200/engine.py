@@ -19,7 +19,9 @@ when read.
 from __future__ import annotations
 
 import enum
+import itertools
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -126,6 +128,9 @@ class StepReport:
         return cls(int(r["step"]), int(r["moved"]), int(r["newly_crossed_top"]), int(r["newly_crossed_bottom"]))
 
 
+_STATE_TOKENS = itertools.count(1)
+
+
 class SimState:
     """pedflow::SimState (inc/state.hpp:16-31): occupancy, index, agents,
     pheromone (ACO), step. Planes are numpy arrays in the reference's layout
@@ -150,7 +155,8 @@ class SimState:
         self._scores = np.zeros((n_agents, 8), np.float64)  # CandidateScores::score by agent id
         self._step = 0
         self._device = None  # (engine, replica) holding a newer copy
-        self._version = 0    # bumped on host-side modification
+        self._version = 0    # bumped whenever the host planes change (touch, download)
+        self._token = next(_STATE_TOKENS)  # never reused (unlike id())
 
     # --- lazy sync -----------------------------------------------------
     def _pull(self):
@@ -284,7 +290,8 @@ class StepEngine:
         self._opt = opt
         self._ctx: _lib.Context | None = None
         self._dims = None
-        self._bound = None  # (state id, version) resident on the device
+        self._bound = None  # (state token, version) the device copy equals
+        self._resident = None  # weakref to the state whose newest copy is on the device
 
     def options(self) -> EngineOptions:
         return self._opt
@@ -298,11 +305,18 @@ class StepEngine:
     def _attach(self, state: SimState):
         if state._device is not None and state._device[0] is self:
             return  # already resident and newer on the device
-        state._pull()
-        if self._ctx is not None and self._bound == (id(state), state._version):
+        state._pull()  # newer on another engine: bring it home first (bumps _version)
+        if self._ctx is not None and self._bound == (state._token, state._version):
+            self._resident = weakref.ref(state)
             return  # the device copy equals the host planes
         if Model(state.model) != Model(self._opt.model):
             raise ConfigError("state model disagrees with engine options")
+        # Another state's newest copy lives here: download it before its planes
+        # are overwritten (the reference's step(SimState&) accepts any state).
+        other = self._resident() if self._resident is not None else None
+        if other is not None and other is not state and other._device is not None and other._device[0] is self:
+            other._pull()
+        self._resident = None
         dims = (state.width, state.height, len(state._agents))
         if self._ctx is None or self._dims != dims:
             if self._ctx is not None:
@@ -311,14 +325,18 @@ class StepEngine:
             self._ctx = _lib.Context(_pf_config(sc, self._opt.seed, device=self._opt.device, kernel=self._opt.kernel))
             self._dims = dims
         self._ctx.load(0, state._occ, state._index, state._agents, state._tau_top, state._tau_bot, state._step)
-        self._bound = (id(state), state._version)
+        self._bound = (state._token, state._version)
+        self._resident = weakref.ref(state)
 
     def _download(self, state: SimState, rep: int):
         # planes are written in place by the library
         state._step = self._ctx.store(rep, state._occ, state._index, state._agents, state._tau_top, state._tau_bot)
         if len(state._agents):
             self._ctx.store_scores(rep, state._scores)
-        self._bound = (id(state), state._version)
+        # The host planes changed: every other engine's copy of this state is
+        # now stale; this engine's copy equals the new planes.
+        state._version += 1
+        self._bound = (state._token, state._version)
 
     # --- phase-level stepping (src/engine.cpp:64-193) ------------------------
     def _phase(self, state: SimState, phase: int):
@@ -369,6 +387,11 @@ class StepEngine:
         return self._ctx
 
     def close(self):
+        other = self._resident() if self._resident is not None else None
+        if other is not None and other._device is not None and other._device[0] is self:
+            other._pull()  # the state must outlive the device copy it depends on
+        self._resident = None
+        self._bound = None
         if self._ctx is not None:
             self._ctx.close()
             self._ctx = None

@@ -18,7 +18,7 @@ its hex hashes use a byte layout the survey does not fully specify, so the
 hashes here are regenerated with the definition above.
 
 Usage (build container only; needs /root/reference):
-    python tests/golden/make_golden.py [--big]
+    python tests/golden/make_golden.py [--big | --c5-long]
 """
 from __future__ import annotations
 
@@ -92,14 +92,57 @@ def run_one(name, kw, steps, survey, threads):
     return entry
 
 
+# Long C5 horizons with checkpoints: one reference run per model, hashed at each
+# checkpoint (the bench window and the sharded tests sit inside them).
+C5_LONG = {
+    "C5_aco_long": dict(width=16384, height=16384, agents_per_side=25_000_000, model="aco"),
+    "C5_lem_long": dict(width=16384, height=16384, agents_per_side=25_000_000, model="lem"),
+}
+C5_CHECKPOINTS = (10, 30, 100, 300)
+
+
+def run_long(name, kw, checkpoints, threads):
+    sc = Scenario(**kw)
+    t0 = time.time()
+    ref = Reference(sc, threads=threads)
+    print(f"{name}: setup {time.time() - t0:.1f}s", flush=True)
+    reps, cps, done = [], {}, 0
+    for cp in checkpoints:
+        rep, secs = ref.run(cp - done)
+        reps.append(rep)
+        done = cp
+        h = ref.hashes()
+        cps[str(cp)] = {k: f"{v:016x}" for k, v in h.items()}
+        print(f"{name}: step {cp} ({secs:.1f}s) {cps[str(cp)]}", flush=True)
+    import numpy as np
+
+    rep = np.concatenate(reps)
+    return {
+        "scenario": kw,
+        "steps": done,
+        "checkpoints": cps,
+        "series": rep.view("<u4").reshape(-1, 4)[:, 1:].tolist(),
+        "series_hash": f"{series_hash(rep):016x}",
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also anchor C5 (needs ~14 GB RAM, ~2 min)")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--c5-long", action="store_true",
+                    help="only the C5 checkpointed anchors (steps %s; ~1 h on 8 cores)" % (C5_CHECKPOINTS,))
     args = ap.parse_args()
     path = os.path.join(HERE, "anchors.json")
     old = json.load(open(path)) if os.path.exists(path) else {}
     out = dict(old)
+    if args.c5_long:
+        for name, kw in C5_LONG.items():
+            out[name] = run_long(name, kw, C5_CHECKPOINTS, args.threads)
+            with open(path, "w") as f:
+                json.dump(out, f, indent=1, sort_keys=True)
+        print("wrote", path)
+        return
     todo = dict(CONFIGS)
     if args.big:
         todo.update(BIG)

@@ -160,18 +160,6 @@ def test_corrupt_state_rejected():
         eng.step(s)
 
 
-@pytest.mark.parametrize("name", ["C5_aco_16384_25M", "C5_lem_16384_25M"])
-def test_c5_full_grid_anchor(anchors, name):
-    """The 16384 x 16384, 50M-agent grid (BASELINE C5) for its first 3 steps,
-    against the reference's own run (hashes over every plane)."""
-    if name not in anchors:
-        pytest.skip("C5 anchors not generated (make_golden.py --big)")
-    a = anchors[name]
-    state, rep = _run_gpu(a["scenario"], a["steps"])
-    assert int(rep["moved"].astype(np.int64).sum()) == a["sum_moved"]
-    assert hex_hashes(hashes_of(state)) == a["hash"]
-
-
 def _oracle_select(lib, kind, mask, num, seed, step, ent, d0=2.0, mu=1.0, sigma=0.5):
     """The oracle's lem_select / aco_select (goal-relative slot, -1 stay) or
     the movement-phase winner draw (src/engine.cpp:116-120) for one key."""

@@ -25,16 +25,27 @@ def test_demo_reports_config_error():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["batch", "step", "interleave"])
 @pytest.mark.parametrize("name", ["C1_lem_480_1024", "C2_aco_480_1024", "s96_aco_900_s11", "r48x32_aco_300_s9"])
-def test_cpp_dropin_matches_golden(anchors, name):
+def test_cpp_dropin_matches_golden(anchors, name, mode):
+    """batch: step_n; step: the reference's per-step `engine.step(state)` loop
+    (src/engine.cpp:216-221) with the state kept on the device between calls
+    (one upload, one download); interleave: the same with a second state on
+    the same engine, a snapshot copy and a second engine taking over, which
+    must all sync lazily without losing or repeating a step."""
+    import json
+
     a = anchors[name]
     sc = a["scenario"]
     r = subprocess.run([DEMO, sc["model"], str(sc["width"]), str(sc["height"]), str(sc["agents_per_side"]),
-                        str(a["steps"]), str(sc.get("seed", 42))], capture_output=True, text=True, timeout=300)
+                        str(a["steps"]), str(sc.get("seed", 42)), mode], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     moved, top, bot, h_index, h_occ = r.stdout.split()
     assert (int(moved), int(top), int(bot)) == (a["sum_moved"], a["crossed_top"], a["crossed_bottom"])
     assert (h_index, h_occ) == (a["hash"]["index"], a["hash"]["occ"])
+    t = json.loads(r.stderr.strip().splitlines()[-1])
+    if mode in ("batch", "step"):
+        assert (t["uploads"], t["downloads"]) == (1, 1)  # lazy: no per-step round trip
 
 
 @pytest.mark.gpu
