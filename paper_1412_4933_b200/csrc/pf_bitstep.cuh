@@ -131,9 +131,10 @@ struct Smem {
     uint32_t qu[NU];  // unit
     uint32_t qm[NU];  // its bits
     uint32_t qp[NU];  // rank of its first bit
-    // S3: per warp, the words (and ACO tours) at the sources of its row's
-    // arrivals, fetched for all segments at once by cp.async.
+    // S3: per warp, the words (and ACO tours, then deposits) at the sources
+    // of its row's arrivals, by arrival, fetched at once by cp.async.
     uint32_t asw[NW][NS][32];
+    uint16_t alist[NW][NS * 32];  // S3: the row's arrivals (column | direction code << 12), per warp
     unsigned long long mbar[2];
     uint32_t qc[2][2];  // [tile parity][0: S1 draws, 1: S2 contested cells]
     // Next work item. Double-buffered by the parity of the item that claims it:
@@ -551,7 +552,10 @@ __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int r
     __threadfence_system();
 }
 
-template <bool ACO, int CTAS, bool MIRROR>
+// COMPACT: S3 per-arrival work on compacted arrival lists (dense, batched
+// 480^2 grids: C4 x64 -6.4%); off for large grids, where arrivals are sparse
+// and the per-segment form is 1-2% faster.
+template <bool ACO, int CTAS, bool MIRROR, bool COMPACT>
 __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -832,76 +836,172 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 for (int s = 0; s < NS; ++s)
                     tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
             }
-            // The sources of this row's arrivals: all their loads are in
-            // flight together (one round trip per row, not one per segment).
-            // Each source is occupied at step start, so nothing writes it.
-#pragma unroll
-            for (int si = 1; si <= NS; ++si) {
-                if (bit(sm.A[ai][si], lane)) {
-                    const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                       bit(sm.K[2][ai][si], lane) << 2);
-                    const size_t src = size_t(b + kDR[kc]) * W + (c0 + 32 * (si - 1) + lane + kDC[kc]);
-                    cp_async<4>(&sm.asw[warp][si - 1][lane], cw + src);
-                    if (ACO) cp_async<8>(&sm.atr[warp][si - 1][lane], tour + src);
-                }
-            }
-            cp_async_wait_all();
-            __syncwarp();
-            uint2 mine = make_uint2(kWall, kWall);
-#pragma unroll
-            for (int si = 1; si <= NS; ++si) {
-                const int gc = c0 + 32 * (si - 1) + lane;
-                const bool valid = gc < W;
-                const uint32_t Am = sm.A[ai][si], Gm = sm.G[cur][rr][si];
-                uint2 np = sm.pl[rs][si + 1];
-                const size_t gi = row0 + 32 * (si - 1);
-                if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
-                    if (ACO && valid) {
-                        const double2 tt = tv[si - 1];
-                        tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+            if constexpr (COMPACT) {
+                // The row's arrivals, compacted: arrival e (column order) is lane
+                // e % 32's, so the per-arrival work (crossing, counters, tour,
+                // deposit) runs once per 32 arrivals instead of once per moving
+                // segment. alist[e]: its column in the strip | its direction code
+                // (row-major, from the winner planes) << 12. The sources of all
+                // of them are fetched at once (cp.async, one round trip per row)
+                // into asw[e] (word) / atr[e] (ACO tour, then the deposit q / tour);
+                // the segment pass below finds arrival e of a cell as the
+                // segment's first arrival + the arrivals to its left.
+                // Each source is occupied at step start and each destination empty
+                // at step start, so no other thread reads or writes these words.
+                uint16_t* const alist = sm.alist[warp];
+                uint32_t* const asw = &sm.asw[warp][0][0];
+                double* const atr = ACO ? &sm.atr[warp][0][0] : nullptr;
+                const uint32_t lt = (1u << lane) - 1u;
+                uint32_t na = 0;
+    #pragma unroll
+                for (int si = 1; si <= NS; ++si) {
+                    const uint32_t Am = sm.A[ai][si];
+                    if (bit(Am, lane)) {
+                        const uint32_t kc = bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
+                                            bit(sm.K[2][ai][si], lane) << 2;
+                        alist[na + __popc(Am & lt)] = uint16_t(kc << 12 | (32 * (si - 1) + lane));
                     }
-                } else {
-                    const bool arrived = bit(Am, lane) != 0u;
-                    uint32_t group = 0;
-                    double tour_new = 0.0;
-                    if (arrived) {
+                    na += __popc(Am);
+                }
+                __syncwarp();
+                for (uint32_t e = lane; e < na; e += 32) {
+                    const int cc = alist[e] & 0xFFF, kc = alist[e] >> 12;
+                    const size_t src = size_t(b + kDR[kc]) * W + (c0 + cc + kDC[kc]);
+                    cp_async<4>(asw + e, cw + src);
+                    if (ACO) cp_async<8>(atr + e, tour + src);
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                for (uint32_t e = lane; e < na; e += 32) {
+                    const int cc = alist[e] & 0xFFF, kc = alist[e] >> 12;
+                    const uint32_t sw = asw[e];
+                    const uint32_t group = sw >> 30;
+                    uint32_t nw = sw;
+                    if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
+                        nw |= kCrossedBit;
+                        if (group == 1u) ++ntop;
+                        else ++nbot;
+                    }
+                    ++moved;
+                    const size_t gi = size_t(b) * W + c0 + cc;
+                    cw[gi] = nw;
+                    if (ACO) {  // tour += 1 or sqrt(2) (src/engine.cpp:159-160); deposit q / tour (src/aco.cpp:119-123)
+                        const double tour_new = __dadd_rn(atr[e], is_diag(kc) ? a.k.diag : 1.0);
+                        tour[gi] = tour_new;
+                        atr[e] = __ddiv_rn(a.k.q, tour_new);
+                    }
+                }
+                __syncwarp();
+                uint2 mine = make_uint2(kWall, kWall);
+                uint32_t e0 = 0;  // arrivals in the segments left of si
+    #pragma unroll
+                for (int si = 1; si <= NS; ++si) {
+                    const int gc = c0 + 32 * (si - 1) + lane;
+                    const bool valid = gc < W;
+                    const uint32_t Am = sm.A[ai][si], Gm = sm.G[cur][rr][si];
+                    uint2 np = sm.pl[rs][si + 1];
+                    const size_t gi = row0 + 32 * (si - 1);
+                    const uint32_t ea = e0 + __popc(Am & lt);
+                    e0 += __popc(Am);
+                    if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
+                        if (ACO && valid) {
+                            const double2 tt = tv[si - 1];
+                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+                        }
+                    } else {
+                        const bool arrived = bit(Am, lane) != 0u;
+                        const uint32_t group = arrived ? asw[ea] >> 30 : 0u;
+                        const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
+                        np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
+                        np.y = (np.y & ~Gm) | (Am & ~top);
+                        if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
+                            double2 tt = tv[si - 1];
+                            tt.x = __dmul_rn(tt.x, a.k.factor);
+                            tt.y = __dmul_rn(tt.y, a.k.factor);
+                            if (arrived) {
+                                const double dep = atr[ea];
+                                if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
+                                else tt.y = __dadd_rn(tt.y, dep);
+                            }
+                            tout[gi] = tt;
+                        }
+                    }
+                    if (lane == si - 1) mine = np;
+                }
+                if (lane < NS) orow[lane] = mine;
+            } else {
+                // Sparse arrivals (large grids): per segment, lane = column.
+                // The sources of this row's arrivals: all their loads are in
+                // flight together (one round trip per row, not one per segment).
+                // Each source is occupied at step start, so nothing writes it.
+    #pragma unroll
+                for (int si = 1; si <= NS; ++si) {
+                    if (bit(sm.A[ai][si], lane)) {
                         const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
                                            bit(sm.K[2][ai][si], lane) << 2);
-                        const uint32_t sw = sm.asw[warp][si - 1][lane];
-                        group = sw >> 30;
-                        uint32_t nw = sw;
-                        if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
-                            nw |= kCrossedBit;
-                            if (group == 1u) ++ntop;
-                            else ++nbot;
-                        }
-                        ++moved;
-                        cw[gi] = nw;  // empty at step start: nobody reads it this step
-                        if (ACO) {    // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
-                            tour_new = __dadd_rn(sm.atr[warp][si - 1][lane], is_diag(kc) ? a.k.diag : 1.0);
-                            tour[gi] = tour_new;
-                        }
-
-                    }
-                    const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
-                    const uint32_t bot = __ballot_sync(0xFFFFFFFFu, group == 2u);
-                    np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
-                    np.y = (np.y & ~Gm) | bot;
-                    if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
-                        double2 tt = tv[si - 1];
-                        tt.x = __dmul_rn(tt.x, a.k.factor);
-                        tt.y = __dmul_rn(tt.y, a.k.factor);
-                        if (arrived) {
-                            const double dep = __ddiv_rn(a.k.q, tour_new);
-                            if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
-                            else tt.y = __dadd_rn(tt.y, dep);
-                        }
-                        tout[gi] = tt;
+                        const size_t src = size_t(b + kDR[kc]) * W + (c0 + 32 * (si - 1) + lane + kDC[kc]);
+                        cp_async<4>(&sm.asw[warp][si - 1][lane], cw + src);
+                        if (ACO) cp_async<8>(&sm.atr[warp][si - 1][lane], tour + src);
                     }
                 }
-                if (lane == si - 1) mine = np;
+                cp_async_wait_all();
+                __syncwarp();
+                uint2 mine = make_uint2(kWall, kWall);
+    #pragma unroll
+                for (int si = 1; si <= NS; ++si) {
+                    const int gc = c0 + 32 * (si - 1) + lane;
+                    const bool valid = gc < W;
+                    const uint32_t Am = sm.A[ai][si], Gm = sm.G[cur][rr][si];
+                    uint2 np = sm.pl[rs][si + 1];
+                    const size_t gi = row0 + 32 * (si - 1);
+                    if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
+                        if (ACO && valid) {
+                            const double2 tt = tv[si - 1];
+                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+                        }
+                    } else {
+                        const bool arrived = bit(Am, lane) != 0u;
+                        uint32_t group = 0;
+                        double tour_new = 0.0;
+                        if (arrived) {
+                            const int kc = int(bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
+                                               bit(sm.K[2][ai][si], lane) << 2);
+                            const uint32_t sw = sm.asw[warp][si - 1][lane];
+                            group = sw >> 30;
+                            uint32_t nw = sw;
+                            if (!(sw & kCrossedBit) && crossed_at(group, grow, a.k.H, band)) {  // src/engine.cpp:163-170
+                                nw |= kCrossedBit;
+                                if (group == 1u) ++ntop;
+                                else ++nbot;
+                            }
+                            ++moved;
+                            cw[gi] = nw;  // empty at step start: nobody reads it this step
+                            if (ACO) {    // tour += 1 or sqrt(2) (src/engine.cpp:159-160)
+                                tour_new = __dadd_rn(sm.atr[warp][si - 1][lane], is_diag(kc) ? a.k.diag : 1.0);
+                                tour[gi] = tour_new;
+                            }
+
+                        }
+                        const uint32_t top = __ballot_sync(0xFFFFFFFFu, group == 1u);
+                        const uint32_t bot = __ballot_sync(0xFFFFFFFFu, group == 2u);
+                        np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
+                        np.y = (np.y & ~Gm) | bot;
+                        if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
+                            double2 tt = tv[si - 1];
+                            tt.x = __dmul_rn(tt.x, a.k.factor);
+                            tt.y = __dmul_rn(tt.y, a.k.factor);
+                            if (arrived) {
+                                const double dep = __ddiv_rn(a.k.q, tour_new);
+                                if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
+                                else tt.y = __dadd_rn(tt.y, dep);
+                            }
+                            tout[gi] = tt;
+                        }
+                    }
+                    if (lane == si - 1) mine = np;
+                }
+                if (lane < NS) orow[lane] = mine;
             }
-            if (lane < NS) orow[lane] = mine;
         }
         __syncthreads();  // end of tile: the window's slots may be refilled
         if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, parity, rep, it.strip, r0);
@@ -961,11 +1061,11 @@ static_assert(kCtasLem >= 1 && kCtasDefault >= 1, "shared memory must fit one CT
 
 int configure() {
     const int lem = int(kSmemBytes[0]), aco = int(kSmemBytes[1]);
-    for (auto f : {step_bits_kernel<false, kCtasLem, false>, step_bits_kernel<false, kCtasLem, true>,
-                   step_bits_kernel<false, kCtasLemBig, false>, step_bits_kernel<false, kCtasLemBig, true>})
+    for (auto f : {step_bits_kernel<false, kCtasLem, false, true>, step_bits_kernel<false, kCtasLem, true, true>,
+                   step_bits_kernel<false, kCtasLemBig, false, false>, step_bits_kernel<false, kCtasLemBig, true, false>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lem) != cudaSuccess) return 1;
-    for (auto f : {step_bits_kernel<true, kCtasDefault, false>, step_bits_kernel<true, kCtasHbm, false>,
-                   step_bits_kernel<true, kCtasDefault, true>, step_bits_kernel<true, kCtasHbm, true>})
+    for (auto f : {step_bits_kernel<true, kCtasDefault, false, true>, step_bits_kernel<true, kCtasHbm, false, false>,
+                   step_bits_kernel<true, kCtasDefault, true, true>, step_bits_kernel<true, kCtasHbm, true, false>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, aco) != cudaSuccess) return 1;
     return 0;
 }
@@ -1011,17 +1111,17 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const size_t bytes = kSmemBytes[aco ? 1 : 0];
     const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
     if (!aco && big) {
-        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLemBig, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<false, kCtasLemBig, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLemBig, true, false>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLemBig, false, false>, grid, bytes, s, b, slot_idx, parity);
     } else if (!aco) {
-        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<false, kCtasLem, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLem, false, true>, grid, bytes, s, b, slot_idx, parity);
     } else if (hbm) {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasHbm, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true, false>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasHbm, false, false>, grid, bytes, s, b, slot_idx, parity);
     } else {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasDefault, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasDefault, false, true>, grid, bytes, s, b, slot_idx, parity);
     }
     return 1;
 }
