@@ -28,10 +28,11 @@ ap.add_argument("workloads", nargs="+")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--steps", type=int, default=100)
 ap.add_argument("--skip", type=int, default=0)
+ap.add_argument("--tags", default="base,new", help="tools/debug/lib_<tag>.so to compare (first = baseline)")
 args = ap.parse_args()
 res = {}
 for r in range(args.rounds):
-    for tag in ("base", "new"):
+    for tag in args.tags.split(","):
         env = dict(os.environ, PEDFLOW_B200_LIB=os.path.join(ROOT, "tools", "debug", f"lib_{tag}.so"))
         out = subprocess.run([sys.executable, "-c", CODE, str(args.steps), str(args.skip)] + args.workloads, env=env, cwd=ROOT,
                              capture_output=True, text=True).stdout
@@ -39,7 +40,11 @@ for r in range(args.rounds):
             if line.strip():
                 name, us = line.split()
                 res.setdefault((name, tag), []).append(float(us))
+tags = args.tags.split(",")
 for name in args.workloads:
-    b, n = min(res.get((name, "base"), [0])), min(res.get((name, "new"), [0]))
-    print(f"{name:12s} base {b:9.1f} us   new {n:9.1f} us   new/base {n / b if b else 0:.3f}   "
-          f"(all base {res.get((name, 'base'))}, new {res.get((name, 'new'))})")
+    b = min(res.get((name, tags[0]), [0]))
+    line = f"{name:12s} {tags[0]} {b:9.1f} us"
+    for t in tags[1:]:
+        n = min(res.get((name, t), [0]))
+        line += f"   {t} {n:9.1f} us ({n / b if b else 0:.3f})"
+    print(line)
