@@ -135,6 +135,12 @@ def _oracle_lib():
         lib.pfo_normal.argtypes = [u64, u32, u32, u64, u32, d, d]
         lib.pfo_inverse_normal_cdf.restype = d
         lib.pfo_inverse_normal_cdf.argtypes = [d]
+        lib.pfo_log_restated.restype = d
+        lib.pfo_log_restated.argtypes = [d]
+        lib.pfo_log_restated_matches_host.restype = C.c_int
+        lib.pfo_log_restated_matches_host.argtypes = [u32, u64]
+        lib.pfo_normal_batch.restype = None
+        lib.pfo_normal_batch.argtypes = [u32, vp, vp, vp, vp, vp, d, d, vp]
         lib.pfo_distance_table.argtypes = [d, vp]
         lib.pfo_band_height.restype = i32
         lib.pfo_band_height.argtypes = [i32, i32]

@@ -75,6 +75,53 @@ static const double kFarDen[8] = {2.04426310338993978564e-15, 1.4215117583164458
                                   1.48753612908506148525e-2, 1.36929880922735805310e-1,
                                   5.99832206555887937690e-1, 1.0};
 
+/* glibc's log, main path (sysdeps/ieee754/dbl-64/e_log.c, N = 128), in the
+ * order and with the FMA contractions of the -mfma build this image's libm
+ * dispatches to on FMA + AVX2 hosts (__log_fma, glibc 2.39). Constants:
+ * pf_glibc_log.h (tools/gen_log_table.py). */
+#include "pf_glibc_log.h"
+static const double kLogPoly[5] = PF_LOG_POLY_INIT;
+static const double kLogTab[128][2] = PF_LOG_TAB_INIT;
+
+double pfo_log_restated(double x) {
+    uint64_t ix;
+    memcpy(&ix, &x, 8);
+    const uint64_t top = ix >> 48;
+    if (ix - 0x3fee000000000000ULL < 0x3ff1090000000000ULL - 0x3fee000000000000ULL || top - 0x0010 >= 0x7ff0 - 0x0010)
+        return NAN; /* near 1, or zero / subnormal / negative / inf / nan: not restated */
+    const uint64_t tmp = ix - 0x3fe6000000000000ULL;
+    const int i = (int)((tmp >> 45) & 127);
+    const int k = (int)((int64_t)tmp >> 52);
+    const uint64_t iz = ix - (tmp & 0xfffULL << 52);
+    double z;
+    memcpy(&z, &iz, 8);
+    const double kd = (double)k;
+    const double w = fma(kd, PF_LOG_LN2HI, kLogTab[i][1]);
+    const double r = fma(z, kLogTab[i][0], -1.0);
+    const double p21 = fma(r, kLogPoly[2], kLogPoly[1]);
+    const double hi = r + w;
+    const double r2 = r * r;
+    double lo = (w - hi) + r;
+    lo = fma(kd, PF_LOG_LN2LO, lo);
+    const double r3 = r * r2;
+    double p43 = fma(r, kLogPoly[4], kLogPoly[3]);
+    lo = fma(r2, kLogPoly[0], lo);
+    p43 = fma(p43, r2, p21);
+    const double y = fma(r3, p43, lo);
+    return y + hi;
+}
+
+int pfo_log_restated_matches_host(uint32_t n, uint64_t seed) {
+    for (uint32_t j = 0; j < n; ++j) {
+        /* tail arguments of AS241: min(p, 1 - p) with p an open uniform, in (0, 0.075] */
+        const double u = ((double)(pfo_random_bits(seed, j, 0, j, 0) >> 11) + 0.5) * 0x1.0p-53;
+        const double x = u * 0.15 < 0.075 ? u * 0.15 : 0.075;
+        const double a = pfo_log_restated(x), b = log(x);
+        if (memcmp(&a, &b, 8) != 0) return 0;
+    }
+    return 1;
+}
+
 double pfo_inverse_normal_cdf(double p) {
     const double q = p - 0.5;
     if (fabs(q) <= 0.425) {
@@ -99,6 +146,11 @@ double pfo_normal(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity,
                   double mu, double sigma) {
     const double u = ((double)(pfo_random_bits(seed, step, phase, entity, counter) >> 11) + 0.5) * 0x1.0p-53;
     return mu + sigma * pfo_inverse_normal_cdf(u);
+}
+
+void pfo_normal_batch(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                      const uint64_t* entity, const uint32_t* counter, double mu, double sigma, double* out) {
+    for (uint32_t i = 0; i < n; ++i) out[i] = pfo_normal(seed[i], step[i], phase[i], entity[i], counter[i], mu, sigma);
 }
 
 /* -------------------------------------------------------------- grid-core */

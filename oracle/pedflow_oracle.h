@@ -62,6 +62,15 @@ uint32_t pfo_agent_size(void);
 uint64_t pfo_random_bits(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter);
 double pfo_uniform(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter);
 double pfo_inverse_normal_cdf(double p);
+/* glibc 2.39's log (x86-64 FMA variant) restated op for op, for positive
+ * normal x outside [1 - 2^-4, 1 + 0x1.09p-4] (the AS241 tail domain); the
+ * checker of the device's pfdev::glibc_log. NaN outside that domain. */
+double pfo_log_restated(double x);
+/* 1 where this host's log is the variant the restatement follows. */
+int pfo_log_restated_matches_host(uint32_t n, uint64_t seed);
+/* pfo_normal over arrays of keys (out[i] for key i). */
+void pfo_normal_batch(uint32_t n, const uint64_t* seed, const uint32_t* step, const uint32_t* phase,
+                      const uint64_t* entity, const uint32_t* counter, double mu, double sigma, double* out);
 double pfo_normal(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter,
                   double mu, double sigma);
 

@@ -4,11 +4,14 @@
 // Every floating-point operation uses an explicit round-to-nearest intrinsic
 // (__dmul_rn, __dadd_rn, ...) in the reference's evaluation order, so no FMA
 // contraction can change a bit; the library is additionally built with
-// --fmad=false. The only non-IEEE-exact call is log() in the AS241 tail
-// (CUDA: <= 1 ulp); see DESIGN.md "Bit-exactness".
+// --fmad=false. The AS241 tail's log is glibc's algorithm restated
+// (glibc_log); the only non-IEEE-exact call left is pow() for ACO alpha not
+// in {0, 1}; see DESIGN.md "Bit-exactness".
 #pragma once
 
 #include <cstdint>
+
+#include "pf_glibc_log.h"
 
 namespace pfdev {
 
@@ -89,6 +92,42 @@ __device__ __forceinline__ double horner8(const double (&c)[8], double r) {
     return v;
 }
 
+// glibc's log (the reference's std::log, src/rng.cpp:93-96) restated op for
+// op: the main path of sysdeps/ieee754/dbl-64/e_log.c (N = 128 table) in the
+// order and with the FMA contractions of the -mfma build (__log_fma) that
+// this image's glibc 2.39 dispatches to on FMA + AVX2 hosts, constants from
+// its libm (pf_glibc_log.h, tools/gen_log_table.py). Bit-identical to the
+// host's log for positive normal x away from 1 (checked on the host against
+// libm by the oracle's pfo_log_restated, and device against host by
+// tests/test_gpu_parity.py); the AS241 tail only asks for x in (0, 0.075].
+// Outside that domain it falls back to CUDA's log (<= 1 ulp).
+static __device__ const double kLogTab[128][2] = PF_LOG_TAB_INIT;
+static __device__ const double kLogPoly[5] = PF_LOG_POLY_INIT;
+
+__device__ __forceinline__ double glibc_log(double x) {
+    const uint64_t ix = uint64_t(__double_as_longlong(x));
+    const uint64_t top = ix >> 48;
+    if (ix - 0x3fee000000000000ull < 0x3ff1090000000000ull - 0x3fee000000000000ull || top - 0x0010u >= 0x7ff0u - 0x0010u)
+        return log(x);
+    const uint64_t tmp = ix - 0x3fe6000000000000ull;
+    const int i = int((tmp >> 45) & 127u);
+    const int k = int(int64_t(tmp) >> 52);
+    const double z = __longlong_as_double((long long)(ix - (tmp & (0xfffull << 52))));
+    const double kd = double(k);
+    const double w = __fma_rn(kd, PF_LOG_LN2HI, __ldg(&kLogTab[i][1]));
+    const double r = __fma_rn(z, __ldg(&kLogTab[i][0]), -1.0);
+    const double p21 = __fma_rn(r, __ldg(&kLogPoly[2]), __ldg(&kLogPoly[1]));
+    const double hi = __dadd_rn(r, w);
+    const double r2 = __dmul_rn(r, r);
+    double lo = __dadd_rn(__dsub_rn(w, hi), r);
+    lo = __fma_rn(kd, PF_LOG_LN2LO, lo);
+    const double r3 = __dmul_rn(r, r2);
+    double p43 = __fma_rn(r, __ldg(&kLogPoly[4]), __ldg(&kLogPoly[3]));
+    lo = __fma_rn(r2, __ldg(&kLogPoly[0]), lo);
+    p43 = __fma_rn(p43, r2, p21);
+    return __dadd_rn(__fma_rn(r3, p43, lo), hi);
+}
+
 // Wichura AS241 PPND16 (src/rng.cpp:61-150), same coefficients and order.
 static __device__ __noinline__ double inverse_normal_cdf(double p) {
     const double q = __dsub_rn(p, 0.5);
@@ -103,7 +142,7 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
         return __ddiv_rn(__dmul_rn(q, horner8(num, r)), horner8(den, r));
     }
     double r = (q < 0.0) ? p : __dsub_rn(1.0, p);
-    r = __dsqrt_rn(-log(r));
+    r = __dsqrt_rn(-glibc_log(r));
     double val;
     if (r <= 5.0) {
         constexpr double num[8] = {7.74545014278341407640e-4, 2.27238449892691845833e-2, 2.41780725177450611770e-1,

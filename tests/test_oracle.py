@@ -217,3 +217,17 @@ def test_oracle_winner_draw_uniform():
     k = 5
     idx = [min(int(lib.pfo_uniform(7, 123, 3, cell, 0) * k), k - 1) for cell in range(100_000)]
     assert chisquare(np.bincount(idx, minlength=k)).pvalue > 1e-3
+
+
+def test_log_restatement_matches_host_glibc():
+    """The restatement of glibc's log that the device uses (oracle's
+    pfo_log_restated, constants from tools/gen_log_table.py) equals this host's
+    log bit for bit over 2M AS241 tail arguments, and at hand-picked points."""
+    import math
+
+    from oracle.oracle import oracle
+
+    lib = oracle()
+    assert lib.pfo_log_restated_matches_host(2_000_000, 7) == 1
+    for x in (2.0**-54, 1e-300 * 1e290, 1e-5, 0.01, 0.0499, 0.075, 0.5, 0.9, 2.0, 1e300):
+        assert lib.pfo_log_restated(x).hex() == math.log(x).hex(), x
