@@ -463,6 +463,14 @@ def run_gpu_arm(args):
     _, kernel_ms_isolated = eng.ctx.time_steps(min(args.steps, 20), kernel=True)
     kernel_ms_isolated = max_over_ranks(kernel_ms_isolated)
     eng.close()
+    torch.cuda.empty_cache()
+    # Setup again in this process: the placement (new_environment's keyed
+    # Fisher-Yates) now comes from the library's cache.
+    t_setup = time.perf_counter()
+    eng = ShardedEngine(cfg, rank, world, device=local, replicas=reps)
+    setup_warm_s = time.perf_counter() - t_setup
+    eng.close()
+    torch.cuda.empty_cache()
     kernel_ms = ms / args.steps if world == 1 else kernel_ms_isolated
 
     agents_total = 2 * n * reps
@@ -505,6 +513,10 @@ def run_gpu_arm(args):
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "setup_s": setup_s,
+            "setup_warm_s": setup_warm_s,
+            "setup_note": "ShardedEngine construction: device allocation + new_environment placement (computed in the "
+                          "background from pf_create) + upload; setup_warm_s = the same in this process again "
+                          "(placement served from the in-process cache)",
             "moved_in_window_rank0": moved_local,
         }
         if e2e:

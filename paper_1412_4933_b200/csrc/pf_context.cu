@@ -259,6 +259,7 @@ int pf_new_environment(const pf_config* c, uint64_t seed, uint8_t* occ, uint32_t
         std::fill(tau_bot, tau_bot + cells, c->tau0);
     }
     const uint32_t W = uint32_t(c->width);
+    try {
     pfhost::place_all(c->width, c->height, c->agents_per_side, seed, [&](uint32_t cell, uint32_t id, uint32_t g) {
         occ[cell] = uint8_t(g);
         index[cell] = id;
@@ -270,6 +271,9 @@ int pf_new_environment(const pf_config* c, uint64_t seed, uint8_t* occ, uint32_t
         a.tour_length = 0.0;
         a.crossed = 0;
     });
+    } catch (const std::exception& e) {
+        return fail(PF_ERR_ARG, std::string("new_environment: ") + e.what());
+    }
     return PF_OK;
 }
 
@@ -421,6 +425,12 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     for (int r = 0; r < cfg->replicas; ++r)
         ctx->reps[size_t(r)] = {cfg->seed + uint64_t(r), pfhost::band_height(cfg->agents_per_side, cfg->width),
                                 2u * uint32_t(cfg->agents_per_side)};
+    // Large grids: compute the placement (new_environment's keyed Fisher-Yates,
+    // host work) in the background while the device is set up; the
+    // pf_init_environment that normally follows finds it cached.
+    if (size_t(cfg->width) * size_t(cfg->height) >= (size_t(1) << 20))
+        for (int r = 0; r < std::min(cfg->replicas, 4); ++r)
+            pfhost::prefetch_placement(cfg->width, cfg->height, cfg->agents_per_side, ctx->reps[size_t(r)].seed);
     {
         auto* d_rep = static_cast<pfdev::ReplicaParams*>(alloc(ctx->reps.size() * sizeof(pfdev::ReplicaParams)));
         if (!d_rep || cudaMemcpy(d_rep, ctx->reps.data(), ctx->reps.size() * sizeof(pfdev::ReplicaParams),
@@ -552,11 +562,13 @@ int pf_init_environment(pf_ctx* ctx) {
     const int R = c.replicas;
     const int nthreads = std::max(1, std::min<int>(R, int(std::thread::hardware_concurrency())));
     std::vector<std::vector<uint32_t>> words(std::min(R, nthreads));
+    std::atomic<bool> failed{false};
     for (int r0 = 0; r0 < R; r0 += nthreads) {
         const int nb = std::min(nthreads, R - r0);
         std::vector<std::thread> ts;
         for (int t = 0; t < nb; ++t) {
             ts.emplace_back([&, t] {
+              try {
                 std::vector<uint32_t>& w = words[size_t(t)];
                 w.assign(ctx->plane(), 0u);
                 for (int b = 0; b < ctx->rows_buf; ++b) {
@@ -570,9 +582,13 @@ int pf_init_environment(pf_ctx* ctx) {
                                       if (row < lo || row >= hi) return;
                                       w[size_t(row - lo) * W + cell % W] = id | (g << 30);
                                   });
+              } catch (...) {
+                failed = true;
+              }
             });
         }
         for (auto& t : ts) t.join();
+        if (failed) return fail(PF_ERR_CUDA, "new_environment: host allocation failed");
         for (int t = 0; t < nb; ++t)
             if (int rc = upload_replica(ctx, r0 + t, words[size_t(t)], nullptr, nullptr)) return rc;
     }

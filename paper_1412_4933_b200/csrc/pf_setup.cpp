@@ -8,7 +8,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <future>
+#include <list>
+#include <map>
+#include <mutex>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 namespace pfhost {
@@ -75,12 +80,113 @@ void place_side(int32_t width, uint32_t group, int32_t row_begin, int32_t row_en
     for (int32_t k = 0; k < n; ++k) put(cells[size_t(k)], first_id + uint32_t(k));
 }
 
+namespace {
+
+using Key = std::tuple<int32_t, int32_t, int32_t, uint64_t>;
+using Pending = std::shared_future<std::shared_ptr<const Placement>>;
+
+struct Cache {
+    std::mutex mu;
+    std::map<Key, Pending> entries;
+    std::list<Key> lru;  // front = most recent
+    size_t bytes = 0;
+    static constexpr size_t kCapacity = size_t(3) << 29;  // 1.5 GB of cell lists
+};
+
+Cache& cache() {
+    static Cache c;
+    return c;
+}
+
+std::shared_ptr<const Placement> compute(int32_t width, int32_t height, int32_t n, uint64_t seed) {
+    auto pl = std::make_shared<Placement>();
+    pl->band = band_height(n, width);
+    const int32_t band = pl->band;
+    auto side = [&](int s) {
+        std::vector<uint32_t>& out = pl->cells[s];
+        out.resize(size_t(std::max(0, n)));
+        place_side(width, uint32_t(s + 1), s == 0 ? 0 : height - band, s == 0 ? band : height, n, 0, seed,
+                   [&](uint32_t cell, uint32_t k) { out[k] = cell; });
+    };
+    std::thread bottom(side, 1);  // the two sides are independent swap chains
+    side(0);
+    bottom.join();
+    return pl;
+}
+
+Pending request(int32_t width, int32_t height, int32_t n, uint64_t seed, bool async) {
+    Cache& c = cache();
+    const Key key{width, height, n, seed};
+    std::unique_lock<std::mutex> lk(c.mu);
+    auto it = c.entries.find(key);
+    if (it != c.entries.end()) {
+        c.lru.remove(key);
+        c.lru.push_front(key);
+        return it->second;
+    }
+    std::promise<std::shared_ptr<const Placement>> prom;
+    Pending fut = prom.get_future().share();
+    c.entries.emplace(key, fut);
+    c.lru.push_front(key);
+    lk.unlock();
+    auto work = [width, height, n, seed, key, p = std::move(prom)]() mutable {
+        std::shared_ptr<const Placement> pl;
+        try {
+            pl = compute(width, height, n, seed);
+        } catch (...) {  // out of host memory: forget the entry, report to every waiter
+            Cache& cc = cache();
+            {
+                std::lock_guard<std::mutex> g(cc.mu);
+                cc.entries.erase(key);
+                cc.lru.remove(key);
+            }
+            p.set_exception(std::current_exception());
+            return;
+        }
+        Cache& cc = cache();
+        {
+            std::lock_guard<std::mutex> g(cc.mu);
+            cc.bytes += pl->bytes();
+            // Evict least recently used finished entries beyond the capacity.
+            const std::vector<Key> order(cc.lru.rbegin(), cc.lru.rend());
+            for (const Key& k : order) {
+                if (cc.bytes <= Cache::kCapacity) break;
+                auto e = cc.entries.find(k);
+                if (k == key || e == cc.entries.end() ||
+                    e->second.wait_for(std::chrono::seconds(0)) != std::future_status::ready)
+                    continue;
+                cc.bytes -= e->second.get()->bytes();
+                cc.entries.erase(e);
+                cc.lru.remove(k);
+            }
+        }
+        p.set_value(std::move(pl));
+    };
+    if (async) std::thread(std::move(work)).detach();
+    else work();
+    return fut;
+}
+
+}  // namespace
+
+std::shared_ptr<const Placement> placement(int32_t width, int32_t height, int32_t n, uint64_t seed) {
+    return request(width, height, n, seed, false).get();
+}
+
+void prefetch_placement(int32_t width, int32_t height, int32_t n, uint64_t seed) {
+    request(width, height, n, seed, true);
+}
+
 void place_all(int32_t width, int32_t height, int32_t n, uint64_t seed,
                const std::function<void(uint32_t cell, uint32_t id, uint32_t group)>& put) {
-    const int32_t band = band_height(n, width);
-    place_side(width, 1, 0, band, n, 1, seed, [&](uint32_t c, uint32_t id) { put(c, id, 1); });
-    place_side(width, 2, height - band, height, n, uint32_t(n) + 1, seed,
-               [&](uint32_t c, uint32_t id) { put(c, id, 2); });
+    if (n <= 0) return;
+    const std::shared_ptr<const Placement> pl = placement(width, height, n, seed);
+    parallel_for(size_t(n), [&](size_t b, size_t e) {
+        for (size_t k = b; k < e; ++k) {
+            put(pl->cells[0][k], uint32_t(k) + 1, 1);
+            put(pl->cells[1][k], uint32_t(n) + uint32_t(k) + 1, 2);
+        }
+    });
 }
 
 }  // namespace pfhost

@@ -124,6 +124,35 @@ def test_new_environment_matches_oracle(kw):
     s = p.new_environment(to_config(kw), kw.get("seed", 42))
     assert hashes_of(s) == o.hashes()
     assert (s.agents == o.agents).all()
+    # The second call is served from the library's placement cache.
+    s2 = p.new_environment(to_config(kw), kw.get("seed", 42))
+    assert hashes_of(s2) == o.hashes()
+    assert (s2.agents == o.agents).all()
+
+
+def test_placement_cache_keys_and_speed():
+    """Placements are cached per (W, H, n, seed): a different seed or density
+    is placed afresh (and still equals the oracle), and a repeated large
+    placement (1.3M agents per side) comes back well under the cold time."""
+    import time
+
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState, Scenario
+
+    kw = dict(width=96, height=96, agents_per_side=900, model="lem")
+    for seed, n in ((5, 900), (6, 900), (5, 700)):
+        k = dict(kw, seed=seed, agents_per_side=n)
+        s = p.new_environment(to_config(k), seed)
+        assert hashes_of(s) == OracleState(Scenario(**k)).hashes()
+    big = p.ScenarioConfig(width=4096, height=1024, agents_per_side=1_300_000, model=p.Model.Lem)
+    t0 = time.perf_counter()
+    a = p.new_environment(big, 99)
+    cold = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    b = p.new_environment(big, 99)
+    warm = time.perf_counter() - t0
+    assert (a.index == b.index).all() and (a.agents == b.agents).all()
+    assert warm < cold
 
 
 def test_device_calls_fail_loudly_without_gpu():
