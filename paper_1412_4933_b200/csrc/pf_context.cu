@@ -517,13 +517,16 @@ static cudaError_t copy_d2d(void* dst, const void* src, size_t n, cudaStream_t s
 }
 
 // Upload one replica's buffer-row planes (cells + tour) and set the step.
-static int upload_replica(pf_ctx* ctx, int rep, const std::vector<uint32_t>& words, const std::vector<double>* tour,
-                          const std::vector<double2>* tau) {
+static int ensure_scratch(pf_ctx* ctx, size_t need);
+
+// After replica rep's words are in P.cell[0]: the second word buffer, the
+// occupancy planes, tours and pheromone (uploaded, or the initial values).
+static int finish_replica_upload(pf_ctx* ctx, int rep, const std::vector<double>* tour,
+                                 const std::vector<double2>* tau) {
     const size_t off = size_t(rep) * ctx->plane();
     pfk::Planes& P = ctx->args.p;
-    // One host->device copy per plane; the second ping-pong buffer is filled
-    // device-side (its ghost rows must hold the same walls / halo).
-    PF_CUDA(ctx->stage[0].h2d(P.cell[0] + off, words.data(), ctx->plane() * 4, ctx->stream));
+    // The second ping-pong buffer is filled device-side (its ghost rows must
+    // hold the same walls / halo).
     PF_CUDA(copy_d2d(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, ctx->stream));
     build_occ(ctx, rep);
     if (ctx->aco()) {
@@ -557,40 +560,54 @@ int pf_init_environment(pf_ctx* ctx) {
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
     const pf_config& c = ctx->cfg;
     const uint32_t W = uint32_t(c.width);
-    // Placement is host work; replicas are independent, so build them on
-    // worker threads and upload in order.
+    // new_environment (src/state.cpp:17-75): the placement (keyed
+    // Fisher-Yates) is host work, cached per scenario and normally already
+    // computed in the background since pf_create; replicas are independent,
+    // so several are placed at once. Only the placed agents' cell lists go to
+    // the device, where a kernel writes their words into a zeroed plane.
     const int R = c.replicas;
     const int nthreads = std::max(1, std::min<int>(R, int(std::thread::hardware_concurrency())));
-    std::vector<std::vector<uint32_t>> words(std::min(R, nthreads));
-    std::atomic<bool> failed{false};
+    std::vector<std::shared_ptr<const pfhost::Placement>> pls(size_t(std::min(R, nthreads)));
+    pfk::Planes& P = ctx->args.p;
+    const int64_t g_lo = grow_of(ctx, 0);
     for (int r0 = 0; r0 < R; r0 += nthreads) {
         const int nb = std::min(nthreads, R - r0);
+        std::atomic<bool> failed{false};
         std::vector<std::thread> ts;
         for (int t = 0; t < nb; ++t) {
             ts.emplace_back([&, t] {
-              try {
-                std::vector<uint32_t>& w = words[size_t(t)];
-                w.assign(ctx->plane(), 0u);
-                for (int b = 0; b < ctx->rows_buf; ++b) {
-                    const int64_t g = grow_of(ctx, b);
-                    if (g < 0 || g >= c.height) std::fill(w.begin() + size_t(b) * W, w.begin() + size_t(b + 1) * W, kWall);
+                try {
+                    pls[size_t(t)] = pfhost::placement(c.width, c.height, ctx->rep_aps[size_t(r0 + t)],
+                                                       ctx->reps[size_t(r0 + t)].seed);
+                } catch (...) {
+                    failed = true;
                 }
-                const int64_t lo = grow_of(ctx, 0), hi = grow_of(ctx, ctx->rows_buf);
-                pfhost::place_all(c.width, c.height, ctx->rep_aps[size_t(r0 + t)], ctx->reps[size_t(r0 + t)].seed,
-                                  [&](uint32_t cell, uint32_t id, uint32_t g) {
-                                      const int64_t row = cell / W;
-                                      if (row < lo || row >= hi) return;
-                                      w[size_t(row - lo) * W + cell % W] = id | (g << 30);
-                                  });
-              } catch (...) {
-                failed = true;
-              }
             });
         }
         for (auto& t : ts) t.join();
         if (failed) return fail(PF_ERR_CUDA, "new_environment: host allocation failed");
-        for (int t = 0; t < nb; ++t)
-            if (int rc = upload_replica(ctx, r0 + t, words[size_t(t)], nullptr, nullptr)) return rc;
+        for (int t = 0; t < nb; ++t) {
+            const int rep = r0 + t;
+            const size_t off = size_t(rep) * ctx->plane();
+            const uint32_t n = uint32_t(ctx->rep_aps[size_t(rep)]);
+            PF_CUDA(cudaMemsetAsync(P.cell[0] + off, 0, ctx->plane() * 4, ctx->stream));
+            for (int b = 0; b < ctx->rows_buf; ++b) {  // rows outside the grid are walls
+                const int64_t g = grow_of(ctx, b);
+                if (g < 0 || g >= c.height)
+                    PF_CUDA(cudaMemsetAsync(P.cell[0] + off + size_t(b) * W, 0xFF, size_t(W) * 4, ctx->stream));
+            }
+            if (n > 0) {
+                if (int rc = ensure_scratch(ctx, size_t(n) * 8)) return rc;
+                uint32_t* d_cells = static_cast<uint32_t*>(ctx->io_scratch);
+                PF_CUDA(ctx->stage[0].h2d(d_cells, pls[size_t(t)]->cells[0].data(), size_t(n) * 4, ctx->stream));
+                PF_CUDA(ctx->stage[0].h2d(d_cells + n, pls[size_t(t)]->cells[1].data(), size_t(n) * 4, ctx->stream));
+                ctx->launches += pfk::launch_scatter_placement(P.cell[0] + off, d_cells, n, 1u, 1u, W, g_lo,
+                                                               ctx->rows_buf, ctx->stream);
+                ctx->launches += pfk::launch_scatter_placement(P.cell[0] + off, d_cells + n, n, n + 1u, 2u, W, g_lo,
+                                                               ctx->rows_buf, ctx->stream);
+            }
+            if (int rc = finish_replica_upload(ctx, rep, nullptr, nullptr)) return rc;
+        }
     }
     ctx->parity = 0;
     set_step(ctx, 0);

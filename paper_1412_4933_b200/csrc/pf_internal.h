@@ -96,6 +96,10 @@ int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
 // Fill a tau plane range with {v, v}.
 int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);
+// words[(row - g_lo) * W + col] = (first_id + k) | group << 30 for cells[k] on
+// buffer rows [0, rows) (row = cells[k] / W).
+int launch_scatter_placement(uint32_t* words, const uint32_t* cells, uint32_t n, uint32_t first_id, uint32_t group,
+                             uint32_t W, long long g_lo, int rows, cudaStream_t s);
 int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agents, uint32_t* seen,
                  unsigned long long* counts, cudaStream_t s);
 // State upload / download layout transforms.

@@ -394,6 +394,26 @@ int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s) {
     return 1;
 }
 
+// new_environment on the device: the placed agents' cell words
+// (id | group << 30, src/state.cpp:38-48) scattered into the buffer rows
+// [g_lo, g_lo + rows) of a zeroed word plane. cells[k] = global linear cell of
+// agent first_id + k (the host's keyed Fisher-Yates, pf_setup.cpp).
+__global__ void scatter_placement_kernel(uint32_t* words, const uint32_t* cells, uint32_t n, uint32_t first_id,
+                                         uint32_t group, uint32_t W, long long g_lo, int rows) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t cell = cells[k];
+        const long long row = (long long)(cell / W) - g_lo;
+        if (row >= 0 && row < rows) words[size_t(row) * W + cell % W] = (first_id + k) | (group << 30);
+    }
+}
+
+int launch_scatter_placement(uint32_t* words, const uint32_t* cells, uint32_t n, uint32_t first_id, uint32_t group,
+                             uint32_t W, long long g_lo, int rows, cudaStream_t s) {
+    if (n == 0) return 0;
+    scatter_placement_kernel<<<148 * 8, 256, 0, s>>>(words, cells, n, first_id, group, W, g_lo, rows);
+    return 1;
+}
+
 __global__ void fill_u8_kernel(uint8_t* p, size_t n, uint8_t v) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         p[i] = v;
