@@ -3,6 +3,7 @@
 #include "../../include/pf_gpu.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -27,6 +28,16 @@ using pfdev::kWall;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX ranges around every C-ABI entry point that does device work (SURVEY
+// §5 tracing): visible in Nsight Systems / ncu --nvtx as pf_step,
+// pf_load_state, ... (header-only NVTX3: no cost without an attached tool).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -321,6 +332,7 @@ static int fill_consts(pf_ctx* ctx) {
 }
 
 int pf_create(const pf_config* cfg, pf_ctx** out) {
+    NvtxRange nvtx_range("pf_create");
     if (!out) return fail(PF_ERR_ARG, "null out");
     *out = nullptr;
     if (int rc = pf_validate(cfg)) return rc;
@@ -556,6 +568,7 @@ static void set_step(pf_ctx* ctx, uint32_t step) {
 }
 
 int pf_init_environment(pf_ctx* ctx) {
+    NvtxRange nvtx_range("pf_init_environment");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
     const pf_config& c = ctx->cfg;
@@ -629,6 +642,7 @@ static size_t up256(size_t b) { return (b + 255) & ~size_t(255); }
 
 int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* index, const pf_agent* agents,
                   uint32_t n_agents, const double* tau_top, const double* tau_bot, uint32_t step) {
+    NvtxRange nvtx_range("pf_load_state");
     if (!ctx || !occ || !index) return fail(PF_ERR_ARG, "null argument");
     if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
     const pf_config& c = ctx->cfg;
@@ -799,6 +813,7 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
 
 int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_agent* agents, uint32_t n_agents,
                    double* tau_top, double* tau_bot, uint32_t* step) {
+    NvtxRange nvtx_range("pf_store_state");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
     const pf_config& c = ctx->cfg;
@@ -983,6 +998,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
 }
 
 int pf_step_async(pf_ctx* ctx, uint32_t n) {
+    NvtxRange nvtx_range("pf_step_async");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (ctx->phase) return fail(PF_ERR_ARG, "a phase-level step is in progress: finish it with PF_PHASE_RESET");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -1022,6 +1038,7 @@ int pf_synchronize(pf_ctx* ctx) {
 }
 
 int pf_step(pf_ctx* ctx, uint32_t n, pf_step_report* out) {
+    NvtxRange nvtx_range("pf_step");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (ctx->phase) return fail(PF_ERR_ARG, "a phase-level step is in progress: finish it with PF_PHASE_RESET");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -1167,6 +1184,7 @@ int pf_exchange_pair(pf_ctx* upper, pf_ctx* lower) {
 }
 
 int pf_phase(pf_ctx* ctx, int32_t phase, pf_step_report* out) {
+    NvtxRange nvtx_range("pf_phase");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (ctx->cfg.kernel != PF_KERNEL_PIPELINE)
         return fail(PF_ERR_CONFIG, "phase-level stepping needs PF_KERNEL_PIPELINE (the fused kernels run all four phases "
@@ -1343,6 +1361,7 @@ int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc
 }
 
 int pf_audit(pf_ctx* ctx, int32_t rep, uint64_t* agent_cells) {
+    NvtxRange nvtx_range("pf_audit");
     if (!ctx) return fail(PF_ERR_ARG, "null ctx");
     if (rep < 0 || rep >= ctx->cfg.replicas) return fail(PF_ERR_ARG, "replica out of range");
     PF_CUDA(cudaSetDevice(ctx->cfg.device));
