@@ -141,7 +141,8 @@ struct Smem {
     // with one-tile items the next claim can come before the slowest warp
     // has read the previous one (no barrier in between).
     int item[2];
-    int idec[2][4];   // the same items decoded (rep, strip, chunk, sides) once: no divisions per thread
+    int idec[2][5];   // the same items decoded (rep, strip, chunk, sides, step offset) once: no divisions per thread
+    int defer[2];     // multi-step launches: the item's window could not be prefetched (dependencies pending)
     uint32_t cnt[3];
     double atr[NW][NS][32];  // ACO only: LEM launches allocate the struct without it (last member)
 };
@@ -369,6 +370,7 @@ __device__ __forceinline__ void set_winner(Smem& sm, int cur, int ai, int si, in
 // replica.
 struct Item {
     int rep, strip, chunk, c0, t_first, t_end;
+    int sl;     // step of the item relative to the launch's first step (multi-step launches)
     int sides;  // bit 0 / 1: the item reads the upper / lower ghost rows (and writes the rows they mirror)
 };
 
@@ -426,6 +428,7 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
         it.chunk = spread ? two_ended(item / (strips * reps), n_chunks) : item / (strips * reps);
     }
     it.sides = bfirst ? chunk_sides(it.chunk, tiles_per_item, n_tiles, rows_owned) : 0;
+    it.sl = 0;
     it.c0 = it.strip * (NS * 32);
     it.t_first = it.chunk * tiles_per_item;
     it.t_end = min(it.t_first + tiles_per_item, n_tiles);
@@ -433,22 +436,79 @@ __device__ __forceinline__ Item decode_item(int item, int strips, int n_chunks, 
 }
 
 // An item decoded by the claiming warp (Smem::idec) for the rest of the CTA.
-__device__ __forceinline__ void publish_item(int (&d)[4], const Item& it) {
+__device__ __forceinline__ void publish_item(int (&d)[5], const Item& it) {
     d[0] = it.rep;
     d[1] = it.strip;
     d[2] = it.chunk;
     d[3] = it.sides;
+    d[4] = it.sl;
 }
-__device__ __forceinline__ Item read_item(const int (&d)[4], int n_tiles, int tiles_per_item) {
+__device__ __forceinline__ Item read_item(const int (&d)[5], int n_tiles, int tiles_per_item) {
     Item it;
     it.rep = d[0];
     it.strip = d[1];
     it.chunk = d[2];
     it.sides = d[3];
+    it.sl = d[4];
     it.c0 = it.strip * (NS * 32);
     it.t_first = it.chunk * tiles_per_item;
     it.t_end = min(it.t_first + tiles_per_item, n_tiles);
     return it;
+}
+
+// Multi-step launches (StepArgs::nsteps > 1, unlinked contexts): the launch
+// runs nsteps consecutive steps and its CTAs claim items step-major from one
+// counter, g = sl * n_items + i. An item of step step0 + sl > step0 starts
+// once the 3x3 neighbourhood of its tiles (strips strip - 1 .. strip + 1,
+// tiles t_first - 1 .. t_end; the step's dependency radius, 3 rows and 64
+// columns, is within one tile and one strip) has completed the previous step:
+// tile_done[rep][strip][tile] = last completed step + 1, released by the CTA
+// that finished the tile. Steps thus overlap in the tail instead of
+// draining the GPU at every step boundary. The reads and writes the wait
+// orders are exactly those of the stream order between step launches:
+// step s reads the neighbourhood's step s-1 output and overwrites the
+// buffers (ping-pong planes, in-place words and tours at cells empty at step
+// start) that the neighbourhood read during step s-1.
+__device__ __forceinline__ Item decode_global(int g, int n_items, int strips, int n_chunks, int n_tiles,
+                                              int tiles_per_item, int reps, bool bfirst, int rows_owned, bool spread,
+                                              bool multi) {
+    const int sl = multi ? g / n_items : 0;
+    Item it = decode_item(g - sl * n_items, strips, n_chunks, n_tiles, tiles_per_item, reps, bfirst, rows_owned, spread);
+    it.sl = sl;
+    return it;
+}
+
+// Called by a full warp: are the neighbourhood's tiles done with step
+// need - 1? With `block`, spins until they are (30 s timeout sets *a.err).
+__device__ __forceinline__ bool deps_ready(const StepArgs& a, const Item& it, uint32_t need, int strips, int n_tiles,
+                                           bool block) {
+    const int lane = threadIdx.x & 31;
+    const int s_lo = max(0, it.strip - 1), s_hi = min(strips - 1, it.strip + 1);
+    const int t_lo = max(0, it.t_first - 1), t_hi = min(n_tiles - 1, it.t_end);
+    const int nt = t_hi - t_lo + 1, total = (s_hi - s_lo + 1) * nt;
+    uint64_t t0 = 0;
+    for (;;) {
+        bool ok = true;
+        for (int k = lane; k < total; k += 32) {
+            const uint32_t* f = a.tile_done + (size_t(it.rep) * strips + (s_lo + k / nt)) * n_tiles + (t_lo + k % nt);
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            ok = ok && int32_t(v - need) >= 0;
+        }
+        ok = __all_sync(0xFFFFFFFFu, ok);
+        if (ok || !block) return ok;
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (!t0) t0 = now;
+        uint32_t err;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(err) : "l"(a.err) : "memory");
+        if (__any_sync(0xFFFFFFFFu, (err & 2u) != 0u)) return true;  // another wait timed out: drain
+        if (now - t0 > 10000000000ull) {
+            if (lane == 0) atomicOr(a.err, 2u);
+            return true;
+        }
+        __nanosleep(64);
+    }
 }
 
 // Issue the TMA loads of `nrows` staged plane rows (tile rows first_sr..,
@@ -555,7 +615,9 @@ __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int r
 // COMPACT: S3 per-arrival work on compacted arrival lists (dense, batched
 // 480^2 grids: C4 x64 -6.4%); off for large grids, where arrivals are sparse
 // and the per-segment form is 1-2% faster.
-template <bool ACO, int CTAS, bool MIRROR, bool COMPACT>
+// MULTI: compiled with the multi-step (tile-dependency) logic; instantiated
+// only for the dense-grid variants that launch() runs that way.
+template <bool ACO, int CTAS, bool MIRROR, bool COMPACT, bool MULTI>
 __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -565,11 +627,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     const int strips = (W + NS * 32 - 1) / (NS * 32);
     const int n_tiles = (a.rows_owned + RT - 1) / RT;
     const int n_chunks = (n_tiles + a.tiles_per_cta - 1) / a.tiles_per_cta;
-    const int n_items = strips * n_chunks * a.replicas;
+    const int n_items = strips * n_chunks * a.replicas;  // per step
     // Two-ended row bands only pay when items queue up; when every item has
     // its own CTA (small grids), plain order keeps neighbouring tiles on
     // neighbouring CTAs.
     const bool spread = n_items > int(gridDim.x);
+    const bool multi = MULTI && !MIRROR && a.nsteps > 1;  // tile-level dependencies between the launch's steps
+    const int n_all = n_items * (multi ? a.nsteps : 1);
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.mbar[0], 1);
@@ -602,16 +666,17 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     // previous step's tail; from here on the previous step's results (planes,
     // words, step counter) are complete and visible.
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t step = *a.d_step + uint32_t(slot_idx);
+    const uint32_t step0 = *a.d_step + uint32_t(slot_idx);
     __syncthreads();
     if (warp == 0) {
         if (lane == 0) sm.item[1] = item;
-        if (item < n_items) {
-            const Item first = decode_item(item, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread);
+        if (item < n_all) {
+            const Item first = decode_global(item, n_items, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread, multi);
             if (lane == 0) publish_item(sm.idec[1], first);
-            if (MIRROR && first.sides && lane == 0) wait_boundary(a, first.sides, step);
+            if (MIRROR && first.sides && lane == 0) wait_boundary(a, first.sides, step0);
+            if (multi && first.sl > 0) deps_ready(a, first, step0 + uint32_t(first.sl), strips, n_tiles, true);
             __syncwarp();
-            load_rows(sm, a, parity, first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
+            load_rows(sm, a, parity ^ (first.sl & 1), first, first.t_first * RT, 0, 0, SR, &sm.mbar[0]);
         }
     }
     __syncthreads();  // item id and wall rows written by warp 0 are visible to all
@@ -619,20 +684,22 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     int islot = 1;    // sm.idec slot of the current item
     int ipar = 0;     // the current item's last tile claims the next one into sm.item[ipar]
     uint32_t moved = 0, ntop = 0, nbot = 0;
-    uint32_t nload = item < n_items ? 1u : 0u;  // load i completes mbar[i & 1], phase i >> 1
+    uint32_t nload = item < n_all ? 1u : 0u;    // load i completes mbar[i & 1], phase i >> 1
     int base = 0;                               // ring slot of staged row 0 of the current tile
     int cur = 0;                                // tile parity: G / dirty / work-list counters
     uint32_t* const cells = a.p.cell[0];
-    while (item < n_items) {
+    while (item < n_all) {
     const Item it = read_item(sm.idec[islot], n_tiles, a.tiles_per_cta);
     const int rep = it.rep, c0 = it.c0;
+    const uint32_t step = step0 + uint32_t(it.sl);  // this item's step and read parity
+    const int par = parity ^ (it.sl & 1);
     const uint64_t seed = __ldg(&a.rep[rep].seed);
     const int band = __ldg(&a.rep[rep].band);
     const size_t plane_base = size_t(rep) * a.p.plane;
     uint32_t* const cw = cells + plane_base;
-    uint2* const oout = a.p.occ[parity ^ 1] + size_t(rep) * a.p.occ_plane + size_t(it.strip) * NS + 2;
-    const double2* __restrict__ tin = ACO ? a.p.tau[parity] + plane_base : nullptr;
-    double2* __restrict__ tout = ACO ? a.p.tau[parity ^ 1] + plane_base : nullptr;
+    uint2* const oout = a.p.occ[par ^ 1] + size_t(rep) * a.p.occ_plane + size_t(it.strip) * NS + 2;
+    const double2* __restrict__ tin = ACO ? a.p.tau[par] + plane_base : nullptr;
+    double2* __restrict__ tout = ACO ? a.p.tau[par ^ 1] + plane_base : nullptr;
     double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
     int next_base = 0;
 
@@ -643,7 +710,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // previous readers all passed the end-of-tile barrier): the next
         // tile's RT new rows, or on the last tile the next item's window.
         if (t + 1 < it.t_end) {
-            if (warp == kIoWarp) load_rows(sm, a, parity, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
+            if (warp == kIoWarp) load_rows(sm, a, par, it, r0 + RT, slot(base, RT), 6, RT, &sm.mbar[nload & 1]);
             ++nload;
         } else {
             next_base = kCrossPrefetch ? slot(base, SR) : 0;
@@ -654,14 +721,21 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 if (lane == 0) sm.item[ipar] = nx;
                 // This CTA's last item: the next step's grid may be scheduled
                 // (its CTAs wait in griddepcontrol.wait until this grid ends).
-                if (nx >= n_items && lane == 0) asm volatile("griddepcontrol.launch_dependents;");
-                if (nx < n_items) {
-                    const Item nit = decode_item(nx, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread);
+                if (nx >= n_all && lane == 0) asm volatile("griddepcontrol.launch_dependents;");
+                if (nx < n_all) {
+                    const Item nit = decode_global(nx, n_items, strips, n_chunks, n_tiles, a.tiles_per_cta, a.replicas, MIRROR, a.rows_owned, spread, multi);
                     if (lane == 0) publish_item(sm.idec[ipar], nit);
-                    if (kCrossPrefetch) {
-                        if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
+                    // Multi-step: prefetch only if the next item's neighbourhood
+                    // is already done (it may include this very item, which
+                    // finishes only after this tile); else load it after the
+                    // item (a blocking wait is safe there).
+                    const bool ready = !multi || nit.sl == 0 ||
+                                       deps_ready(a, nit, step0 + uint32_t(nit.sl), strips, n_tiles, false);
+                    if (lane == 0) sm.defer[ipar] = ready ? 0 : 1;
+                    if (kCrossPrefetch && ready) {
+                        if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step0);
                         __syncwarp();
-                        load_rows(sm, a, parity, nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
+                        load_rows(sm, a, parity ^ (nit.sl & 1), nit, nit.t_first * RT, next_base, 0, SR, &sm.mbar[nload & 1]);
                     }
                 }
             }
@@ -1004,7 +1078,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             }
         }
         __syncthreads();  // end of tile: the window's slots may be refilled
-        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, parity, rep, it.strip, r0);
+        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, par, rep, it.strip, r0);
         base = slot(base, RT);
         cur ^= 1;
     }
@@ -1028,22 +1102,32 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         if (sm.cnt[2]) atomicAdd(&rep_slot[3], sm.cnt[2]);
         sm.cnt[0] = sm.cnt[1] = sm.cnt[2] = 0u;
         if (MIRROR && it.sides) signal_boundary(a, it.sides, step, strips, n_chunks, n_tiles);  // after the barrier: all mirror stores fenced
+        // Release the item's tiles. The barrier above orders every thread's
+        // stores of the item before this thread's; the gpu-scope release
+        // (cumulative) publishes them with the flag (as CUTLASS's semaphore).
+        if (multi) {
+            for (int t = it.t_first; t < it.t_end; ++t) {
+                uint32_t* f = a.tile_done + (size_t(rep) * strips + it.strip) * n_tiles + t;
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(step + 1u) : "memory");
+            }
+        }
     }
     item = sm.item[ipar];  // claimed during the last tile (visible after its barriers)
     islot = ipar;
     ipar ^= 1;
-    if (!kCrossPrefetch && item < n_items) {
-        // Small ring: the next item's window is loaded only now, into the
-        // slots the finished item released.
+    if ((!kCrossPrefetch || (multi && sm.defer[islot])) && item < n_all) {
+        // Small ring, or a deferred multi-step item: the next item's window
+        // is loaded only now, into the slots the finished item released.
         if (warp == kIoWarp) {
             const Item nit = read_item(sm.idec[islot], n_tiles, a.tiles_per_cta);
-            if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step);
+            if (MIRROR && nit.sides && lane == 0) wait_boundary(a, nit.sides, step0);
+            if (multi && nit.sl > 0) deps_ready(a, nit, step0 + uint32_t(nit.sl), strips, n_tiles, true);
             __syncwarp();
-            load_rows(sm, a, parity, nit, nit.t_first * RT, 0, 0, SR, &sm.mbar[nload & 1]);
+            load_rows(sm, a, parity ^ (nit.sl & 1), nit, nit.t_first * RT, base, 0, SR, &sm.mbar[nload & 1]);
         }
         __syncthreads();  // wall rows written by the I/O warp are visible to all
     }
-    if (item < n_items) ++nload;
+    if (item < n_all) ++nload;
     }  // work items
 }
 
@@ -1061,11 +1145,13 @@ static_assert(kCtasLem >= 1 && kCtasDefault >= 1, "shared memory must fit one CT
 
 int configure() {
     const int lem = int(kSmemBytes[0]), aco = int(kSmemBytes[1]);
-    for (auto f : {step_bits_kernel<false, kCtasLem, false, true>, step_bits_kernel<false, kCtasLem, true, true>,
-                   step_bits_kernel<false, kCtasLemBig, false, false>, step_bits_kernel<false, kCtasLemBig, true, false>})
+    for (auto f : {step_bits_kernel<false, kCtasLem, false, true, false>, step_bits_kernel<false, kCtasLem, true, true, false>,
+                   step_bits_kernel<false, kCtasLem, false, true, true>,
+                   step_bits_kernel<false, kCtasLemBig, false, false, false>, step_bits_kernel<false, kCtasLemBig, true, false, false>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lem) != cudaSuccess) return 1;
-    for (auto f : {step_bits_kernel<true, kCtasDefault, false, true>, step_bits_kernel<true, kCtasHbm, false, false>,
-                   step_bits_kernel<true, kCtasDefault, true, true>, step_bits_kernel<true, kCtasHbm, true, false>})
+    for (auto f : {step_bits_kernel<true, kCtasDefault, false, true, false>, step_bits_kernel<true, kCtasHbm, false, false, false>,
+                   step_bits_kernel<true, kCtasDefault, true, true, false>, step_bits_kernel<true, kCtasHbm, true, false, false>,
+                   step_bits_kernel<true, kCtasDefault, false, true, true>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, aco) != cudaSuccess) return 1;
     return 0;
 }
@@ -1107,21 +1193,36 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     StepArgs b = a;
     b.tiles_per_cta = int(std::max<long long>(1, std::min<long long>(16, tiles / (ctas_max * a.items_per_cta))));
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
-    dim3 grid(unsigned(std::min(items, ctas_max)));
-    const size_t bytes = kSmemBytes[aco ? 1 : 0];
     const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
+    // Multi-step launches pay where a step's tail is a large part of it: a
+    // few items per resident CTA (the 480^2 x64 batches: C4 -9%, C3 -10%).
+    // With many items per CTA (C5) the tail is negligible and the per-item
+    // dependency polls cost (C5 LEM +11%); with fewer items than CTAs
+    // (single 480^2 scenarios) the flag round trips cost more than the
+    // launches they replace (C1 +25%). Those take one launch per step.
+    if (b.nsteps > 1 && (mirror || big || items < ctas_max || items > 12 * ctas_max)) {
+        const int n = b.nsteps;
+        b.nsteps = 1;
+        int launches = 0;
+        for (int i = 0; i < n; ++i) launches += launch(b, slot_idx + i, parity ^ (i & 1), s);
+        return launches;
+    }
+    dim3 grid(unsigned(std::min(items * std::max(1, b.nsteps), ctas_max)));
+    const size_t bytes = kSmemBytes[aco ? 1 : 0];
     if (!aco && big) {
-        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLemBig, true, false>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<false, kCtasLemBig, false, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLemBig, true, false, false>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLemBig, false, false, false>, grid, bytes, s, b, slot_idx, parity);
     } else if (!aco) {
-        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<false, kCtasLem, false, true>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true, true, false>, grid, bytes, s, b, slot_idx, parity);
+        else if (b.nsteps > 1) launch_pdl(step_bits_kernel<false, kCtasLem, false, true, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<false, kCtasLem, false, true, false>, grid, bytes, s, b, slot_idx, parity);
     } else if (hbm) {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true, false>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasHbm, false, false>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true, false, false>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasHbm, false, false, false>, grid, bytes, s, b, slot_idx, parity);
     } else {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasDefault, false, true>, grid, bytes, s, b, slot_idx, parity);
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true, true, false>, grid, bytes, s, b, slot_idx, parity);
+        else if (b.nsteps > 1) launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, true>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, false>, grid, bytes, s, b, slot_idx, parity);
     }
     return 1;
 }

@@ -185,6 +185,7 @@ struct pf_ctx {
     cudaStream_t stream2 = nullptr;  // side stream for host<->device state transfers
     uint64_t launches = 0;
     std::map<std::pair<uint32_t, int>, cudaGraphExec_t> graphs;
+    std::map<std::pair<uint32_t, int>, uint64_t> graph_launches;  // kernel launches per replay
     std::vector<void*> allocs;
     Stager stage[2];                            // [0] main thread, [1] side thread
     void* io_scratch = nullptr;                 // device staging of exported SimState planes
@@ -197,6 +198,8 @@ struct pf_ctx {
     uint32_t* d_err = nullptr;
     uint32_t* remote_flag[2] = {nullptr, nullptr};
     int linked = 0;                             // bit s: neighbour on side s
+    bool multistep = true;                      // PF_KERNEL_FUSED, unlinked: one launch per batch of steps
+    size_t tile_done_bytes = 0;
     std::vector<void*> ipc_opened;              // peer allocations opened with cudaIpcOpenMemHandle
     // Phase-level stepping (pf_phase, PF_KERNEL_PIPELINE): 0 between steps,
     // else the last phase done + 1; CandidateScores by agent id.
@@ -393,6 +396,17 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->d_step = static_cast<uint32_t*>(alloc(4));
     ctx->d_sync = static_cast<uint32_t*>(alloc(8));
     ctx->d_err = static_cast<uint32_t*>(alloc(4));
+    if (ctx->bits()) {
+        // Per-tile completion flags of multi-step launches, sized for the
+        // smallest tile geometry (64-column strips, 8-row tiles).
+        ctx->tile_done_bytes = 4 * (size_t(cfg->replicas) * size_t((cfg->width + 63) / 64) *
+                                        size_t((ctx->rows_owned + 7) / 8) + 1);
+        ctx->args.tile_done = static_cast<uint32_t*>(alloc(ctx->tile_done_bytes));
+        ok = ok && ctx->args.tile_done;
+        const char* ms = std::getenv("PEDFLOW_MULTISTEP");  // dev: 0 = one launch per step
+        ctx->multistep = !(ms && std::atoi(ms) == 0);
+    }
+    ctx->args.nsteps = 1;
     ctx->args.bcount = static_cast<uint32_t*>(alloc(size_t(kReportCap) * 8));
     ok = ok && ctx->d_sync && ctx->d_err && ctx->args.bcount;
     ctx->args.sync_local = ctx->d_sync;
@@ -426,7 +440,8 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         (P.occ[1] && cudaMemsetAsync(P.occ[1], 0xFF, P.occ_plane * size_t(cfg->replicas) * 8, ctx->stream) != cudaSuccess) ||
         cudaMemsetAsync(ctx->d_step, 0, 4, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(ctx->d_sync, 0, 8, ctx->stream) != cudaSuccess ||
-        cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream) != cudaSuccess)
+        cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream) != cudaSuccess ||
+        (ctx->args.tile_done && cudaMemsetAsync(ctx->args.tile_done, 0, ctx->tile_done_bytes, ctx->stream) != cudaSuccess))
         return cleanup(fail(PF_ERR_CUDA, "cudaMemset failed"));
     if (P.intent) {
         ctx->launches += pfk::launch_fill_u8(P.intent, n, pfdev::kNone, ctx->stream);
@@ -560,6 +575,9 @@ static void set_step(pf_ctx* ctx, uint32_t step) {
     ctx->step = step;
     ctx->phase = 0;
     cudaMemcpyAsync(ctx->d_step, &ctx->step, 4, cudaMemcpyHostToDevice, ctx->stream);
+    // Multi-step launches wait for tile_done >= their steps: no flag may be
+    // ahead of the (possibly earlier) step the state is set to.
+    if (ctx->args.tile_done) cudaMemsetAsync(ctx->args.tile_done, 0, ctx->tile_done_bytes, ctx->stream);
     if (ctx->linked) {  // linked neighbours are (re)loaded to the same step
         const uint32_t sync[2] = {step, step};
         cudaMemcpyAsync(ctx->d_sync, sync, 8, cudaMemcpyHostToDevice, ctx->stream);
@@ -935,16 +953,25 @@ static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
 // Steps are stream-ordered; a handshake timeout (a neighbour that never
 // completed its step) is reported at the next synchronisation.
 static int check_halo(pf_ctx* ctx) {
-    if (!ctx->linked) return PF_OK;
+    if (!ctx->linked && !ctx->multistep) return PF_OK;
     uint32_t err = 0;
     PF_CUDA(cudaMemcpy(&err, ctx->d_err, 4, cudaMemcpyDeviceToHost));
-    if (err) return fail(PF_ERR_COMM, "fused halo exchange: a neighbour shard did not complete its step (timeout)");
+    if (err & 1u) return fail(PF_ERR_COMM, "fused halo exchange: a neighbour shard did not complete its step (timeout)");
+    if (err & 2u) return fail(PF_ERR_CUDA, "multi-step launch: a tile dependency wait timed out (internal error)");
     return PF_OK;
 }
 
-// Enqueue n <= kBatchCap steps (batch slots 0..n-1) with the given start parity.
+// Enqueue n <= kBatchCap steps (batch slots 0..n-1) with the given start
+// parity: one multi-step launch (PF_KERNEL_FUSED, unlinked contexts: steps
+// overlap at tile granularity, pf_bitstep.cuh) or one launch per step.
 static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
-    for (uint32_t i = 0; i < n; ++i) launch_one_step(ctx, i, (parity + int(i)) & 1);
+    if (ctx->cfg.kernel == PF_KERNEL_FUSED && ctx->multistep && !ctx->linked && n > 1) {
+        pfk::StepArgs b = ctx->args;
+        b.nsteps = int(n);
+        ctx->launches += pfk::launch_step_bits(b, 0, parity, ctx->stream);
+    } else {
+        for (uint32_t i = 0; i < n; ++i) launch_one_step(ctx, i, (parity + int(i)) & 1);
+    }
     ctx->launches += pfk::launch_advance_step(ctx->d_step, n, ctx->stream);
     return PF_OK;
 }
@@ -961,6 +988,7 @@ static int batch_graph(pf_ctx* ctx, uint32_t n, int parity, cudaGraphExec_t* out
         PF_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         enqueue_direct(ctx, n, parity);
         PF_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        ctx->graph_launches[key] = ctx->launches - before;
         ctx->launches = before;  // counted when replayed
         PF_CUDA(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
@@ -989,8 +1017,7 @@ static int enqueue_batch(pf_ctx* ctx, uint32_t n) {
     cudaGraphExec_t ge = nullptr;
     if (int rc = batch_graph(ctx, n, ctx->parity, &ge)) return rc;
     PF_CUDA(cudaGraphLaunch(ge, ctx->stream));
-    const uint32_t per_step = ctx->cfg.kernel == PF_KERNEL_PIPELINE ? 3 : 1;
-    ctx->launches += uint64_t(n) * per_step + 1;
+    ctx->launches += ctx->graph_launches[std::make_pair(n, ctx->parity)];
     ctx->parity ^= int(n & 1u);
     ctx->step += n;
     PF_CUDA(cudaGetLastError());
@@ -1357,6 +1384,7 @@ int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc
     ctx->linked |= 1 << side;
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // recaptured with the handshake
     ctx->graphs.clear();
+    ctx->graph_launches.clear();
     return PF_OK;
 }
 

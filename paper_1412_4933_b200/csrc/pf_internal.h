@@ -74,6 +74,12 @@ struct StepArgs {
     uint32_t* bcount;
     uint32_t* err;
     int peer_same_device;   // a linked neighbour shares this GPU: leave it resident slots (no in-kernel wait deadlock)
+    // Bit kernel, unlinked contexts: steps per launch (1, or a multi-step
+    // launch with tile-level dependencies) and the per-tile completion flags
+    // [replicas][strips][tiles] (last completed step + 1; zeroed whenever the
+    // step counter is set).
+    int nsteps;
+    uint32_t* tile_done;
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
