@@ -85,6 +85,44 @@ def test_replicas_match_single_runs(anchors):
         assert first_divergence(s, ora) == "identical"
 
 
+@pytest.mark.parametrize("model", ["lem", "aco"])
+def test_multistep_launch_matches_per_step_launches_and_oracle(model):
+    """Dense batches run as multi-step launches with tile-level dependencies
+    (pf_bitstep.cuh, launch()): 480^2 x 16 replicas at C3/C4 density (960
+    one-tile items per step on ~600 resident CTAs) in graph batches of 256,
+    100 and 1 steps must equal one launch per step (PEDFLOW_MULTISTEP=0) on
+    every replica and every plane, through the crowds' meeting (~step 130),
+    and the oracle on two replicas."""
+    import os
+
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    kw = dict(width=480, height=480, agents_per_side=51_200, model=model, seed=42)
+    cfg = to_config(kw)
+    R, steps = 16, 357
+    ens = {}
+    for flag in ("1", "0"):
+        os.environ["PEDFLOW_MULTISTEP"] = flag
+        try:
+            e = p.Ensemble(cfg, replicas=R)
+        finally:
+            os.environ.pop("PEDFLOW_MULTISTEP", None)
+        reps = [e.run(256), e.run(100), e.run(1)]
+        ens[flag] = (e, np.concatenate(reps, axis=1))
+    (em, rm), (es, rs) = ens["1"], ens["0"]
+    assert (rm == rs).all()
+    for i in range(R):
+        assert hashes_of(em.state(i)) == hashes_of(es.state(i)), f"replica {i}"
+    for i in (0, 11):
+        ora = OracleState(to_scenario(dict(kw, seed=42 + i)))
+        o = ora.run(steps)
+        assert (rm[i]["moved"] == o["moved"]).all()
+        assert first_divergence(em.state(i), ora) == "identical"
+    em.close()
+    es.close()
+
+
 def test_device_rng_matches_oracle():
     """Device Philox / uniform / AS241 normal vs the oracle (all three branches)."""
     from oracle.oracle import oracle

@@ -15,6 +15,8 @@ from paper_1412_4933_b200.engine import _pf_config  # noqa: E402
 from paper_1412_4933_b200.sharding import row_partition  # noqa: E402
 
 steps = int(os.environ.get("STEPS", "12"))
+if os.environ.get("SANITIZE_NO_LINK"):  # kernels one at a time: no in-kernel waits between CTAs either
+    os.environ["PEDFLOW_MULTISTEP"] = "0"
 C = p.ScenarioConfig
 for model in (p.Model.Lem, p.Model.Aco):
     # Small single grids take the small-grid geometry; the 64-replica 96^2
@@ -22,8 +24,9 @@ for model in (p.Model.Lem, p.Model.Aco):
     # 20-replica 624-wide LEM batch the 320-column / 32-row one.
     # Dense bands (96^2 with 3000 per side: 32 rows) put agents in the ghost
     # rows of the 4-way shard split from step 0.
+    # 192^2 x 64 (768 one-tile items per step) runs as multi-step launches.
     for w, h, n, reps in ((96, 96, 3000, 2), (624, 48, 6000, 1), (480, 64, 9000, 1), (96, 96, 3000, 64),
-                          (624, 96, 9000, 20)):
+                          (624, 96, 9000, 20), (192, 192, 6000, 64)):
         cfg = C(width=w, height=h, agents_per_side=n, model=model, seed=5)
         for kernel in ("fused", "tile", "pipeline"):
             e = p.Ensemble(cfg, replicas=reps, kernel=kernel)
