@@ -46,7 +46,7 @@ int32_t band_height(int32_t agents_per_side, int32_t width) {
     return int32_t((int64_t(agents_per_side) + width - 1) / width);
 }
 
-static void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
+void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
     const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
     const size_t nt = std::min<size_t>(hw, std::max<size_t>(1, n / (1u << 16)));
     if (nt <= 1) {

@@ -11,6 +11,9 @@ namespace pfhost {
 uint64_t philox_bits(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter);
 double uniform(uint64_t seed, uint32_t step, uint32_t phase, uint64_t entity, uint32_t counter);
 int32_t band_height(int32_t agents_per_side, int32_t width);
+// fn(begin, end) over [0, n) on up to hardware_concurrency threads (ranges of
+// at least 64K).
+void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn);
 
 // Keyed Fisher-Yates placement of one side (src/state.cpp:17-50): calls
 // put(global linear cell, agent id) for the n placed agents.
