@@ -85,16 +85,29 @@ def summarize(tag, specs):
              "on `python tools/profile_step.py <workload> S+2` (one launch at step S, named in each heading; cold "
              "caches, serialised: compare shares, not absolute times, with the bench).", ""]
     for spec in specs:
-        rep, workload = spec.split(":")
+        # rep:workload[:steps] -- steps > 1 for a multi-step launch (per-step traffic = launch / steps)
+        parts = spec.split(":")
+        rep, workload = parts[0], parts[1]
+        nsteps = int(parts[2]) if len(parts) > 2 else 1
         d = raw(rep)
         rd = to_bytes(*d["dram__bytes_read.sum"])
         wr = to_bytes(*d["dram__bytes_write.sum"])
-        traffic[workload] = rd + wr
-        lines += [f"## {workload} — `{os.path.basename(rep)}`", "", "| metric | value |", "|---|---|"]
+        traffic[workload] = (rd + wr) / nsteps
+        head = f"## {workload} — `{os.path.basename(rep)}`"
+        if nsteps > 1:
+            head += f" (one multi-step launch of {nsteps} steps)"
+        lines += [head, "", "| metric | value |", "|---|---|"]
         for key, name in KEYS:
             if key in d:
                 lines.append(f"| {name} (`{key}`) | {d[key][0]} {d[key][1]} |")
         lines.append(f"| DRAM read+write per launch | {(rd + wr) / 1e9:.3f} GB |")
+        if nsteps > 1:
+            lines.append(f"| DRAM read+write per step | {(rd + wr) / nsteps / 1e9:.3f} GB |")
+            dur = d.get("gpu__time_duration.sum")
+            if dur:
+                x = float(dur[0].replace(",", "")) * {"ns": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3,
+                                                      "nsecond": 1e-3}.get(dur[1], 1)
+                lines.append(f"| duration per step | {x / nsteps:.2f} us |")
         ph = phases(rep)
         if ph:
             lines += ["", "| phase (SASS between barriers) | stall samples % | instructions % | warp instructions |",

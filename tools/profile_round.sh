@@ -5,13 +5,20 @@
 #   python tools/ncu_summarize.py --launches TAG gpurun_out/launches_TAG.csv
 #   python tools/ncu_summarize.py TAG gpurun_out/TAG_c5_aco_s150.ncu-rep:c5_aco_step150 ...
 # 1. the launch list of the bench command (cold-cache, serialised per-launch times);
-# 2. one `ncu --set full` capture of the step kernel at step 150 (mid bench window) per workload.
+# 2. one `ncu --set full` capture of the step kernel at step 150 (mid bench window) per workload
+#    (for the x64 batches: the 10-step multi-step launch of steps 150..159).
 TAG=${1:-rXX}
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 60 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/${TAG}_bench_ncu.log 2>&1
-for w in c5_aco c5_lem c4_aco_x64 c3_lem_x64; do
+for w in c5_aco c5_lem; do
   timeout 300 ncu --set full --import-source on --clock-control none -k regex:step_bits -s 150 -c 1 \
     -o gpurun_out/${TAG}_${w}_s150 python tools/profile_step.py $w 152 > gpurun_out/${TAG}_$w.log 2>&1
+done
+# The dense 480^2 x64 batches run each graph batch as one multi-step launch:
+# capture the launch of steps 150..159 (per-step figures = launch / 10).
+for w in c4_aco_x64 c3_lem_x64; do
+  timeout 300 ncu --set full --import-source on --clock-control none -k regex:step_bits -s 1 -c 1 \
+    -o gpurun_out/${TAG}_${w}_s150 python tools/profile_step.py $w 150 fused 10 > gpurun_out/${TAG}_$w.log 2>&1
 done
