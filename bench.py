@@ -303,10 +303,23 @@ def secondary_runs(steps):
         n = min(steps if not name.startswith("c5") else 300, 1024)
         ens.ctx.prepare_steps(n)
         tot, _ = ens.time_steps(n)
-        movers = float(ens.ctx.read_reports(n)["moved"].astype(np.int64).sum()) / n
+        moved = ens.ctx.read_reports(n)["moved"].astype(np.int64)  # [replica][step 5 + i]
+        movers = float(moved.sum()) / n
         _, ker = ens.time_steps(min(n, 50), kernel=True)
         model = "lem" if cfg.model == p.Model.Lem else "aco"
         rl = roofline_pair(cfg.width, cfg.height, model, reps, cfg.agents_per_side, movers, tot / n, peak)
+        # ncu's DRAM traffic (profiles/ncu_traffic.json) was captured at step
+        # 150 (the x64 batches: steps 150..159): compare it with the byte
+        # models at those steps' movers.
+        tw = (150, 160) if name.endswith("_x64") else (150, 151)
+        traffic = ncu_traffic(name)
+        tcmp = None
+        if traffic and moved.shape[1] >= tw[1] - 5:
+            mv = float(moved[:, tw[0] - 5:tw[1] - 5].sum()) / (tw[1] - tw[0])
+            ab = alg_bytes_bitplane(cfg.width, cfg.height, model, reps, mv)
+            asv = alg_bytes_survey(cfg.width, cfg.height, model, reps, cfg.agents_per_side)
+            tcmp = {"steps": f"{tw[0]}..{tw[1] - 1}", "movers_per_step": mv, "traffic_per_step": traffic,
+                    "over_bitplane": traffic / ab, "over_survey": traffic / asv}
         out[name] = {
             "workload": desc, "window": f"steps 5..{5 + n}", "ms_per_step": tot / n,
             "kernel_ms_isolated_launch_events": ker,
@@ -316,9 +329,25 @@ def secondary_runs(steps):
             "roofline_frac": rl["survey"]["frac"], "roofline_frac_bitplane": rl["bitplane"]["frac"],
             "alg_bytes_per_step": rl["survey"]["alg_bytes_per_launch"],
             "alg_bytes_per_step_bitplane": rl["bitplane"]["alg_bytes_per_launch"],
-            "traffic": ncu_traffic(name),
+            "traffic": traffic, "traffic_vs_models": tcmp,
         }
         ens.close()
+    # C5 ACO with fp32 pheromone storage (PF_KERNEL_FUSED_F32): tolerance-only
+    # parity (tests/test_f32_pheromone.py), half the pheromone stream.
+    cfg, reps, desc = scenario("c5_aco")
+    ens = p.Ensemble(cfg, replicas=1, kernel="fused_f32")
+    ens.run(5)
+    ens.ctx.prepare_steps(300)
+    tot, _ = ens.time_steps(300)
+    mv = float(ens.ctx.read_reports(300)["moved"].astype(np.int64).sum()) / 300
+    b32 = alg_bytes_bitplane(cfg.width, cfg.height, "aco", 1, mv) - 16 * cfg.width * cfg.height
+    out["c5_aco_f32"] = {
+        "workload": desc + ", pheromone stored as fp32 (tolerance-only; fp64 arithmetic, one rounding per store)",
+        "window": "steps 5..305", "ms_per_step": tot / 300,
+        "agent_updates_per_s": 2 * cfg.agents_per_side * 300 / (tot / 1e3),
+        "alg_bytes_per_step_bitplane_f32": b32, "roofline_frac_bitplane_f32": b32 / (tot / 300 / 1e3) / 1e9 / peak,
+        "note": "not the headline: the reference's fields are fp64 and this mode is not bit-exact (DESIGN.md §4)"}
+    ens.close()
     # C5 ACO as linked shards on this one GPU
     cfg, reps, desc = scenario("c5_aco")
     shard = {}

@@ -35,6 +35,9 @@ extern "C" {
 #define PF_KERNEL_FUSED 0    /* one bit-sliced kernel per step on occupancy bit planes (default) */
 #define PF_KERNEL_PIPELINE 1 /* propose / resolve / commit, three kernels per step */
 #define PF_KERNEL_TILE 2     /* one kernel per step, scalar per-cell shared-memory tile */
+#define PF_KERNEL_FUSED_F32 3 /* PF_KERNEL_FUSED with the ACO pheromone stored as fp32 (arithmetic still
+                               * fp64, one rounding per store): half the pheromone traffic,
+                               * tolerance-only parity; LEM runs as PF_KERNEL_FUSED */
 
 /* Number of ghost rows kept above and below a row shard: one step's
  * dependency radius. */
@@ -51,7 +54,7 @@ typedef struct pf_config {
     int32_t row_begin; /* owned global rows [row_begin, row_end) of a row shard; */
     int32_t row_end;   /* row_end == 0 means the whole grid */
     int32_t device;    /* CUDA device ordinal */
-    int32_t kernel;    /* PF_KERNEL_FUSED, PF_KERNEL_PIPELINE or PF_KERNEL_TILE */
+    int32_t kernel;    /* PF_KERNEL_FUSED, PF_KERNEL_PIPELINE, PF_KERNEL_TILE or PF_KERNEL_FUSED_F32 */
 } pf_config;
 
 /* Byte-identical to pedflow::AgentRecord (inc/grid.hpp:84-93), 40 bytes. */

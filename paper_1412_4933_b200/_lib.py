@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("PEDFLOW_B200_LIB") or os.path.join(HERE, "libpedflow_
 
 PF_OK, PF_ERR_CONFIG, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, 2, 3, 4, 5, 6
 PF_MODEL_LEM, PF_MODEL_ACO = 0, 1
-PF_KERNEL_FUSED, PF_KERNEL_PIPELINE, PF_KERNEL_TILE = 0, 1, 2
+PF_KERNEL_FUSED, PF_KERNEL_PIPELINE, PF_KERNEL_TILE, PF_KERNEL_FUSED_F32 = 0, 1, 2, 3
 PF_PHASE_SCORE, PF_PHASE_INTENTION, PF_PHASE_MOVEMENT, PF_PHASE_RESET = 0, 1, 2, 3
 PF_GHOST_ROWS = 3
 

@@ -202,6 +202,26 @@ __device__ __forceinline__ int slot(int base, int sr) {
 
 __device__ __forceinline__ uint32_t empty_of(uint2 p) { return ~(p.x | p.y); }
 
+// Pheromone storage per cell: {top, bottom} as fp64 (double2, the product,
+// bit-exact) or fp32 (float2, PF_KERNEL_FUSED_F32, tolerance-only). All
+// arithmetic is fp64 (the reference's order and rounding); an fp32 store
+// rounds the result once.
+template <class TV> struct Tau;
+template <> struct Tau<double2> {
+    using S = double;
+    __device__ __forceinline__ static double2 make(double a, double b) { return make_double2(a, b); }
+};
+template <> struct Tau<float2> {
+    using S = float;
+    __device__ __forceinline__ static float2 make(double a, double b) {
+        return make_float2(__double2float_rn(a), __double2float_rn(b));
+    }
+};
+template <class TV>
+__device__ __forceinline__ TV evaporated(TV t, double f) {
+    return Tau<TV>::make(__dmul_rn(double(t.x), f), __dmul_rn(double(t.y), f));
+}
+
 // Emptiness around one intent unit: the eight neighbour planes, shifted so
 // bit j is the neighbour of column j.
 struct Around {
@@ -302,9 +322,9 @@ __device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t 
 // lem_select / aco_select (src/lem.cpp:28-60, src/aco.cpp:64-92). The agent's
 // id (the selection key, src/engine.cpp:82) is read from its cell word: the
 // cell is occupied at step start, so no thread writes it during this step.
-template <bool ACO>
+template <bool ACO, class TV>
 __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, int base, const uint32_t* cells,
-                                           const double2* __restrict__ tin, int di, int si, int j, bool bottom,
+                                           const TV* __restrict__ tin, int di, int si, int j, bool bottom,
                                            int r0, int c0, uint64_t seed, uint32_t step) {
     const int sr = di + 1;
     const int W = a.k.W;
@@ -328,12 +348,13 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
         // buffer, while a closed one may lie outside it (an agent in a
         // shard's first ghost row at column 0 has its (-1,-1) neighbour
         // before the start of the allocation).
-        const double* t0 = reinterpret_cast<const double*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
+        using S = typename Tau<TV>::S;
+        const S* t0 = reinterpret_cast<const S*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
         double tn[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-            tn[i] = (open >> i & 1u) ? __ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code])) : 0.0;
+            tn[i] = (open >> i & 1u) ? double(__ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code]))) : 0.0;
         }
         double num[8];
 #pragma unroll
@@ -581,7 +602,7 @@ __device__ __forceinline__ void signal_boundary(const StepArgs& a, int sides, ui
 // harmless there as here). Called by the whole CTA after the end-of-tile
 // barrier; the system fence orders the stores before the step's completion
 // flag (signal_boundary).
-template <bool ACO>
+template <bool ACO, class TV>
 __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int rep, int strip, int r0) {
     const int W = a.k.W;
     const int c0 = strip * NS * 32, ncols = min(NS * 32, W - c0);
@@ -599,7 +620,7 @@ __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int r
                 pr.cell[dst + i] = a.p.cell[0][src + i];
                 if (ACO) {
                     pr.tour[dst + i] = a.p.tour[src + i];
-                    pr.tau[parity ^ 1][dst + i] = a.p.tau[parity ^ 1][src + i];
+                    reinterpret_cast<TV*>(pr.tau[parity ^ 1])[dst + i] = reinterpret_cast<const TV*>(a.p.tau[parity ^ 1])[src + i];
                 }
             }
             if (threadIdx.x < NS) {
@@ -617,7 +638,7 @@ __device__ __forceinline__ void mirror_tile(const StepArgs& a, int parity, int r
 // and the per-segment form is 1-2% faster.
 // MULTI: compiled with the multi-step (tile-dependency) logic; instantiated
 // only for the dense-grid variants that launch() runs that way.
-template <bool ACO, int CTAS, bool MIRROR, bool COMPACT, bool MULTI>
+template <bool ACO, int CTAS, bool MIRROR, bool COMPACT, bool MULTI, class TV = double2>
 __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, int slot_idx, int parity) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -698,8 +719,8 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     const size_t plane_base = size_t(rep) * a.p.plane;
     uint32_t* const cw = cells + plane_base;
     uint2* const oout = a.p.occ[par ^ 1] + size_t(rep) * a.p.occ_plane + size_t(it.strip) * NS + 2;
-    const double2* __restrict__ tin = ACO ? a.p.tau[par] + plane_base : nullptr;
-    double2* __restrict__ tout = ACO ? a.p.tau[par ^ 1] + plane_base : nullptr;
+    const TV* __restrict__ tin = ACO ? reinterpret_cast<const TV*>(a.p.tau[par]) + plane_base : nullptr;
+    TV* __restrict__ tout = ACO ? reinterpret_cast<TV*>(a.p.tau[par ^ 1]) + plane_base : nullptr;
     double* __restrict__ tour = ACO ? a.p.tour + plane_base : nullptr;
     int next_base = 0;
 
@@ -810,7 +831,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 list_entry(sm, ne, e, u, j);
                 const int di = u / SS, si = u - di * SS;
                 const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
-                const int code = draw_intent<ACO>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
+                const int code = draw_intent<ACO, TV>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
                 atomicOr(&sm.D[code][di][si + 1], 1u << j);
             }
             __syncthreads();
@@ -890,25 +911,25 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 if (lane < NS) orow[lane] = sm.pl[rs][lane + 2];
                 if (ACO) {
                     const size_t r0c = size_t(b) * W + c0 + lane;
-                    double2 tc[NS];
+                    TV tc[NS];
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
-                        tc[s] = (c0 + 32 * s + lane < W) ? tin[r0c + 32 * s] : make_double2(0.0, 0.0);
+                        tc[s] = (c0 + 32 * s + lane < W) ? tin[r0c + 32 * s] : Tau<TV>::make(0.0, 0.0);
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
                         if (c0 + 32 * s + lane < W)
-                            tout[r0c + 32 * s] = make_double2(__dmul_rn(tc[s].x, a.k.factor), __dmul_rn(tc[s].y, a.k.factor));
+                            tout[r0c + 32 * s] = evaporated(tc[s], a.k.factor);
                 }
                 continue;
             }
             const size_t row0 = size_t(b) * W + c0 + lane;  // this lane's cell in segment 1
             // ACO: issue the whole row's pheromone loads before using any of them
             // (and before the arrival-source fetch, so both round trips overlap).
-            double2 tv[NS];
+            TV tv[NS];
             if (ACO) {
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
-                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : make_double2(0.0, 0.0);
+                    tv[s] = (c0 + 32 * s + lane < W) ? tin[row0 + 32 * s] : Tau<TV>::make(0.0, 0.0);
             }
             if constexpr (COMPACT) {
                 // The row's arrivals, compacted: arrival e (column order) is lane
@@ -979,8 +1000,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                     e0 += __popc(Am);
                     if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
                         if (ACO && valid) {
-                            const double2 tt = tv[si - 1];
-                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+                            tout[gi] = evaporated(tv[si - 1], a.k.factor);
                         }
                     } else {
                         const bool arrived = bit(Am, lane) != 0u;
@@ -989,15 +1009,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                         np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
                         np.y = (np.y & ~Gm) | (Am & ~top);
                         if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
-                            double2 tt = tv[si - 1];
-                            tt.x = __dmul_rn(tt.x, a.k.factor);
-                            tt.y = __dmul_rn(tt.y, a.k.factor);
+                            double tx = __dmul_rn(double(tv[si - 1].x), a.k.factor);
+                            double ty = __dmul_rn(double(tv[si - 1].y), a.k.factor);
                             if (arrived) {
                                 const double dep = atr[ea];
-                                if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
-                                else tt.y = __dadd_rn(tt.y, dep);
+                                if (group == 1u) tx = __dadd_rn(tx, dep);
+                                else ty = __dadd_rn(ty, dep);
                             }
-                            tout[gi] = tt;
+                            tout[gi] = Tau<TV>::make(tx, ty);
                         }
                     }
                     if (lane == si - 1) mine = np;
@@ -1030,8 +1049,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                     const size_t gi = row0 + 32 * (si - 1);
                     if ((Am | Gm) == 0u) {  // warp-uniform: nothing moves in this segment
                         if (ACO && valid) {
-                            const double2 tt = tv[si - 1];
-                            tout[gi] = make_double2(__dmul_rn(tt.x, a.k.factor), __dmul_rn(tt.y, a.k.factor));
+                            tout[gi] = evaporated(tv[si - 1], a.k.factor);
                         }
                     } else {
                         const bool arrived = bit(Am, lane) != 0u;
@@ -1061,15 +1079,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                         np.x = (np.x & ~Gm) | top;  // vacated sources clear, arrivals set
                         np.y = (np.y & ~Gm) | bot;
                         if (ACO && valid) {  // evaporate, then deposit (src/engine.cpp:124-131, src/aco.cpp:119-123)
-                            double2 tt = tv[si - 1];
-                            tt.x = __dmul_rn(tt.x, a.k.factor);
-                            tt.y = __dmul_rn(tt.y, a.k.factor);
+                            double tx = __dmul_rn(double(tv[si - 1].x), a.k.factor);
+                            double ty = __dmul_rn(double(tv[si - 1].y), a.k.factor);
                             if (arrived) {
                                 const double dep = __ddiv_rn(a.k.q, tour_new);
-                                if (group == 1u) tt.x = __dadd_rn(tt.x, dep);
-                                else tt.y = __dadd_rn(tt.y, dep);
+                                if (group == 1u) tx = __dadd_rn(tx, dep);
+                                else ty = __dadd_rn(ty, dep);
                             }
-                            tout[gi] = tt;
+                            tout[gi] = Tau<TV>::make(tx, ty);
                         }
                     }
                     if (lane == si - 1) mine = np;
@@ -1078,7 +1095,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             }
         }
         __syncthreads();  // end of tile: the window's slots may be refilled
-        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO>(a, par, rep, it.strip, r0);
+        if (MIRROR && (r0 < kGhost || r0 + RT > a.rows_owned - kGhost)) mirror_tile<ACO, TV>(a, par, rep, it.strip, r0);
         base = slot(base, RT);
         cur ^= 1;
     }
@@ -1143,16 +1160,24 @@ constexpr int kCtasHbm = kCtasDefault > 1 && NT == 256 ? 3 : kCtasDefault;
 constexpr int kCtasLemBig = NT == 256 && smem_ctas(false) >= 5 ? 5 : kCtasLem;
 static_assert(kCtasLem >= 1 && kCtasDefault >= 1, "shared memory must fit one CTA per SM");
 
+template <class TV>
+int configure_aco(int bytes) {
+    for (auto f : {step_bits_kernel<true, kCtasDefault, false, true, false, TV>,
+                   step_bits_kernel<true, kCtasHbm, false, false, false, TV>,
+                   step_bits_kernel<true, kCtasDefault, true, true, false, TV>,
+                   step_bits_kernel<true, kCtasHbm, true, false, false, TV>,
+                   step_bits_kernel<true, kCtasDefault, false, true, true, TV>})
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
+    return 0;
+}
+
 int configure() {
     const int lem = int(kSmemBytes[0]), aco = int(kSmemBytes[1]);
     for (auto f : {step_bits_kernel<false, kCtasLem, false, true, false>, step_bits_kernel<false, kCtasLem, true, true, false>,
                    step_bits_kernel<false, kCtasLem, false, true, true>,
                    step_bits_kernel<false, kCtasLemBig, false, false, false>, step_bits_kernel<false, kCtasLemBig, true, false, false>})
         if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lem) != cudaSuccess) return 1;
-    for (auto f : {step_bits_kernel<true, kCtasDefault, false, true, false>, step_bits_kernel<true, kCtasHbm, false, false, false>,
-                   step_bits_kernel<true, kCtasDefault, true, true, false>, step_bits_kernel<true, kCtasHbm, true, false, false>,
-                   step_bits_kernel<true, kCtasDefault, false, true, true>})
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, aco) != cudaSuccess) return 1;
+    if (configure_aco<double2>(aco) || configure_aco<float2>(aco)) return 1;
     return 0;
 }
 
@@ -1172,6 +1197,19 @@ static void launch_pdl(Kernel kernel, dim3 grid, size_t smem, cudaStream_t s, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kernel, b, slot_idx, parity);
+}
+
+template <class TV>
+static void launch_aco(const StepArgs& b, bool hbm, bool mirror, dim3 grid, size_t bytes, cudaStream_t s, int slot_idx,
+                       int parity) {
+    if (hbm) {
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true, false, false, TV>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasHbm, false, false, false, TV>, grid, bytes, s, b, slot_idx, parity);
+    } else {
+        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true, true, false, TV>, grid, bytes, s, b, slot_idx, parity);
+        else if (b.nsteps > 1) launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, true, TV>, grid, bytes, s, b, slot_idx, parity);
+        else launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, false, TV>, grid, bytes, s, b, slot_idx, parity);
+    }
 }
 
 // Persistent grid: one CTA per resident slot (SMs x 3, 4 or 5) at most. Work
@@ -1216,13 +1254,10 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
         if (mirror) launch_pdl(step_bits_kernel<false, kCtasLem, true, true, false>, grid, bytes, s, b, slot_idx, parity);
         else if (b.nsteps > 1) launch_pdl(step_bits_kernel<false, kCtasLem, false, true, true>, grid, bytes, s, b, slot_idx, parity);
         else launch_pdl(step_bits_kernel<false, kCtasLem, false, true, false>, grid, bytes, s, b, slot_idx, parity);
-    } else if (hbm) {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasHbm, true, false, false>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasHbm, false, false, false>, grid, bytes, s, b, slot_idx, parity);
+    } else if (b.tau_f32) {  // (large grids: 3 CTAs/SM as for fp64; 4 measured 7.5% slower at C5)
+        launch_aco<float2>(b, hbm, mirror, grid, bytes, s, slot_idx, parity);
     } else {
-        if (mirror) launch_pdl(step_bits_kernel<true, kCtasDefault, true, true, false>, grid, bytes, s, b, slot_idx, parity);
-        else if (b.nsteps > 1) launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, true>, grid, bytes, s, b, slot_idx, parity);
-        else launch_pdl(step_bits_kernel<true, kCtasDefault, false, true, false>, grid, bytes, s, b, slot_idx, parity);
+        launch_aco<double2>(b, hbm, mirror, grid, bytes, s, slot_idx, parity);
     }
     return 1;
 }

@@ -209,7 +209,11 @@ struct pf_ctx {
     std::vector<int32_t> rep_aps;               // agents_per_side of each replica
     std::vector<pfdev::ReplicaParams> reps;     // host copy of args.rep
     bool aco() const { return cfg.model == PF_MODEL_ACO; }
-    bool bits() const { return cfg.kernel == PF_KERNEL_FUSED; }  // occupancy planes + in-place words
+    bool bits() const { return cfg.kernel == PF_KERNEL_FUSED || cfg.kernel == PF_KERNEL_FUSED_F32; }  // occupancy planes + in-place words
+    bool f32() const { return cfg.kernel == PF_KERNEL_FUSED_F32 && aco(); }  // pheromone stored as float2
+    size_t tau_elem() const { return f32() ? 8 : 16; }
+    // Element `elem` of pheromone buffer `buf` (double2 or float2 storage).
+    void* tau_ptr(int buf, size_t elem) const { return reinterpret_cast<char*>(args.p.tau[buf]) + elem * tau_elem(); }
     size_t plane() const { return size_t(rows_buf) * size_t(cfg.width); }
     size_t total() const { return plane() * size_t(cfg.replicas); }
 };
@@ -246,7 +250,8 @@ int pf_validate(const pf_config* c) {
     if (2 * int64_t(c->agents_per_side) >= (int64_t(1) << 29)) return fail(PF_ERR_CONFIG, "2 * agents_per_side must be < 2^29");
     if (c->replicas < 1) return fail(PF_ERR_CONFIG, "replicas must be >= 1");
     if (c->replicas > 65535) return fail(PF_ERR_CONFIG, "replicas must be <= 65535");
-    if (c->kernel != PF_KERNEL_FUSED && c->kernel != PF_KERNEL_PIPELINE && c->kernel != PF_KERNEL_TILE)
+    if (c->kernel != PF_KERNEL_FUSED && c->kernel != PF_KERNEL_PIPELINE && c->kernel != PF_KERNEL_TILE &&
+        c->kernel != PF_KERNEL_FUSED_F32)
         return fail(PF_ERR_CONFIG, "unknown kernel");
     if (c->row_end != 0) {
         if (c->row_begin < 0 || c->row_end > c->height || c->row_begin >= c->row_end)
@@ -411,6 +416,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
         ctx->multistep = !(ms && std::atoi(ms) == 0);
     }
     ctx->args.nsteps = 1;
+    ctx->args.tau_f32 = ctx->f32() ? 1 : 0;
     ctx->args.bcount = static_cast<uint32_t*>(alloc(size_t(kReportCap) * 8));
     ok = ok && ctx->d_sync && ctx->d_err && ctx->args.bcount;
     ctx->args.sync_local = ctx->d_sync;
@@ -563,12 +569,12 @@ static int finish_replica_upload(pf_ctx* ctx, int rep, const std::vector<double>
     if (ctx->aco()) {
         if (tour) PF_CUDA(ctx->stage[0].h2d(P.tour + off, tour->data(), ctx->plane() * 8, ctx->stream));
         else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
-        if (tau) {
+        if (tau && !ctx->f32()) {
             PF_CUDA(ctx->stage[0].h2d(P.tau[0] + off, tau->data(), ctx->plane() * 16, ctx->stream));
             PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
         } else {
-            ctx->launches += pfk::launch_fill_tau(P.tau[0] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
-            ctx->launches += pfk::launch_fill_tau(P.tau[1] + off, ctx->plane(), ctx->cfg.tau0, ctx->stream);
+            ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(0, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
+            ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(1, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
         }
     }
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -686,7 +692,7 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     const size_t win = size_t(g_hi - g_lo) * W;
     const size_t plane = ctx->plane();
     const size_t need = up256(win) + up256(win * 4) + up256(size_t(n_agents) * 40) + up256(plane * 4) +
-                        (ctx->aco() ? up256(plane * 8) : 0) + 16;
+                        (ctx->aco() ? up256(plane * 8) : 0) + (ctx->f32() ? up256(win * 16) : 0) + 16;
     if (int rc = ensure_scratch(ctx, need)) return rc;
     if (!ctx->io_event) PF_CUDA(cudaEventCreateWithFlags(&ctx->io_event, cudaEventDisableTiming));
     char* sp = static_cast<char*>(ctx->io_scratch);
@@ -700,12 +706,15 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     char* d_agents = take(size_t(n_agents) * 40);
     auto* d_words = reinterpret_cast<uint32_t*>(take(plane * 4));
     double* d_tour = ctx->aco() ? reinterpret_cast<double*>(take(plane * 8)) : nullptr;
-    auto* d_status = reinterpret_cast<unsigned long long*>(sp);
     // Pheromone fields go up on a helper thread into the non-current ping-pong
     // buffer (scratch until the state is known to be valid).
+    // (fp32 storage: the f64 fields go to the transfer scratch instead.)
     const int cur = ctx->parity;
-    double* d_top = ctx->aco() ? reinterpret_cast<double*>(P.tau[cur ^ 1] + off) : nullptr;
-    double* d_bot = d_top ? d_top + plane : nullptr;
+    double* d_top = !ctx->aco() ? nullptr
+                    : ctx->f32() ? reinterpret_cast<double*>(take(win * 16))
+                                 : reinterpret_cast<double*>(P.tau[cur ^ 1] + off);
+    double* d_bot = d_top ? d_top + (ctx->f32() ? win : plane) : nullptr;
+    auto* d_status = reinterpret_cast<unsigned long long*>(sp);
     cudaError_t side_err = cudaSuccess;
     std::thread side;
     if (ctx->aco()) {
@@ -758,11 +767,12 @@ int pf_load_state(pf_ctx* ctx, int32_t rep, const uint8_t* occ, const uint32_t* 
     if (e == cudaSuccess && ctx->aco()) {
         // Interleave the two fields into {top, bottom} pairs (ghost rows
         // outside the grid hold zeros), then mirror into the scratch buffer.
-        e = cudaMemsetAsync(P.tau[cur] + off, 0, plane * 16, ctx->stream);
-        ctx->launches += pfk::launch_interleave_tau(P.tau[cur] + off + b_lo * W, d_top, d_bot, win, ctx->stream);
+        e = cudaMemsetAsync(ctx->tau_ptr(cur, off), 0, plane * ctx->tau_elem(), ctx->stream);
+        ctx->launches += pfk::launch_interleave_tau(ctx->tau_ptr(cur, off + b_lo * W), d_top, d_bot, win, ctx->f32(),
+                                                    ctx->stream);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(P.tau[cur ^ 1] + off, P.tau[cur] + off, plane * 16, cudaMemcpyDeviceToDevice,
-                                ctx->stream);
+            e = cudaMemcpyAsync(ctx->tau_ptr(cur ^ 1, off), ctx->tau_ptr(cur, off), plane * ctx->tau_elem(),
+                                cudaMemcpyDeviceToDevice, ctx->stream);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return fail(PF_ERR_CUDA, std::string("state upload: ") + cudaGetErrorString(e));
@@ -801,8 +811,10 @@ static int store_whole(pf_ctx* ctx, int rep, uint8_t* occ, uint32_t* index, pf_a
                                               d_status, ctx->stream);
     double* top = nullptr;
     if (ctx->aco() && (tau_top || tau_bot)) {
+        // f64 scratch in the other ping-pong buffer (16 B per cell are allocated in both storage modes)
         top = reinterpret_cast<double*>(P.tau[ctx->parity ^ 1] + off);
-        ctx->launches += pfk::launch_deinterleave_tau(top, top + own, P.tau[ctx->parity] + off, own, ctx->stream);
+        ctx->launches += pfk::launch_deinterleave_tau(top, top + own, ctx->tau_ptr(ctx->parity, off), own, ctx->f32(),
+                                                      ctx->stream);
     }
     PF_CUDA(cudaEventRecord(ctx->io_event, ctx->stream));
     PF_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->io_event, 0));
@@ -870,7 +882,8 @@ int pf_store_state(pf_ctx* ctx, int32_t rep, uint8_t* occ, uint32_t* index, pf_a
         PF_CUDA(cudaMalloc(&d_pa, std::max<size_t>(8, size_t(n_agents) * 8)));
         double* top = reinterpret_cast<double*>(P.tau[ctx->parity ^ 1] + off);
         double* bot = top + own;
-        ctx->launches += pfk::launch_deinterleave_tau(top, bot, P.tau[ctx->parity] + off, own, ctx->stream);
+        ctx->launches += pfk::launch_deinterleave_tau(top, bot, ctx->tau_ptr(ctx->parity, off), own, ctx->f32(),
+                                                      ctx->stream);
         ctx->launches += pfk::launch_gather_tour(d_pa, P.cell[ctx->parity] + off, P.tour + off, own, ctx->stream);
         side = std::thread([&, top, bot] {
             cudaSetDevice(c.device);
@@ -947,7 +960,8 @@ static int launch_one_step(pf_ctx* ctx, uint32_t i, int parity) {
     // Linked shards: the step kernel itself orders its boundary items against
     // the neighbours' (wait_boundary / signal_boundary in pf_bitstep.cuh).
     switch (ctx->cfg.kernel) {
-        case PF_KERNEL_FUSED: ctx->launches += pfk::launch_step_bits(ctx->args, int(i), parity, ctx->stream); break;
+        case PF_KERNEL_FUSED:
+        case PF_KERNEL_FUSED_F32: ctx->launches += pfk::launch_step_bits(ctx->args, int(i), parity, ctx->stream); break;
         case PF_KERNEL_TILE: ctx->launches += pfk::launch_step_fused(ctx->args, int(i), parity, ctx->stream); break;
         default: ctx->launches += pfk::launch_step_pipeline(ctx->args, int(i), parity, ctx->stream); break;
     }
@@ -969,7 +983,7 @@ static int check_halo(pf_ctx* ctx) {
 // parity: one multi-step launch (PF_KERNEL_FUSED, unlinked contexts: steps
 // overlap at tile granularity, pf_bitstep.cuh) or one launch per step.
 static int enqueue_direct(pf_ctx* ctx, uint32_t n, int parity) {
-    if (ctx->cfg.kernel == PF_KERNEL_FUSED && ctx->multistep && !ctx->linked && n > 1) {
+    if (ctx->bits() && ctx->multistep && !ctx->linked && n > 1) {
         pfk::StepArgs b = ctx->args;
         b.nsteps = int(n);
         ctx->launches += pfk::launch_step_bits(b, 0, parity, ctx->stream);
@@ -1169,8 +1183,8 @@ int pf_halo(pf_ctx* ctx, int32_t rep, int32_t side, int32_t recv, pf_halo_rows* 
         out->occ_bytes = 0;
     }
     if (ctx->aco()) {
-        out->tau = P.tau[ctx->parity] + off + size_t(first) * W;
-        out->tau_bytes = size_t(G) * W * 16;
+        out->tau = ctx->tau_ptr(ctx->parity, off + size_t(first) * W);
+        out->tau_bytes = size_t(G) * W * ctx->tau_elem();
         out->tour = P.tour + off + size_t(tour_row) * W;
         out->tour_bytes = W * 8;
     } else {
@@ -1336,7 +1350,8 @@ int pf_peer_export(pf_ctx* ctx, pf_peer_desc* out) {
 int pf_peer_attach(pf_ctx* ctx, int32_t side, const pf_peer_desc* d, int32_t ipc) {
     if (!ctx || !d) return fail(PF_ERR_ARG, "null argument");
     if (side != 0 && side != 1) return fail(PF_ERR_ARG, "side must be 0 (above) or 1 (below)");
-    if (!ctx->bits() || d->kernel != PF_KERNEL_FUSED) return fail(PF_ERR_CONFIG, "the fused halo exchange needs PF_KERNEL_FUSED");
+    if (!ctx->bits() || d->kernel != ctx->cfg.kernel)
+        return fail(PF_ERR_CONFIG, "the fused halo exchange needs PF_KERNEL_FUSED (or _F32) on both sides");
     if (d->width != ctx->cfg.width || d->replicas != ctx->cfg.replicas || d->model != ctx->cfg.model)
         return fail(PF_ERR_COMM, "neighbour shard has a different grid width, replica count or model");
     const bool adjacent = side == 0 ? d->row_begin + d->rows_owned == ctx->row_begin

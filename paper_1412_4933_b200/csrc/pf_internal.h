@@ -26,7 +26,7 @@ struct Planes {
     uint2* occ[2];
     size_t occ_plane;   // uint2 elements per replica = rows_buf * wsp
     int wsp;
-    double2* tau[2];    // ping-pong {top, bottom} pheromone (ACO)
+    double2* tau[2];    // ping-pong {top, bottom} pheromone (ACO); float2 data when StepArgs::tau_f32
     double* tour;       // cell-resident tour length, updated in place (ACO)
     uint8_t* intent;    // pipeline-kernel scratch
     uint8_t* win;       // pipeline-kernel scratch
@@ -80,6 +80,10 @@ struct StepArgs {
     // step counter is set).
     int nsteps;
     uint32_t* tile_done;
+    // ACO pheromone storage: 0 = {f64, f64} per cell (the product), 1 =
+    // {f32, f32} (PF_KERNEL_FUSED_F32, tolerance-only); Planes::tau then
+    // points at float2 data.
+    int tau_f32;
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
@@ -99,8 +103,8 @@ int launch_step_fused(const StepArgs& a, int slot, int parity, cudaStream_t s); 
 int launch_step_pipeline(const StepArgs& a, int slot, int parity, cudaStream_t s);
 // *d_step += n
 int launch_advance_step(uint32_t* d_step, uint32_t n, cudaStream_t s);
-// Fill a tau plane range with {v, v}.
-int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s);
+// Fill a tau plane range with {v, v} (f32: float2 elements, v rounded).
+int launch_fill_tau(void* p, size_t n, double v, int f32, cudaStream_t s);
 int launch_fill_u8(uint8_t* p, size_t n, uint8_t v, cudaStream_t s);
 // words[(row - g_lo) * W + col] = (first_id + k) | group << 30 for cells[k] on
 // buffer rows [0, rows) (row = cells[k] / W).
@@ -109,8 +113,9 @@ int launch_scatter_placement(uint32_t* words, const uint32_t* cells, uint32_t n,
 int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agents, uint32_t* seen,
                  unsigned long long* counts, cudaStream_t s);
 // State upload / download layout transforms.
-int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s);
-int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s);
+// (f32: the tau plane holds float2 elements; the reference fields are f64)
+int launch_interleave_tau(void* dst, const double* top, const double* bot, size_t n, int f32, cudaStream_t s);
+int launch_deinterleave_tau(double* top, double* bot, const void* src, size_t n, int f32, cudaStream_t s);
 int launch_gather_tour(double* per_agent, const uint32_t* words, const double* tour, size_t n, cudaStream_t s);
 // Reference planes (window rows from g_lo) + AgentRecords -> buffer cell words
 // and cell-resident tour; *status = min(buffer cell << 3 | reason) over violations.

@@ -388,9 +388,14 @@ __global__ void fill_tau_kernel(double2* p, size_t n, double v) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         p[i] = make_double2(v, v);
 }
+__global__ void fill_tau_f32_kernel(float2* p, size_t n, float v) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = make_float2(v, v);
+}
 
-int launch_fill_tau(double2* p, size_t n, double v, cudaStream_t s) {
-    fill_tau_kernel<<<148 * 8, 256, 0, s>>>(p, n, v);
+int launch_fill_tau(void* p, size_t n, double v, int f32, cudaStream_t s) {
+    if (f32) fill_tau_f32_kernel<<<148 * 8, 256, 0, s>>>(static_cast<float2*>(p), n, static_cast<float>(v));
+    else fill_tau_kernel<<<148 * 8, 256, 0, s>>>(static_cast<double2*>(p), n, v);
     return 1;
 }
 
@@ -430,12 +435,23 @@ __global__ void interleave_tau_kernel(double2* dst, const double* top, const dou
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         dst[i] = make_double2(top[i], bot[i]);
 }
+__global__ void interleave_tau_f32_kernel(float2* dst, const double* top, const double* bot, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        dst[i] = make_float2(__double2float_rn(top[i]), __double2float_rn(bot[i]));
+}
 
 __global__ void deinterleave_tau_kernel(double* top, double* bot, const double2* src, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         const double2 t = src[i];
         top[i] = t.x;
         bot[i] = t.y;
+    }
+}
+__global__ void deinterleave_tau_f32_kernel(double* top, double* bot, const float2* src, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const float2 t = src[i];
+        top[i] = double(t.x);
+        bot[i] = double(t.y);
     }
 }
 
@@ -585,12 +601,14 @@ int launch_audit(const uint32_t* words, size_t first, size_t n, uint32_t n_agent
     return 1;
 }
 
-int launch_interleave_tau(double2* dst, const double* top, const double* bot, size_t n, cudaStream_t s) {
-    interleave_tau_kernel<<<148 * 8, 256, 0, s>>>(dst, top, bot, n);
+int launch_interleave_tau(void* dst, const double* top, const double* bot, size_t n, int f32, cudaStream_t s) {
+    if (f32) interleave_tau_f32_kernel<<<148 * 8, 256, 0, s>>>(static_cast<float2*>(dst), top, bot, n);
+    else interleave_tau_kernel<<<148 * 8, 256, 0, s>>>(static_cast<double2*>(dst), top, bot, n);
     return 1;
 }
-int launch_deinterleave_tau(double* top, double* bot, const double2* src, size_t n, cudaStream_t s) {
-    deinterleave_tau_kernel<<<148 * 8, 256, 0, s>>>(top, bot, src, n);
+int launch_deinterleave_tau(double* top, double* bot, const void* src, size_t n, int f32, cudaStream_t s) {
+    if (f32) deinterleave_tau_f32_kernel<<<148 * 8, 256, 0, s>>>(top, bot, static_cast<const float2*>(src), n);
+    else deinterleave_tau_kernel<<<148 * 8, 256, 0, s>>>(top, bot, static_cast<const double2*>(src), n);
     return 1;
 }
 int launch_import_state(const uint8_t* occ, const uint32_t* index, const void* agents, uint32_t n_agents, uint32_t W,

@@ -72,7 +72,9 @@ class ScenarioConfig:
 
 def _pf_config(cfg: ScenarioConfig, seed: int | None = None, *, replicas: int = 1, row_begin: int = 0,
                row_end: int = 0, device: int = 0, kernel: str = "fused") -> _lib.PfConfig:
-    k = {"fused": _lib.PF_KERNEL_FUSED, "pipeline": _lib.PF_KERNEL_PIPELINE, "tile": _lib.PF_KERNEL_TILE}.get(kernel)
+    # "fused_f32": the fused kernel with fp32 pheromone storage (tolerance-only)
+    k = {"fused": _lib.PF_KERNEL_FUSED, "pipeline": _lib.PF_KERNEL_PIPELINE, "tile": _lib.PF_KERNEL_TILE,
+         "fused_f32": _lib.PF_KERNEL_FUSED_F32}.get(kernel)
     if k is None:
         raise ConfigError(f"unknown kernel '{kernel}'")
     return _lib.PfConfig(
