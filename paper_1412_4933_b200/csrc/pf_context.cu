@@ -50,17 +50,10 @@ int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(PF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-// Run fn(begin, end) over [0, n) on the host's threads (state conversion).
+// Run fn(begin, end) over [0, n) on the host's threads (state conversion),
+// on the library's persistent worker pool.
 static void host_parallel(size_t n, const std::function<void(size_t, size_t)>& fn) {
-    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 32), std::max<size_t>(1, n / 64));
-    if (nt <= 1) {
-        fn(0, n);
-        return;
-    }
-    std::vector<std::thread> ts;
-    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
-    for (auto& t : ts) t.join();
+    pfhost::pool_for(n, std::min<size_t>(2 * (pfhost::pool_threads() + 1), std::max<size_t>(1, n / 64)), fn);
 }
 
 // Large host<->device copies of the caller's pageable planes. A plain
@@ -145,8 +138,12 @@ class Stager {
     }
 
   private:
+    // Host side of a chunk: a memcpy split over the library's persistent
+    // worker pool (spawning threads per 64 MB chunk cost a third of the
+    // transfer time at C5).
     static void par_copy(void* dst, const void* src, size_t n) {
-        host_parallel(n / 4096 + 1, [&](size_t b0, size_t b1) {
+        const size_t pages = (n + 4095) / 4096;
+        pfhost::pool_for(pages, std::min<size_t>(pages, 2 * (pfhost::pool_threads() + 1)), [&](size_t b0, size_t b1) {
             const size_t lo = std::min(n, b0 * 4096), hi = std::min(n, b1 * 4096);
             if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
         });

@@ -7,7 +7,10 @@
 #include "pf_setup.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
 #include <future>
 #include <list>
 #include <map>
@@ -45,6 +48,111 @@ int32_t band_height(int32_t agents_per_side, int32_t width) {
     if (width <= 0) return 0;
     return int32_t((int64_t(agents_per_side) + width - 1) / width);
 }
+
+namespace {
+
+// Persistent host worker pool (pool_for): jobs are queued FIFO; workers and
+// the submitting thread take ranges of the front job until it is exhausted.
+struct PoolJob {
+    const std::function<void(size_t, size_t)>* fn;
+    size_t n, parts;
+    std::atomic<size_t> next{0}, done{0};
+    std::mutex m;
+    std::condition_variable cv;
+};
+
+class Pool {
+  public:
+    Pool() {
+        const size_t hw = std::max<unsigned>(2u, std::thread::hardware_concurrency());
+        for (size_t i = 0; i + 1 < std::min<size_t>(hw, 64); ++i) ths_.emplace_back([this] { work(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : ths_) t.join();
+    }
+    size_t threads() const { return ths_.size(); }
+    void run(size_t n, size_t parts, const std::function<void(size_t, size_t)>& fn) {
+        auto job = std::make_shared<PoolJob>();
+        job->fn = &fn;
+        job->n = n;
+        job->parts = parts;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            q_.push_back(job);
+        }
+        cv_.notify_all();
+        help(*job);
+        std::unique_lock<std::mutex> lk(job->m);
+        job->cv.wait(lk, [&] { return job->done.load() == job->parts; });
+        std::lock_guard<std::mutex> g(mu_);
+        for (auto it = q_.begin(); it != q_.end(); ++it)
+            if (it->get() == job.get()) {
+                q_.erase(it);
+                break;
+            }
+    }
+
+  private:
+    static void help(PoolJob& j) {
+        for (size_t i; (i = j.next.fetch_add(1)) < j.parts;) {
+            (*j.fn)(j.n * i / j.parts, j.n * (i + 1) / j.parts);
+            if (j.done.fetch_add(1) + 1 == j.parts) {
+                std::lock_guard<std::mutex> g(j.m);
+                j.cv.notify_all();
+            }
+        }
+    }
+    void work() {
+        for (;;) {
+            std::shared_ptr<PoolJob> j;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] {
+                    if (stop_) return true;
+                    for (auto& x : q_)
+                        if (x->next.load() < x->parts) return true;
+                    return false;
+                });
+                if (stop_) return;
+                for (auto& x : q_)
+                    if (x->next.load() < x->parts) {
+                        j = x;
+                        break;
+                    }
+            }
+            if (j) help(*j);
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::shared_ptr<PoolJob>> q_;
+    std::vector<std::thread> ths_;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p;
+    return p;
+}
+
+}  // namespace
+
+void pool_for(size_t n, size_t parts, const std::function<void(size_t, size_t)>& fn) {
+    if (n == 0) return;
+    parts = std::max<size_t>(1, std::min(parts, n));
+    if (parts == 1) {
+        fn(0, n);
+        return;
+    }
+    pool().run(n, parts, fn);
+}
+
+size_t pool_threads() { return pool().threads(); }
 
 void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
     const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());

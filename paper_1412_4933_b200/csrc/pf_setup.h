@@ -14,6 +14,12 @@ int32_t band_height(int32_t agents_per_side, int32_t width);
 // fn(begin, end) over [0, n) on up to hardware_concurrency threads (ranges of
 // at least 64K).
 void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn);
+// fn(begin, end) over [0, n) split into `parts` ranges, run on the library's
+// persistent worker threads plus the caller (no thread creation per call;
+// several callers may run jobs at once). Returns when every range is done.
+void pool_for(size_t n, size_t parts, const std::function<void(size_t, size_t)>& fn);
+// Worker threads of the pool (hardware_concurrency - 1, at least 1).
+size_t pool_threads();
 
 // Keyed Fisher-Yates placement of one side (src/state.cpp:17-50): calls
 // put(global linear cell, agent id) for the n placed agents.
