@@ -677,8 +677,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     // The counter of batch slot slot_idx is zeroed before the batch and no
     // other launch touches it, so the first claim needs no ordering.
     uint32_t* const work = a.work + slot_idx;
+    // At most one item per CTA (single small grids): CTA b takes item b and
+    // nothing is claimed (no counter round trips on the step's critical path).
+    const bool one_each = n_all <= int(gridDim.x);
     int item = 0;
-    if (warp == 0) {
+    if (one_each) {
+        item = int(blockIdx.x);
+    } else if (warp == 0) {
         if (lane == 0) item = int(atomicAdd(work, 1u));
         item = __shfl_sync(0xFFFFFFFFu, item, 0);
     }
@@ -737,7 +742,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
             next_base = kCrossPrefetch ? slot(base, SR) : 0;
             if (warp == kIoWarp) {
                 int nx = 0;
-                if (lane == 0) nx = int(atomicAdd(work, 1u));
+                if (lane == 0) nx = one_each ? n_all : int(atomicAdd(work, 1u));
                 nx = __shfl_sync(0xFFFFFFFFu, nx, 0);
                 if (lane == 0) sm.item[ipar] = nx;
                 // This CTA's last item: the next step's grid may be scheduled
@@ -770,125 +775,142 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         mbar_wait(&sm.mbar[my_load & 1], (my_load >> 1) & 1u);
 
 #ifndef PF_BITS_STREAM_ONLY
-        // ------------------------------------------------------------ S1
-        // Intents for rows -2 .. RT+1, all staged segments (halo segments
-        // only at the two columns next to the strip). A thread takes two
-        // vertically adjacent units: they share two of their four staged
-        // rows (12 plane loads instead of 18).
-        static_assert(DROWS % 2 == 0, "S1 pairs intent rows");
-        for (int u2 = threadIdx.x; u2 < (DROWS / 2) * SS; u2 += NT) {
-            const int dp = u2 / SS, si = u2 - dp * SS;
-            const int di0 = 2 * dp;  // intent rows di0, di0 + 1 = staged rows di0 + 1, di0 + 2
-            uint32_t E[4][3];        // emptiness of staged rows di0 .. di0 + 3 at segments si-1, si, si+1
-            uint2 P[2];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint2* row = sm.pl[slot(base, di0 + r)] + si + 1;
-                const uint2 m = row[0];
-                E[r][0] = empty_of(row[-1]);
-                E[r][1] = empty_of(m);
-                E[r][2] = empty_of(row[1]);
-                if (r == 1) P[0] = m;
-                if (r == 2) P[1] = m;
+        // A window without agents (no cell with exactly one occupancy bit in
+        // staged rows -3 .. RT+2; walls have both) needs no S1/S2: nothing can
+        // arrive in or leave the tile's rows, so S3 takes the no-movement path
+        // for every row (planes copied, ACO pheromone evaporated). The work
+        // scratch of this tile is already zero. (The crowd-free middle of the
+        // C5 grid, most of it early in a run.)
+        // Large LEM grids only (C5 LEM -7..-10%): for ACO the pheromone stream
+        // bounds the step and the check cost +1.7% at C5, and in the dense
+        // small-grid variants it made ptxas spill (C4 single +20%).
+        bool any_agent = ACO || COMPACT;
+        if (!ACO && !COMPACT)
+            for (int i = threadIdx.x; i < SR * SP; i += NT) {
+                const uint2 q = sm.pl[slot(base, i / SP)][i % SP];
+                any_agent |= (q.x ^ q.y) != 0u;
             }
-            const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int di = di0 + k, u = di * SS + si;
-                Around n;
-                n.em = E[k][1];
-                n.emL = from_left(E[k][1], E[k][0]);
-                n.emR = from_right(E[k][1], E[k][2]);
-                n.e0L = from_left(E[k + 1][1], E[k + 1][0]);
-                n.e0R = from_right(E[k + 1][1], E[k + 1][2]);
-                n.ep = E[k + 2][1];
-                n.epL = from_left(E[k + 2][1], E[k + 2][0]);
-                n.epR = from_right(E[k + 2][1], E[k + 2][2]);
-                const uint2 p = P[k];
-                const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
-                uint32_t d[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) d[q] = 0u;
-                d[6] = T & n.ep;  // Top forward: (+1, 0)
-                d[1] = B & n.em;  // Bottom forward: (-1, 0)
-                const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
-                const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
-                if (slow) {
-                    enqueue(sm, &sm.qc[cur][0], u, slow);
-                    sm.rowdraw[cur][di] = 1u;
+        if (ACO || COMPACT || __syncthreads_or(any_agent)) {
+            // ------------------------------------------------------------ S1
+            // Intents for rows -2 .. RT+1, all staged segments (halo segments
+            // only at the two columns next to the strip). A thread takes two
+            // vertically adjacent units: they share two of their four staged
+            // rows (12 plane loads instead of 18).
+            static_assert(DROWS % 2 == 0, "S1 pairs intent rows");
+            for (int u2 = threadIdx.x; u2 < (DROWS / 2) * SS; u2 += NT) {
+                const int dp = u2 / SS, si = u2 - dp * SS;
+                const int di0 = 2 * dp;  // intent rows di0, di0 + 1 = staged rows di0 + 1, di0 + 2
+                uint32_t E[4][3];        // emptiness of staged rows di0 .. di0 + 3 at segments si-1, si, si+1
+                uint2 P[2];
+    #pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint2* row = sm.pl[slot(base, di0 + r)] + si + 1;
+                    const uint2 m = row[0];
+                    E[r][0] = empty_of(row[-1]);
+                    E[r][1] = empty_of(m);
+                    E[r][2] = empty_of(row[1]);
+                    if (r == 1) P[0] = m;
+                    if (r == 2) P[1] = m;
                 }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
-            }
-        }
-        __syncthreads();
-        // Draws, spread evenly over the CTA (the barrier is skipped,
-        // uniformly, when there are none).
-        if (const uint32_t nq = sm.qc[cur][0] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[cur][0] >> 16;
-            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                int u, j;
-                list_entry(sm, ne, e, u, j);
-                const int di = u / SS, si = u - di * SS;
-                const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
-                const int code = draw_intent<ACO, TV>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
-                atomicOr(&sm.D[code][di][si + 1], 1u << j);
+                const uint32_t segmask = si == 0 ? 0xC0000000u : (si == SS - 1 ? 0x00000003u : 0xFFFFFFFFu);
+    #pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int di = di0 + k, u = di * SS + si;
+                    Around n;
+                    n.em = E[k][1];
+                    n.emL = from_left(E[k][1], E[k][0]);
+                    n.emR = from_right(E[k][1], E[k][2]);
+                    n.e0L = from_left(E[k + 1][1], E[k + 1][0]);
+                    n.e0R = from_right(E[k + 1][1], E[k + 1][2]);
+                    n.ep = E[k + 2][1];
+                    n.epL = from_left(E[k + 2][1], E[k + 2][0]);
+                    n.epR = from_right(E[k + 2][1], E[k + 2][2]);
+                    const uint2 p = P[k];
+                    const uint32_t T = p.x & ~p.y & segmask, B = p.y & ~p.x & segmask;
+                    uint32_t d[8];
+    #pragma unroll
+                    for (int q = 0; q < 8; ++q) d[q] = 0u;
+                    d[6] = T & n.ep;  // Top forward: (+1, 0)
+                    d[1] = B & n.em;  // Bottom forward: (-1, 0)
+                    const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
+                    const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
+                    if (slow) {
+                        enqueue(sm, &sm.qc[cur][0], u, slow);
+                        sm.rowdraw[cur][di] = 1u;
+                    }
+    #pragma unroll
+                    for (int q = 0; q < 8; ++q) sm.D[q][di][si + 1] = d[q];
+                }
             }
             __syncthreads();
-        }
+            // Draws, spread evenly over the CTA (the barrier is skipped,
+            // uniformly, when there are none).
+            if (const uint32_t nq = sm.qc[cur][0] & 0xFFFFu) {
+                const uint32_t ne = sm.qc[cur][0] >> 16;
+                for (uint32_t e = threadIdx.x; e < nq; e += NT) {
+                    int u, j;
+                    list_entry(sm, ne, e, u, j);
+                    const int di = u / SS, si = u - di * SS;
+                    const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
+                    const int code = draw_intent<ACO, TV>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
+                    atomicOr(&sm.D[code][di][si + 1], 1u << j);
+                }
+                __syncthreads();
+            }
 
-        // ------------------------------------------------------------ S2
-        // Claims, winners and grants for destinations in rows -1 .. RT.
-        for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
-            const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
-            if (!(sm.rowdraw[cur][ai] | sm.rowdraw[cur][ai + 1] | sm.rowdraw[cur][ai + 2])) {
-                // No agent in the three intent rows around these destinations
-                // drew: the only claims are forward moves, from the row above
-                // (Top, code 1) and the row below (Bottom, code 6).
-                const uint32_t segmask = si == 0 ? 0x80000000u : (si == SS - 1 ? 0x00000001u : 0xFFFFFFFFu);
-                const uint32_t c1 = sm.D[6][ai][si + 1] & segmask, c6 = sm.D[1][ai + 2][si + 1] & segmask;
-                const uint32_t twos = c1 & c6, w1 = c1 & ~twos, w6 = c6 & ~twos;
-                sm.A[ai][si] = c1 | c6;
-                if ((c1 | c6) && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
-                sm.K[0][ai][si] = w1;
-                sm.K[1][ai][si] = w6;
-                sm.K[2][ai][si] = w6;
-                if (w1) grant(sm, cur, ai - 1, si, 1, w1);
-                if (w6) grant(sm, cur, ai - 1, si, 6, w6);
+            // ------------------------------------------------------------ S2
+            // Claims, winners and grants for destinations in rows -1 .. RT.
+            for (int u = threadIdx.x; u < AROWS * SS; u += NT) {
+                const int ai = u / SS, si = u - ai * SS;  // ai = rr + 1
+                if (!(sm.rowdraw[cur][ai] | sm.rowdraw[cur][ai + 1] | sm.rowdraw[cur][ai + 2])) {
+                    // No agent in the three intent rows around these destinations
+                    // drew: the only claims are forward moves, from the row above
+                    // (Top, code 1) and the row below (Bottom, code 6).
+                    const uint32_t segmask = si == 0 ? 0x80000000u : (si == SS - 1 ? 0x00000001u : 0xFFFFFFFFu);
+                    const uint32_t c1 = sm.D[6][ai][si + 1] & segmask, c6 = sm.D[1][ai + 2][si + 1] & segmask;
+                    const uint32_t twos = c1 & c6, w1 = c1 & ~twos, w6 = c6 & ~twos;
+                    sm.A[ai][si] = c1 | c6;
+                    if ((c1 | c6) && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
+                    sm.K[0][ai][si] = w1;
+                    sm.K[1][ai][si] = w6;
+                    sm.K[2][ai][si] = w6;
+                    if (w1) grant(sm, cur, ai - 1, si, 1, w1);
+                    if (w6) grant(sm, cur, ai - 1, si, 6, w6);
+                    if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
+                    continue;
+                }
+                uint32_t C[8];
+                claims(sm, ai, si, C);
+                uint32_t ones = 0u, twos = 0u;
+    #pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    twos |= ones & C[q];
+                    ones |= C[q];
+                }
+                uint32_t win[8];
+    #pragma unroll
+                for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
+                sm.A[ai][si] = ones;
+                if (ones && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
+                sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
+                sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
+                sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
+    #pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (win[q]) grant(sm, cur, ai - 1, si, q, win[q]);
                 if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
-                continue;
-            }
-            uint32_t C[8];
-            claims(sm, ai, si, C);
-            uint32_t ones = 0u, twos = 0u;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                twos |= ones & C[q];
-                ones |= C[q];
-            }
-            uint32_t win[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) win[q] = C[q] & ~twos;
-            sm.A[ai][si] = ones;
-            if (ones && ai >= 1 && ai <= RT) sm.dirty[cur][ai - 1] = 1u;
-            sm.K[0][ai][si] = win[1] | win[3] | win[5] | win[7];
-            sm.K[1][ai][si] = win[2] | win[3] | win[6] | win[7];
-            sm.K[2][ai][si] = win[4] | win[5] | win[6] | win[7];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (win[q]) grant(sm, cur, ai - 1, si, q, win[q]);
-            if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
-        }
-        __syncthreads();
-        if (const uint32_t nq = sm.qc[cur][1] & 0xFFFFu) {
-            const uint32_t ne = sm.qc[cur][1] >> 16;
-            for (uint32_t e = threadIdx.x; e < nq; e += NT) {
-                int u, j;
-                list_entry(sm, ne, e, u, j);
-                const int ai = u / SS, si = u - ai * SS;
-                set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
             }
             __syncthreads();
+            if (const uint32_t nq = sm.qc[cur][1] & 0xFFFFu) {
+                const uint32_t ne = sm.qc[cur][1] >> 16;
+                for (uint32_t e = threadIdx.x; e < nq; e += NT) {
+                    int u, j;
+                    list_entry(sm, ne, e, u, j);
+                    const int ai = u / SS, si = u - ai * SS;
+                    set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
+                }
+                __syncthreads();
+            }
         }
 
 #else
