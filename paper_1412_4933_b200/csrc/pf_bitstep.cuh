@@ -1234,6 +1234,10 @@ static void launch_aco(const StepArgs& b, bool hbm, bool mirror, dim3 grid, size
     }
 }
 
+#ifndef PF_MULTI_MAX_ITEMS_PER_CTA
+#define PF_MULTI_MAX_ITEMS_PER_CTA 16  // x128 batches (13 per CTA) -1.7% multi-step, x256 (26) +2%
+#endif
+
 // Persistent grid: one CTA per resident slot (SMs x 3, 4 or 5) at most. Work
 // items are chunks of up to 16 consecutive RT-row tiles of one strip of one
 // replica, about items_per_cta items per CTA (pf_context.cu: one tile per
@@ -1255,12 +1259,12 @@ int launch(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     const long long items = (long long)strips * ((n_tiles + b.tiles_per_cta - 1) / b.tiles_per_cta) * a.replicas;
     const bool mirror = a.peer[0].cell || a.peer[1].cell;  // linked shard: fused halo exchange
     // Multi-step launches pay where a step's tail is a large part of it: a
-    // few items per resident CTA (the 480^2 x64 batches: C4 -9%, C3 -10%).
+    // few items per resident CTA (the 480^2 x64 batches: C4 -9%, C3 -10%; x128 -1.7%).
     // With many items per CTA (C5) the tail is negligible and the per-item
     // dependency polls cost (C5 LEM +11%); with fewer items than CTAs
     // (single 480^2 scenarios) the flag round trips cost more than the
     // launches they replace (C1 +25%). Those take one launch per step.
-    if (b.nsteps > 1 && (mirror || big || items < ctas_max || items > 12 * ctas_max)) {
+    if (b.nsteps > 1 && (mirror || big || items < ctas_max || items > PF_MULTI_MAX_ITEMS_PER_CTA * ctas_max)) {
         const int n = b.nsteps;
         b.nsteps = 1;
         int launches = 0;
