@@ -553,10 +553,10 @@ static cudaError_t copy_d2d(void* dst, const void* src, size_t n, cudaStream_t s
 // Upload one replica's buffer-row planes (cells + tour) and set the step.
 static int ensure_scratch(pf_ctx* ctx, size_t need);
 
-// After replica rep's words are in P.cell[0]: the second word buffer, the
-// occupancy planes, tours and pheromone (uploaded, or the initial values).
-static int finish_replica_upload(pf_ctx* ctx, int rep, const std::vector<double>* tour,
-                                 const std::vector<double2>* tau) {
+// After replica rep's words are in P.cell[0] (pf_init_environment): the
+// second word buffer, the occupancy planes, zero tours and the initial
+// pheromone tau0 in both buffers (src/state.cpp:40-47).
+static int finish_replica_init(pf_ctx* ctx, int rep) {
     const size_t off = size_t(rep) * ctx->plane();
     pfk::Planes& P = ctx->args.p;
     // The second ping-pong buffer is filled device-side (its ghost rows must
@@ -564,15 +564,9 @@ static int finish_replica_upload(pf_ctx* ctx, int rep, const std::vector<double>
     PF_CUDA(copy_d2d(P.cell[1] + off, P.cell[0] + off, ctx->plane() * 4, ctx->stream));
     build_occ(ctx, rep);
     if (ctx->aco()) {
-        if (tour) PF_CUDA(ctx->stage[0].h2d(P.tour + off, tour->data(), ctx->plane() * 8, ctx->stream));
-        else PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
-        if (tau && !ctx->f32()) {
-            PF_CUDA(ctx->stage[0].h2d(P.tau[0] + off, tau->data(), ctx->plane() * 16, ctx->stream));
-            PF_CUDA(cudaMemcpyAsync(P.tau[1] + off, P.tau[0] + off, ctx->plane() * 16, cudaMemcpyDeviceToDevice, ctx->stream));
-        } else {
-            ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(0, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
-            ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(1, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
-        }
+        PF_CUDA(cudaMemsetAsync(P.tour + off, 0, ctx->plane() * 8, ctx->stream));
+        ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(0, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
+        ctx->launches += pfk::launch_fill_tau(ctx->tau_ptr(1, off), ctx->plane(), ctx->cfg.tau0, ctx->f32(), ctx->stream);
     }
     PF_CUDA(cudaStreamSynchronize(ctx->stream));
     return PF_OK;
@@ -644,7 +638,7 @@ int pf_init_environment(pf_ctx* ctx) {
                 ctx->launches += pfk::launch_scatter_placement(P.cell[0] + off, d_cells + n, n, n + 1u, 2u, W, g_lo,
                                                                ctx->rows_buf, ctx->stream);
             }
-            if (int rc = finish_replica_upload(ctx, rep, nullptr, nullptr)) return rc;
+            if (int rc = finish_replica_init(ctx, rep)) return rc;
         }
     }
     ctx->parity = 0;
