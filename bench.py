@@ -615,10 +615,7 @@ def e2e_runs(args, cfg, reps, rank, world, local, barrier, max_over_ranks):
                         + ("page-locked numpy planes (pf_host_alloc)" if pinned else "pageable numpy planes")}
         head = variants["cpp_step_loop_pageable"]
     else:
-        from paper_1412_4933_b200.sharding import row_partition
-
         secs = capi_batch(args, cfg, rank, world, local, barrier, max_over_ranks, False)
-        lo, hi = row_partition(H, world)[rank]
         head = {"value": agents * args.steps / secs, "seconds": secs,
                 "path": "per rank: pf_load_state -> pf_step_async(K) -> reports -> pf_store_state of its row shard, "
                         "pageable planes"}
@@ -634,10 +631,10 @@ def capi_batch(args, cfg, rank, world, local, barrier, max_over_ranks, pinned):
     import paper_1412_4933_b200 as p
     from paper_1412_4933_b200 import _lib
     from paper_1412_4933_b200.engine import _pf_config
-    from paper_1412_4933_b200.sharding import row_partition
+    from paper_1412_4933_b200.sharding import balanced_row_partition
 
     state = p.new_environment(cfg, 42, pinned=pinned)
-    lo, hi = row_partition(cfg.height, world)[rank]
+    lo, hi = balanced_row_partition(cfg, world)[rank]
     c = _lib.Context(_pf_config(cfg, 42, row_begin=0 if world == 1 else lo, row_end=0 if world == 1 else hi,
                                 device=local))
     if world > 1:  # fused halo exchange between the ranks' contexts (CUDA IPC, device handshake)

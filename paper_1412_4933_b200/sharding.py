@@ -49,6 +49,58 @@ def row_partition(height: int, world: int) -> list[tuple[int, int]]:
     return parts
 
 
+# Relative cost of a row inside a starting band of agents against an empty
+# row, per model, measured at C5 on one GPU (profiles/shard_projection_r02.md:
+# 8 equal shards, band shard vs interior shard): ACO is bound by its pheromone
+# stream, uniform over rows; LEM's work follows the agents.
+BAND_ROW_COST = {0: 2.9, 1: 1.13}  # Model.Lem, Model.Aco
+
+
+def balanced_row_partition(cfg, world: int) -> list[tuple[int, int]]:
+    """Contiguous row blocks [lo, hi) of about equal step cost: rows in the
+    two starting bands (band_height rows at each end, src/state.cpp:72-73,
+    src/metrics.cpp:8-11) weigh BAND_ROW_COST[model], empty rows 1. The bands
+    move ~1 row per step, so the balance holds for the first few hundred
+    steps. Every shard owns >= GHOST rows; with no agents this is
+    row_partition."""
+    if world < 1:
+        raise _lib.ConfigError("world size must be >= 1")
+    H = int(cfg.height)
+    if world == 1:
+        return [(0, H)]
+    band = min(H, int(_lib.lib.pf_band_height(int(cfg.agents_per_side), int(cfg.width)))) if cfg.agents_per_side else 0
+    wb = BAND_ROW_COST.get(int(cfg.model), 1.0)
+
+    def cum(r):  # total weight of rows [0, r)
+        top = min(r, band)
+        bot = max(0, r - (H - band)) if band else 0
+        return r + (wb - 1.0) * (top + bot)
+
+    total = cum(H)
+    cuts = [0]
+    for k in range(1, world):
+        target = total * k / world
+        lo, hi = cuts[-1] + GHOST, H - GHOST * (world - k)
+        r = max(lo, min(hi, int(round(_inverse(cum, target, H)))))
+        cuts.append(r)
+    cuts.append(H)
+    parts = list(zip(cuts[:-1], cuts[1:]))
+    if min(hi - lo for lo, hi in parts) < GHOST:
+        raise _lib.ConfigError(f"each shard must own at least {GHOST} rows")
+    return parts
+
+
+def _inverse(cum, target, H):
+    lo, hi = 0, H  # cum is increasing: smallest r with cum(r) >= target
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if cum(mid) < target:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo
+
+
 class HaloExchanger:
     """Per-step ghost-row swap with the neighbours rank-1 (above) and rank+1
     (below) over a torch.distributed process group.
@@ -134,7 +186,7 @@ class ShardedEngine:
         self.rank, self.world = rank, world
         self.group = group
         self.device = rank if device is None else device
-        self.lo, self.hi = row_partition(cfg.height, world)[rank]
+        self.lo, self.hi = balanced_row_partition(cfg, world)[rank]
         whole = world == 1
         self.ctx = _lib.Context(_pf_config(cfg, cfg.seed if seed is None else seed, replicas=replicas,
                                            row_begin=0 if whole else self.lo, row_end=0 if whole else self.hi,

@@ -445,3 +445,24 @@ def test_gpu_sharded_engine_two_ranks_one_device(model, exchange):
             if tt is not None:
                 assert (tt[lo:hi] == ref.pheromone_top[lo:hi]).all()
                 assert (tb[lo:hi] == ref.pheromone_bottom[lo:hi]).all()
+
+
+def test_balanced_row_partition():
+    """ShardedEngine's cost-weighted rows: contiguous, covering, >= 3 rows
+    each, equal rows without agents, fewer rows for the band shards."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200.sharding import balanced_row_partition, row_partition
+
+    for model in (p.Model.Lem, p.Model.Aco):
+        cfg = p.ScenarioConfig(width=16384, height=16384, agents_per_side=25_000_000, model=model)
+        for P in (1, 2, 3, 4, 8):
+            parts = balanced_row_partition(cfg, P)
+            assert parts[0][0] == 0 and parts[-1][1] == 16384
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            assert all(hi - lo >= 3 for lo, hi in parts)
+        eight = balanced_row_partition(cfg, 8)
+        assert eight[0][1] - eight[0][0] < 2048 and eight[-1][1] - eight[-1][0] < 2048
+    empty = p.ScenarioConfig(width=96, height=96, agents_per_side=0, model=p.Model.Aco)
+    assert balanced_row_partition(empty, 3) == row_partition(96, 3)
+    tiny = p.ScenarioConfig(width=16, height=16, agents_per_side=120, model=p.Model.Lem)
+    assert all(hi - lo >= 3 for lo, hi in balanced_row_partition(tiny, 5))

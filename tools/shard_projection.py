@@ -5,7 +5,11 @@ the shard's own work, not the exchange). Interior and edge shards are timed.
 The exchange cost is measured separately by linked shards on one GPU
 (bench secondary c5_aco_linked_shards_one_gpu). Projection, not a scaling run.
 
-    python tools/shard_projection.py [c5_aco|c5_lem] [steps]
+    python tools/shard_projection.py [c5_aco|c5_lem] [steps] [equal|balanced]
+
+equal: row_partition (equal rows; an edge and an interior shard are timed);
+balanced: balanced_row_partition (ShardedEngine's cost-weighted rows; every
+shard is timed).
 """
 import json
 import os
@@ -15,16 +19,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_1412_4933_b200 import _lib  # noqa: E402
 from paper_1412_4933_b200.engine import _pf_config  # noqa: E402
-from paper_1412_4933_b200.sharding import row_partition  # noqa: E402
+from paper_1412_4933_b200.sharding import balanced_row_partition, row_partition  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5_aco"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+mode = sys.argv[3] if len(sys.argv) > 3 else "equal"
 cfg, reps, desc = bench.scenario(name)
-out = {"workload": desc, "steps": steps, "window": f"steps 5..{5 + steps}", "per_P": {}}
+out = {"workload": desc, "steps": steps, "window": f"steps 5..{5 + steps}", "partition": mode, "per_P": {}}
 for P in (1, 2, 4, 8):
-    parts = row_partition(cfg.height, P)
+    parts = row_partition(cfg.height, P) if mode == "equal" else balanced_row_partition(cfg, P)
     times = {}
-    for r in sorted({0, P // 2}):  # an edge shard (band rows) and an interior one
+    ranks = sorted({0, P // 2}) if mode == "equal" else range(P)
+    for r in ranks:  # equal: an edge shard (band rows) and an interior one
         lo, hi = parts[r]
         c = _lib.Context(_pf_config(cfg, 42, row_begin=0 if P == 1 else lo, row_end=0 if P == 1 else hi))
         c.init_environment()
