@@ -193,7 +193,7 @@ class ShardedEngine:
                                            device=self.device, kernel=kernel))
         self.ctx.init_environment()
         if exchange is None:
-            exchange = "p2p" if kernel == "fused" else "collective"
+            exchange = "p2p" if kernel in ("fused", "fused_f32") else "collective"
         if exchange not in ("p2p", "collective"):
             raise _lib.ConfigError(f"unknown halo exchange {exchange!r} (p2p or collective)")
         self.exchange = exchange if world > 1 else "none"
