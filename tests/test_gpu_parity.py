@@ -123,6 +123,33 @@ def test_multistep_launch_matches_per_step_launches_and_oracle(model):
     es.close()
 
 
+def test_multistep_launch_with_multi_tile_items():
+    """Multi-step launches whose work items are chunks of several tiles
+    (PEDFLOW_ITEMS_PER_CTA=1: 480^2 x 40 ACO, 4-tile items, 640 items per
+    step): the dependency window spans the chunk's tiles +- 1. Equal to one
+    launch per step on every replica over 200 steps."""
+    import os
+
+    import paper_1412_4933_b200 as p
+
+    cfg = to_config(dict(width=480, height=480, agents_per_side=51_200, model="aco", seed=7))
+    R = 40
+    got = {}
+    for flag in ("1", "0"):
+        os.environ["PEDFLOW_MULTISTEP"] = flag
+        os.environ["PEDFLOW_ITEMS_PER_CTA"] = "1"
+        try:
+            e = p.Ensemble(cfg, replicas=R, seed=7)
+        finally:
+            os.environ.pop("PEDFLOW_MULTISTEP", None)
+            os.environ.pop("PEDFLOW_ITEMS_PER_CTA", None)
+        rep = e.run(200)
+        got[flag] = (rep, [hashes_of(e.state(i)) for i in range(R)])
+        e.close()
+    assert (got["1"][0] == got["0"][0]).all()
+    assert got["1"][1] == got["0"][1]
+
+
 def test_device_rng_matches_oracle():
     """Device Philox / uniform / AS241 normal vs the oracle (all three branches)."""
     from oracle.oracle import oracle
