@@ -7,7 +7,9 @@
 // but waste whole segments when the grid width is not a multiple of 320:
 // for LEM the strip width with fewer units per row wins (A/B at step 150: C5
 // LEM -9% with 10; 480-wide grids: 8, since 10 would pad 15 segments to 20).
-// ACO, bound by its pheromone stream, keeps 8 (C5 ACO +0.4% with 10).
+// ACO, bound by its pheromone stream, keeps 8 (C5 ACO +0.4% with 10, and
+// +22% with 10 since the 32-row tiles came); with fp32 pheromone storage it
+// takes the LEM rule (C5: 10, -2%: twice the bytes in flight per lane).
 #include "pf_internal.h"
 
 namespace pfk {
@@ -24,8 +26,8 @@ int configure();
 int launch(const StepArgs& a, int slot, int parity, cudaStream_t s);
 }  // namespace bits_small
 
-int bits_strip_segments(int width, int model) {
-    if (model == 1) return 8;
+int bits_strip_segments(int width, int model, bool tau_f32) {
+    if (model == 1 && !tau_f32) return 8;
     const int ws = (width + 31) / 32;
     auto units = [ws](int ns) { return ((ws + ns - 1) / ns) * (ns + 2); };
     return units(10) < units(8) ? 10 : 8;

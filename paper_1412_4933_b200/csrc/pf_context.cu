@@ -378,7 +378,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     if (ctx->bits()) {
         // Plane pitch: every strip's window (NS + 4 segments from segment
         // strip * NS - 2) lies inside the row, and rows stay 16-byte aligned.
-        const int ns = pfk::bits_strip_segments(cfg->width, cfg->model);
+        const int ns = pfk::bits_strip_segments(cfg->width, cfg->model, ctx->f32());
         ctx->args.strip_segs = ns;
         const int strips = (cfg->width + 32 * ns - 1) / (32 * ns);
         P.wsp = strips * ns + 4;

@@ -90,7 +90,7 @@ struct StepArgs {
 // Returns the number of kernel launches issued.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s);   // PF_KERNEL_FUSED
 int configure_step_bits();
-int bits_strip_segments(int width, int model);  // strip width in segments (8 or 10)
+int bits_strip_segments(int width, int model, bool tau_f32);  // strip width in segments (8 or 10)
 // Occupancy planes of rows [0, rows) from cell words (W columns; padding
 // segments untouched); written to occ0 and, if non-null, occ1.
 int launch_build_occ(const uint32_t* words, int W, int rows, int wsp, uint2* occ0, uint2* occ1, cudaStream_t s);

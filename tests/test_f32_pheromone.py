@@ -30,6 +30,8 @@ CASES = [
     (dict(width=480, height=480, agents_per_side=1024, model="aco", seed=42), 300),
     (dict(width=96, height=96, agents_per_side=2000, model="aco", seed=5, alpha=0.0, beta=1.0, rho=0.3, tau0=0.5,
           q=2.0), 100),
+    # wide enough for the 320-column strips fp32 storage takes on large grids (C5's geometry)
+    (dict(width=2560, height=512, agents_per_side=20_000, model="aco", seed=13), 80),
 ]
 
 
