@@ -280,6 +280,22 @@ __device__ __forceinline__ void grant(Smem& sm, int cur, int rr, int si, int k, 
     }
 }
 
+// Flat form of the work list: one u16 (unit << 5 | bit) per listed bit, by
+// rank, in the per-warp S3 buffers (free during S1/S2; the end-of-tile
+// barrier separates their uses). A list longer than kFlatCap (it cannot be
+// at realistic densities, but no bound rules it out) falls back to the
+// binary search over the entries.
+// Throughput geometries only (C3 x64 -6%, C4 x64 -3.6%): in the latency-bound
+// small-grid geometry the producer's per-bit loop lengthens the slowest S1
+// thread (singles +8%), so it keeps the search.
+constexpr bool kFlat = NS >= 8;
+constexpr int kFlatCap = kFlat ? int((sizeof(uint32_t) * NW * NS * 32 + sizeof(uint16_t) * NW * NS * 32) / sizeof(uint16_t)) : 0;
+static_assert(NU < (1 << 11), "unit index must fit the flat list's 11 bits");
+__device__ __forceinline__ uint16_t* flat_list(Smem& sm) { return reinterpret_cast<uint16_t*>(&sm.asw[0][0][0]); }
+__device__ __forceinline__ const uint16_t* flat_list(const Smem& sm) {
+    return reinterpret_cast<const uint16_t*>(&sm.asw[0][0][0]);
+}
+
 // Add unit u's bits `mask` to work list `list`.
 __device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t mask) {
     const uint32_t old = atomicAdd(qc, (1u << 16) | uint32_t(__popc(mask)));
@@ -287,6 +303,12 @@ __device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t 
     sm.qu[e] = uint32_t(u);
     sm.qm[e] = mask;
     sm.qp[e] = old & 0xFFFFu;
+    uint16_t* fl = flat_list(sm);
+    if (kFlat)
+        for (int k = int(old & 0xFFFFu); mask && k < kFlatCap; ++k) {
+            fl[k] = uint16_t(u << 5 | (__ffs(mask) - 1));
+            mask &= mask - 1u;
+        }
 }
 
 // Position of the k-th (0-based) set bit of m.
@@ -304,8 +326,14 @@ __device__ __forceinline__ int nth_bit(uint32_t m, int k) {
     return pos;
 }
 
-// Work-list rank r -> (unit, bit), n entries.
-__device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t r, int& u, int& j) {
+// Work-list rank r -> (unit, bit), n entries, nq bits.
+__device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t nq, uint32_t r, int& u, int& j) {
+    if (kFlat && nq <= uint32_t(kFlatCap)) {
+        const uint32_t v = flat_list(sm)[r];
+        u = int(v >> 5);
+        j = int(v & 31u);
+        return;
+    }
     int lo = 0, hi = int(n) - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -849,7 +877,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 const uint32_t ne = sm.qc[cur][0] >> 16;
                 for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                     int u, j;
-                    list_entry(sm, ne, e, u, j);
+                    list_entry(sm, ne, nq, e, u, j);
                     const int di = u / SS, si = u - di * SS;
                     const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
                     const int code = draw_intent<ACO, TV>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
@@ -905,7 +933,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 const uint32_t ne = sm.qc[cur][1] >> 16;
                 for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                     int u, j;
-                    list_entry(sm, ne, e, u, j);
+                    list_entry(sm, ne, nq, e, u, j);
                     const int ai = u / SS, si = u - ai * SS;
                     set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
                 }
