@@ -296,7 +296,8 @@ __device__ __forceinline__ const uint16_t* flat_list(const Smem& sm) {
     return reinterpret_cast<const uint16_t*>(&sm.asw[0][0][0]);
 }
 
-// Add unit u's bits `mask` to work list `list`.
+// Add unit u's bits `mask` to work list `list` (FLAT: also per-bit entries).
+template <bool FLAT>
 __device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t mask) {
     const uint32_t old = atomicAdd(qc, (1u << 16) | uint32_t(__popc(mask)));
     const int e = int(old >> 16);
@@ -304,7 +305,7 @@ __device__ __forceinline__ void enqueue(Smem& sm, uint32_t* qc, int u, uint32_t 
     sm.qm[e] = mask;
     sm.qp[e] = old & 0xFFFFu;
     uint16_t* fl = flat_list(sm);
-    if (kFlat)
+    if (FLAT)
         for (int k = int(old & 0xFFFFu); mask && k < kFlatCap; ++k) {
             fl[k] = uint16_t(u << 5 | (__ffs(mask) - 1));
             mask &= mask - 1u;
@@ -327,8 +328,9 @@ __device__ __forceinline__ int nth_bit(uint32_t m, int k) {
 }
 
 // Work-list rank r -> (unit, bit), n entries, nq bits.
+template <bool FLAT>
 __device__ __forceinline__ void list_entry(const Smem& sm, uint32_t n, uint32_t nq, uint32_t r, int& u, int& j) {
-    if (kFlat && nq <= uint32_t(kFlatCap)) {
+    if (FLAT && nq <= uint32_t(kFlatCap)) {
         const uint32_t v = flat_list(sm)[r];
         u = int(v >> 5);
         j = int(v & 31u);
@@ -682,6 +684,9 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     // neighbouring CTAs.
     const bool spread = n_items > int(gridDim.x);
     const bool multi = MULTI && !MIRROR && a.nsteps > 1;  // tile-level dependencies between the launch's steps
+    // Flat draw queues (kFlat) except for large ACO grids, where the
+    // pheromone stream bounds the step and the producer loop cost 0.7% at C5.
+    constexpr bool FLAT = kFlat && (COMPACT || !ACO);
     const int n_all = n_items * (multi ? a.nsteps : 1);
 
     if (threadIdx.x == 0) {
@@ -863,7 +868,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                     const uint32_t any8 = n.ep | n.epL | n.epR | n.e0L | n.e0R | n.em | n.emL | n.emR;
                     const uint32_t slow = ((T & ~n.ep) | (B & ~n.em)) & any8;
                     if (slow) {
-                        enqueue(sm, &sm.qc[cur][0], u, slow);
+                        enqueue<FLAT>(sm, &sm.qc[cur][0], u, slow);
                         sm.rowdraw[cur][di] = 1u;
                     }
     #pragma unroll
@@ -877,7 +882,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                 const uint32_t ne = sm.qc[cur][0] >> 16;
                 for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                     int u, j;
-                    list_entry(sm, ne, nq, e, u, j);
+                    list_entry<FLAT>(sm, ne, nq, e, u, j);
                     const int di = u / SS, si = u - di * SS;
                     const bool bottom = bit(sm.pl[slot(base, di + 1)][si + 1].y, j) != 0u;
                     const int code = draw_intent<ACO, TV>(a, sm, base, cw, tin, di, si, j, bottom, r0, c0, seed, step);
@@ -904,7 +909,7 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
                     sm.K[2][ai][si] = w6;
                     if (w1) grant(sm, cur, ai - 1, si, 1, w1);
                     if (w6) grant(sm, cur, ai - 1, si, 6, w6);
-                    if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
+                    if (twos) enqueue<FLAT>(sm, &sm.qc[cur][1], u, twos);
                     continue;
                 }
                 uint32_t C[8];
@@ -926,14 +931,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     if (win[q]) grant(sm, cur, ai - 1, si, q, win[q]);
-                if (twos) enqueue(sm, &sm.qc[cur][1], u, twos);
+                if (twos) enqueue<FLAT>(sm, &sm.qc[cur][1], u, twos);
             }
             __syncthreads();
             if (const uint32_t nq = sm.qc[cur][1] & 0xFFFFu) {
                 const uint32_t ne = sm.qc[cur][1] >> 16;
                 for (uint32_t e = threadIdx.x; e < nq; e += NT) {
                     int u, j;
-                    list_entry(sm, ne, nq, e, u, j);
+                    list_entry<FLAT>(sm, ne, nq, e, u, j);
                     const int ai = u / SS, si = u - ai * SS;
                     set_winner(sm, cur, ai, si, j, draw_winner(a, sm, ai, si, j, r0, c0, seed, step));
                 }
