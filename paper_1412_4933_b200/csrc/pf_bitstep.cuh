@@ -1006,16 +1006,16 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
     #pragma unroll
                 for (int si = 1; si <= NS; ++si) {
                     const uint32_t Am = sm.A[ai][si];
-                    if (bit(Am, lane)) {
-                        const uint32_t kc = bit(sm.K[0][ai][si], lane) | bit(sm.K[1][ai][si], lane) << 1 |
-                                            bit(sm.K[2][ai][si], lane) << 2;
-                        alist[na + __popc(Am & lt)] = uint16_t(kc << 12 | (32 * (si - 1) + lane));
-                    }
+                    if (bit(Am, lane)) alist[na + __popc(Am & lt)] = uint16_t(32 * (si - 1) + lane);
                     na += __popc(Am);
                 }
                 __syncwarp();
                 for (uint32_t e = lane; e < na; e += 32) {
-                    const int cc = alist[e] & 0xFFF, kc = alist[e] >> 12;
+                    // The direction code, once per arrival (not per segment and lane),
+                    // kept in the entry for the process loop.
+                    const int cc = alist[e], si = (cc >> 5) + 1, j = cc & 31;
+                    const int kc = int(bit(sm.K[0][ai][si], j) | bit(sm.K[1][ai][si], j) << 1 | bit(sm.K[2][ai][si], j) << 2);
+                    alist[e] = uint16_t(kc << 12 | cc);
                     const size_t src = size_t(b + kDR[kc]) * W + (c0 + cc + kDC[kc]);
                     cp_async<4>(asw + e, cw + src);
                     if (ACO) cp_async<8>(atr + e, tour + src);
