@@ -11,6 +11,8 @@
 
 #include <cstdint>
 
+#include <math_constants.h>
+
 #include "pf_glibc_log.h"
 
 namespace pfdev {
@@ -186,29 +188,28 @@ static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ 
     const double mu = __dmul_rn(__ldg(&k->sel_mu), cmax), sg = __dmul_rn(__ldg(&k->sel_sigma), cmax);
     double r = __dadd_rn(mu, __dmul_rn(sg, inverse_normal_cdf(u)));
     r = (r < 0.0) ? 0.0 : ((cmax < r) ? cmax : r); // std::clamp(r, 0, C_max)
-    double best = -1.0;
-    int ntied = 0;
-    uint32_t tied = 0; // slots in canonical order, 3 bits each
+    // The open slot(s) nearest r (src/lem.cpp:38-52). The reference's scan
+    // (reset on a strictly smaller gap, append on an equal one) ends with
+    // exactly the open slots whose gap equals the minimum, in canonical
+    // order; here that set is built branch-free as a bit mask.
+    double gap[8];
+    double best = CUDART_INF;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        if (!(open >> i & 1u)) continue;
-        const double gap = fabs(__dsub_rn(__ldg(&k->lem_score[i]), r));
-        if (ntied == 0 || gap < best) {
-            best = gap;
-            ntied = 1;
-            tied = uint32_t(i);
-        } else if (gap == best) {
-            tied |= uint32_t(i) << (3 * ntied);
-            ++ntied;
-        }
+        gap[i] = (open >> i & 1u) ? fabs(__dsub_rn(__ldg(&k->lem_score[i]), r)) : CUDART_INF;
+        best = (gap[i] < best) ? gap[i] : best;
     }
-    if (ntied > 1) {
+    uint32_t tied = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tied |= uint32_t((open >> i & 1u) != 0u && gap[i] == best) << i;
+    const int ntied = __popc(tied);
+    if (ntied > 1) {  // tie break: uniform(key.with_phase(TieBreak)) (src/lem.cpp:54-58)
         const double tu = uniform_from_bits(philox_bits(seed, step, kPhaseTieBreak, id, 0));
         int j = __double2int_rz(__dmul_rn(tu, double(ntied)));
         j = j < ntied - 1 ? j : ntied - 1;
-        return int(tied >> (3 * j) & 7u);
+        for (int t = 0; t < j; ++t) tied &= tied - 1u;  // drop the j lowest
     }
-    return int(tied & 7u);
+    return __ffs(tied) - 1;
 }
 
 // Slow path of aco_select (src/aco.cpp:64-92) given the numerators of the
