@@ -216,34 +216,37 @@ static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ 
 // open slots (aco_numerators, src/aco.cpp:39-51).
 static __device__ __forceinline__ int aco_choose(const double (&num)[8], uint32_t open, uint64_t seed, uint32_t step,
                                        uint32_t id) {
+    // Closed slots count as exact zeros (aco_numerators gives them 0,
+    // src/aco.cpp:39-51), and adding an exact zero changes no sum, so the
+    // candidates' sequential sums (src/aco.cpp:65-72, 80-89) are the running
+    // sums over all eight slots in canonical order. The first slot whose
+    // running sum exceeds u * total is open (a closed slot adds nothing), so
+    // the pick is the lowest set bit of a branch-free mask.
+    double v[8];
     double total = 0.0;
-    int k = 0, last = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        if (!(open >> i & 1u)) continue;
-        total = __dadd_rn(total, num[i]);
-        ++k;
-        last = i;
+        v[i] = (open >> i & 1u) ? num[i] : 0.0;
+        total = __dadd_rn(total, v[i]);
     }
+    const int k = __popc(open), last = 31 - __clz(open);
     const double u = uniform_from_bits(philox_bits(seed, step, kPhaseAcoSelect, id, 0));
-    if (total <= 0.0) {
+    if (total <= 0.0) {  // src/aco.cpp:77-79
         int j = __double2int_rz(__dmul_rn(u, double(k)));
         j = j < k - 1 ? j : k - 1;
-        for (int i = 0; i < 8; ++i) {
-            if (!(open >> i & 1u)) continue;
-            if (j-- == 0) return i;
-        }
-        return last;
+        uint32_t m = open;
+        for (int t = 0; t < j; ++t) m &= m - 1u;
+        return __ffs(m) - 1;
     }
     const double target = __dmul_rn(u, total);
     double cum = 0.0;
+    uint32_t over = 0u;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        if (!(open >> i & 1u)) continue;
-        cum = __dadd_rn(cum, num[i]);
-        if (cum > target) return i;
+        cum = __dadd_rn(cum, v[i]);
+        over |= uint32_t(cum > target) << i;
     }
-    return last;
+    return over ? __ffs(over) - 1 : last;
 }
 
 __device__ __forceinline__ double pheromone_term(const StepConsts* __restrict__ k, double tau) {
