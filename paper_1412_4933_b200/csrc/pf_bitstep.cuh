@@ -380,19 +380,32 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
         // before the start of the allocation).
         using S = typename Tau<TV>::S;
         const S* t0 = reinterpret_cast<const S*>(tin + size_t(b) * W + c) + (bottom ? 1 : 0);
+        // Goal-relative slot offsets of a Top agent (inc/grid.hpp:19-43); a
+        // Bottom agent's are their point reflection (inc/grid.hpp:45-49).
+        constexpr int kSlotDR[8] = {1, 1, 1, 0, 0, -1, -1, -1};
+        constexpr int kSlotDC[8] = {0, -1, 1, -1, 1, 0, -1, 1};
+        const ptrdiff_t sg = bottom ? -1 : 1;
         double tn[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint8_t code = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-            tn[i] = (open >> i & 1u) ? double(__ldg(t0 + 2 * (ptrdiff_t(kDR[code]) * W + kDC[code]))) : 0.0;
-        }
-        double num[8];
-#pragma unroll
         for (int i = 0; i < 8; ++i)
-            num[i] = (open >> i & 1u) ? __dmul_rn(pheromone_term(a.kc, tn[i]), __ldg(&a.kc->eta[i])) : 0.0;
+            tn[i] = (open >> i & 1u) ? double(__ldg(t0 + 2 * sg * (ptrdiff_t(kSlotDR[i]) * W + kSlotDC[i]))) : 0.0;
+        // aco_numerators (src/aco.cpp:39-51), the alpha case taken once.
+        double num[8];
+        const int mode = __ldg(&a.kc->alpha_mode);
+        if (mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) num[i] = (open >> i & 1u) ? __dmul_rn(tn[i], a.k.eta[i]) : 0.0;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                num[i] = (open >> i & 1u) ? __dmul_rn(pheromone_term(a.kc, tn[i]), a.k.eta[i]) : 0.0;
+        }
         s = aco_choose(num, open, seed, step, id);
     }
-    return bottom ? 7 - kSlotCodeTop[s] : kSlotCodeTop[s];
+    // Slot -> row-major code: kSlotCodeTop packed in nibbles (6,5,7,3,4,1,0,2),
+    // a Bottom agent's code is 7 - that.
+    const int code = int((0x20143756u >> (4 * s)) & 7u);
+    return bottom ? 7 - code : code;
 }
 
 // Keyed draw for a contested destination at bit j of resolution unit (ai, si):
