@@ -384,11 +384,15 @@ __device__ __forceinline__ int draw_intent(const StepArgs& a, const Smem& sm, in
         // Bottom agent's are their point reflection (inc/grid.hpp:45-49).
         constexpr int kSlotDR[8] = {1, 1, 1, 0, 0, -1, -1, -1};
         constexpr int kSlotDC[8] = {0, -1, 1, -1, 1, 0, -1, 1};
-        const ptrdiff_t sg = bottom ? -1 : 1;
+        // Interleaved {top, bottom}: a neighbour (dr, dc) is 2 * (dr * W + dc)
+        // scalars away; the three rows' pointers and the column step are
+        // formed once.
+        const ptrdiff_t c2 = bottom ? -2 : 2, r2 = c2 * W;
+        const S* rows[3] = {t0 - r2, t0, t0 + r2};  // goal-relative rows dr = -1, 0, +1
         double tn[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            tn[i] = (open >> i & 1u) ? double(__ldg(t0 + 2 * sg * (ptrdiff_t(kSlotDR[i]) * W + kSlotDC[i]))) : 0.0;
+            tn[i] = (open >> i & 1u) ? double(__ldg(rows[kSlotDR[i] + 1] + c2 * kSlotDC[i])) : 0.0;
         // aco_numerators (src/aco.cpp:39-51), the alpha case taken once.
         double num[8];
         const int mode = __ldg(&a.kc->alpha_mode);
