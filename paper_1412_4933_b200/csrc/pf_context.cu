@@ -327,6 +327,10 @@ static int fill_consts(pf_ctx* ctx) {
         k.lem_score[i] = d[0] / d[i];
         k.eta[i] = std::pow(1.0 / d[i], c.beta);
     }
+    // The device's lem_select takes C_max as the first open slot's score:
+    // scores must not grow with the slot index (true for every d0 > 1).
+    for (int i = 1; i < 8; ++i)
+        if (k.lem_score[i] > k.lem_score[i - 1]) return fail(PF_ERR_CONFIG, "distance table not monotone in slot order");
     k.sel_mu = c.sel_mu;
     k.sel_sigma = c.sel_sigma;
     k.alpha = c.alpha;
@@ -353,11 +357,11 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->row_begin = cfg->row_end ? cfg->row_begin : 0;
     ctx->rows_owned = cfg->row_end ? cfg->row_end - cfg->row_begin : cfg->height;
     ctx->rows_buf = ctx->rows_owned + 2 * pfk::kGhost;
-    fill_consts(ctx);
     auto cleanup = [&](int rc) {
         pf_destroy(ctx);
         return rc;
     };
+    if (int rc = fill_consts(ctx)) return cleanup(rc);
     if (cudaSetDevice(cfg->device) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "cudaSetDevice failed"));
     if (pfk::configure_step_bits() != 0) return cleanup(fail(PF_ERR_CUDA, "cannot configure the step kernel's shared memory"));
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||

@@ -176,12 +176,11 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
 // divergent AS241 tail stays out of line.
 static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ k, uint32_t open, uint64_t seed,
                                        uint32_t step, uint32_t id) {
-    double cmax = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double s = (open >> i & 1u) ? __ldg(&k->lem_score[i]) : 0.0;
-        cmax = (cmax < s) ? s : cmax; // std::max
-    }
+    // C_max = the largest open score (src/lem.cpp:28-30). With d0 > 1
+    // (validate) the distance table grows with the slot index (d_F < d_FL <
+    // d_L < d_B < d_BL) and dmin/d_i shrinks, so that is the first open
+    // slot's score (host-checked in fill_consts).
+    const double cmax = __ldg(&k->lem_score[__ffs(open) - 1]);
     // normal(key, mu_sel*C_max, sigma_sel*C_max) (src/lem.cpp:34, src/rng.cpp:152-156)
     const uint64_t bits = philox_bits(seed, step, kPhaseLemSelect, id, 0);
     const double u = __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
