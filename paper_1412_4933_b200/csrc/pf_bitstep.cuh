@@ -834,13 +834,16 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // Large LEM grids only (C5 LEM -7..-10%): for ACO the pheromone stream
         // bounds the step and the check cost +1.7% at C5, and in the dense
         // small-grid variants it made ptxas spill (C4 single +20%).
+        // (Row by row: warp w checks staged rows w, w + NW, ..., lanes < SP.)
         bool any_agent = ACO || COMPACT;
         if (!ACO && !COMPACT)
-            for (int i = threadIdx.x; i < SR * SP; i += NT) {
-                const uint2 q = sm.pl[slot(base, i / SP)][i % SP];
-                any_agent |= (q.x ^ q.y) != 0u;
-            }
-        if (ACO || COMPACT || __syncthreads_or(any_agent)) {
+            for (int r = warp; r < SR; r += NW)
+                if (lane < SP) {
+                    const uint2 q = sm.pl[slot(base, r)][lane];
+                    any_agent |= (q.x ^ q.y) != 0u;
+                }
+        const bool has_agents = ACO || COMPACT || __syncthreads_or(any_agent);
+        if (has_agents) {
             // ------------------------------------------------------------ S1
             // Intents for rows -2 .. RT+1, all staged segments (halo segments
             // only at the two columns next to the strip). A thread takes two
@@ -970,6 +973,14 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         __syncthreads();
 #endif
         // ------------------------------------------------------------ S3
+#ifndef PF_BITS_STREAM_ONLY
+        if (!has_agents) {  // (large LEM grids) an empty window: the tile's planes are copied as they are
+            for (int i = threadIdx.x; i < RT * NS; i += NT) {
+                const int rr = i / NS, sg = i - rr * NS;
+                if (r0 + rr < a.rows_owned) oout[size_t(kGhost + r0 + rr) * a.p.wsp + sg] = sm.pl[slot(base, rr + 3)][sg + 2];
+            }
+        } else
+#endif
         for (int rr = warp; rr < RT; rr += NW) {
             const int lr = r0 + rr;
             if (lr >= a.rows_owned) break;
