@@ -831,18 +831,22 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // for every row (planes copied, ACO pheromone evaporated). The work
         // scratch of this tile is already zero. (The crowd-free middle of the
         // C5 grid, most of it early in a run.)
-        // Large LEM grids only (C5 LEM -7..-10%): for ACO the pheromone stream
-        // bounds the step and the check cost +1.7% at C5, and in the dense
-        // small-grid variants it made ptxas spill (C4 single +20%).
+        // LEM on the 256/320-column geometries, when the starting bands cover
+        // under 30% of the rows (StepArgs::skip_empty: C5 LEM -14%, C1 x64
+        // -10%; C3 x64, whose bands cover 45%, would pay for the check). For
+        // ACO the pheromone stream bounds the step (+1.7% at C5), and in the
+        // small-grid geometry the check made ptxas spill (C4 single +20%).
         // (Row by row: warp w checks staged rows w, w + NW, ..., lanes < SP.)
-        bool any_agent = ACO || COMPACT;
-        if (!ACO && !COMPACT)
+        constexpr bool kSkipEmpty = !ACO && NS >= 8;
+        const bool check = kSkipEmpty && a.skip_empty;
+        bool any_agent = !check;
+        if (check)
             for (int r = warp; r < SR; r += NW)
                 if (lane < SP) {
                     const uint2 q = sm.pl[slot(base, r)][lane];
                     any_agent |= (q.x ^ q.y) != 0u;
                 }
-        const bool has_agents = ACO || COMPACT || __syncthreads_or(any_agent);
+        const bool has_agents = !check || __syncthreads_or(any_agent);
         if (has_agents) {
             // ------------------------------------------------------------ S1
             // Intents for rows -2 .. RT+1, all staged segments (halo segments

@@ -313,6 +313,14 @@ int pf_destroy(pf_ctx* ctx) {
     return PF_OK;
 }
 
+// StepArgs::skip_empty: the widest replica's two starting bands cover under
+// 30% of the grid's rows.
+static void set_skip_empty(pf_ctx* ctx) {
+    int band = 0;
+    for (const auto& r : ctx->reps) band = std::max(band, int(r.band));
+    ctx->args.skip_empty = 2.0 * band < 0.3 * ctx->cfg.height ? 1 : 0;
+}
+
 static int fill_consts(pf_ctx* ctx) {
     const pf_config& c = ctx->cfg;
     pfdev::StepConsts& k = ctx->args.k;
@@ -469,6 +477,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     if (size_t(cfg->width) * size_t(cfg->height) >= (size_t(1) << 20))
         for (int r = 0; r < std::min(cfg->replicas, 4); ++r)
             pfhost::prefetch_placement(cfg->width, cfg->height, cfg->agents_per_side, ctx->reps[size_t(r)].seed);
+    set_skip_empty(ctx);
     {
         auto* d_rep = static_cast<pfdev::ReplicaParams*>(alloc(ctx->reps.size() * sizeof(pfdev::ReplicaParams)));
         if (!d_rep || cudaMemcpy(d_rep, ctx->reps.data(), ctx->reps.size() * sizeof(pfdev::ReplicaParams),
@@ -513,6 +522,10 @@ int pf_set_replicas(pf_ctx* ctx, const int32_t* agents_per_side, const uint64_t*
                        reps.size() * sizeof(pfdev::ReplicaParams), cudaMemcpyHostToDevice));
     ctx->reps.swap(reps);
     ctx->rep_aps.swap(aps);
+    set_skip_empty(ctx);
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // they captured the old StepArgs
+    ctx->graphs.clear();
+    ctx->graph_launches.clear();
     return PF_OK;
 }
 

@@ -84,6 +84,9 @@ struct StepArgs {
     // {f32, f32} (PF_KERNEL_FUSED_F32, tolerance-only); Planes::tau then
     // points at float2 data.
     int tau_f32;
+    // LEM: look for windows without agents and skip their S1/S2 (the
+    // starting bands of every replica cover < 30% of the rows).
+    int skip_empty;
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
