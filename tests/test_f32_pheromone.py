@@ -85,3 +85,43 @@ def test_f32_storage_halves_the_pheromone_planes_on_load_and_store():
     assert (tb == s.pheromone_bottom.astype(np.float32).astype(np.float64)).all()
     assert (idx == s.index).all() and (ag == s.agents).all()
     c.close()
+
+
+def test_f32_linked_shards_equal_unsharded_f32():
+    """fp32 storage through the fused halo exchange: 3 linked row shards
+    (mirror stores of float2 pheromone rows) equal the unsharded fp32 run
+    bit for bit (both round the same fp64 results)."""
+    import paper_1412_4933_b200 as p
+    from paper_1412_4933_b200 import _lib
+    from paper_1412_4933_b200.engine import _pf_config
+    from paper_1412_4933_b200.sharding import row_partition
+
+    kw = dict(width=96, height=112, agents_per_side=1500, model="aco", seed=4)
+    cfg = to_config(kw)
+    steps = 150
+    whole = p.Ensemble(cfg, replicas=1, seed=4, kernel="fused_f32")
+    whole_rep = whole.run(steps)
+    ref = whole.state(0)
+    shards = []
+    for lo, hi in row_partition(cfg.height, 3):
+        c = _lib.Context(_pf_config(cfg, 4, row_begin=lo, row_end=hi, kernel="fused_f32"))
+        c.init_environment()
+        shards.append(c)
+    _lib.link_shards(shards)
+    for c in shards:
+        c.step_async(steps)
+    for c in shards:
+        c.synchronize()
+    tot = sum(c.read_reports(steps)["moved"].astype(np.int64) for c in shards)
+    assert (tot == whole_rep["moved"]).all()
+    H, W = cfg.height, cfg.width
+    occ, idx = np.zeros((H, W), np.uint8), np.zeros((H, W), np.uint32)
+    ag = np.zeros(2 * cfg.agents_per_side, _lib.AGENT_DTYPE)
+    tt, tb = np.zeros((H, W)), np.zeros((H, W))
+    for c in shards:
+        assert c.store(0, occ, idx, ag, tt, tb) == steps
+    assert (idx == ref.index).all() and (occ == ref.occupancy).all()
+    assert (tt == ref.pheromone_top).all() and (tb == ref.pheromone_bottom).all()
+    for c in shards:
+        c.close()
+    whole.close()

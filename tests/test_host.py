@@ -170,3 +170,30 @@ def test_device_calls_fail_loudly_without_gpu():
         eng.step(s)
     with pytest.raises(_lib.DeviceError):
         p.Ensemble(cfg, replicas=2)
+
+
+def test_placement_cache_concurrent_requests():
+    """Several threads asking for the same (and different) placements at once
+    get identical, correct results (one computation per key, shared)."""
+    import threading
+
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState, Scenario
+
+    kw = dict(width=96, height=96, agents_per_side=1200, model="aco")
+    out = {}
+
+    def work(i):
+        seed = 30 + (i % 3)
+        out[i] = (seed, p.new_environment(to_config(dict(kw, seed=seed)), seed))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(9)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for seed in (30, 31, 32):
+        want = OracleState(Scenario(**dict(kw, seed=seed))).hashes()
+        for i, (sd, st) in out.items():
+            if sd == seed:
+                assert hashes_of(st) == want
