@@ -11,6 +11,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <deque>
+#include <exception>
 #include <future>
 #include <list>
 #include <map>
@@ -210,15 +211,22 @@ std::shared_ptr<const Placement> compute(int32_t width, int32_t height, int32_t 
     auto pl = std::make_shared<Placement>();
     pl->band = band_height(n, width);
     const int32_t band = pl->band;
+    std::exception_ptr err[2];
     auto side = [&](int s) {
-        std::vector<uint32_t>& out = pl->cells[s];
-        out.resize(size_t(std::max(0, n)));
-        place_side(width, uint32_t(s + 1), s == 0 ? 0 : height - band, s == 0 ? band : height, n, 0, seed,
-                   [&](uint32_t cell, uint32_t k) { out[k] = cell; });
+        try {
+            std::vector<uint32_t>& out = pl->cells[s];
+            out.resize(size_t(std::max(0, n)));
+            place_side(width, uint32_t(s + 1), s == 0 ? 0 : height - band, s == 0 ? band : height, n, 0, seed,
+                       [&](uint32_t cell, uint32_t k) { out[k] = cell; });
+        } catch (...) {
+            err[s] = std::current_exception();
+        }
     };
     std::thread bottom(side, 1);  // the two sides are independent swap chains
     side(0);
     bottom.join();
+    for (const auto& e : err)
+        if (e) std::rethrow_exception(e);
     return pl;
 }
 
