@@ -157,14 +157,7 @@ size_t pool_threads() { return pool().threads(); }
 
 void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
     const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(hw, std::max<size_t>(1, n / (1u << 16)));
-    if (nt <= 1) {
-        fn(0, n);
-        return;
-    }
-    std::vector<std::thread> ts;
-    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
-    for (auto& t : ts) t.join();
+    pool_for(n, std::min<size_t>(hw, std::max<size_t>(1, n / (1u << 16))), fn);
 }
 
 void place_side(int32_t width, uint32_t group, int32_t row_begin, int32_t row_end, int32_t n, uint32_t first_id,
