@@ -836,16 +836,21 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // -10%; C3 x64, whose bands cover 45%, would pay for the check). For
         // ACO the pheromone stream bounds the step (+1.7% at C5), and in the
         // small-grid geometry the check made ptxas spill (C4 single +20%).
-        // (Row by row: warp w checks staged rows w, w + NW, ..., lanes < SP.)
+        // (The window is SR consecutive ring rows of SP segments, possibly
+        // wrapping: read as 16-byte segment pairs, SP being even.)
         constexpr bool kSkipEmpty = !ACO && NS >= 8;
+        static_assert(SP % 2 == 0, "staged rows are whole 16-byte units");
         const bool check = kSkipEmpty && a.skip_empty;
         bool any_agent = !check;
-        if (check)
-            for (int r = warp; r < SR; r += NW)
-                if (lane < SP) {
-                    const uint2 q = sm.pl[slot(base, r)][lane];
-                    any_agent |= (q.x ^ q.y) != 0u;
-                }
+        if (check) {
+            const uint4* ring = reinterpret_cast<const uint4*>(&sm.pl[0][0]);
+            for (int t = threadIdx.x; t < SR * SP / 2; t += NT) {
+                int i = base * (SP / 2) + t;
+                if (i >= RING * (SP / 2)) i -= RING * (SP / 2);
+                const uint4 q = ring[i];
+                any_agent |= ((q.x ^ q.y) | (q.z ^ q.w)) != 0u;
+            }
+        }
         const bool has_agents = !check || __syncthreads_or(any_agent);
         if (has_agents) {
             // ------------------------------------------------------------ S1
@@ -979,9 +984,13 @@ __global__ void __launch_bounds__(NT, CTAS) step_bits_kernel(const StepArgs a, i
         // ------------------------------------------------------------ S3
 #ifndef PF_BITS_STREAM_ONLY
         if (!has_agents) {  // (large LEM grids) an empty window: the tile's planes are copied as they are
-            for (int i = threadIdx.x; i < RT * NS; i += NT) {
-                const int rr = i / NS, sg = i - rr * NS;
-                if (r0 + rr < a.rows_owned) oout[size_t(kGhost + r0 + rr) * a.p.wsp + sg] = sm.pl[slot(base, rr + 3)][sg + 2];
+            // 16-byte segment pairs: NS, the row pitch and the strip offsets are even.
+            static_assert(NS % 2 == 0, "strips are whole 16-byte units");
+            for (int i = threadIdx.x; i < RT * NS / 2; i += NT) {
+                const int rr = i / (NS / 2), sp = i - rr * (NS / 2);
+                if (r0 + rr < a.rows_owned)
+                    reinterpret_cast<uint4*>(oout + size_t(kGhost + r0 + rr) * a.p.wsp)[sp] =
+                        reinterpret_cast<const uint4*>(&sm.pl[slot(base, rr + 3)][2])[sp];
             }
         } else
 #endif
