@@ -152,7 +152,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, which):
+        """Record the start ("t0") / end ("t1") of the timed region."""
+        setattr(self, which, time.perf_counter())
 
     def __exit__(self, *a):
         if self.proc:
@@ -163,21 +167,33 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        rows = []
-        for ln in self.lines:
+        """Samples read during the timed region (marks t0..t1, plus the 50 ms
+        after it for nvidia-smi's output lag); if the region is too short for
+        any, the ones within 100 ms of it."""
+        parsed = []
+        for ts, ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                parsed.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        window = "whole run"
+        rows = parsed
+        if t0 is not None and t1 is not None:
+            rows = [r for r in parsed if t0 <= r[0] <= t1 + 0.05]
+            window = "timed region"
+            if not rows:
+                rows = [r for r in parsed if t0 - 0.1 <= r[0] <= t1 + 0.1]
+                window = "timed region +- 100 ms"
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({names[i] for _, _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows), "window": window, "interval_ms": 20}
 
 
 def scenario(name):
@@ -472,6 +488,7 @@ def run_gpu_arm(args):
         barrier()
         torch.cuda.synchronize()
         launches0 = eng.ctx.launches
+        clocks.mark("t0")
         e0.record(stream)
         if world == 1:
             eng.ctx.step_async(args.steps)  # CUDA-graph batches
@@ -480,6 +497,8 @@ def run_gpu_arm(args):
         e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
+        clocks.mark("t1")
+        time.sleep(0.06)  # nvidia-smi's last samples of the region
         launches = eng.ctx.launches - launches0
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
