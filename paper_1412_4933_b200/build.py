@@ -24,7 +24,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = GENCODE + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
                      "-I", os.path.join(ROOT, "include")]
-SOURCES = ["pf_kernels.cu", "pf_bitstep.cu", "pf_bitstep_ns8.cu", "pf_bitstep_ns10.cu", "pf_bitstep_small.cu",
+SOURCES = ["pf_kernels.cu", "pf_bitstep.cu", "pf_bitstep_ns8.cu", "pf_bitstep_ns10.cu", "pf_bitstep_small.cu", "pf_cluster.cu",
            "pf_context.cu", "pf_setup.cpp"]
 
 

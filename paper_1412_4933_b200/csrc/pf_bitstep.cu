@@ -43,6 +43,9 @@ int configure_step_bits() { return bits_ns8::configure() | bits_ns10::configure(
 // even (2-agent-dense LEM and sparse grids lose there). The occupancy-plane
 // pitch (strips of 8 or 10 segments) also fits the 2-segment strips.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s) {
+    if (a.cluster > 0 && !a.peer[0].cell && !a.peer[1].cell) {
+        if (const int n = launch_cluster_lem(a, slot, parity, s)) return n;
+    }
     const long long strips = (a.k.W + 255) / 256, tiles16 = strips * ((a.rows_owned + 15) / 16) * a.replicas;
     if (a.small_tiles == 1 || (a.small_tiles < 0 && tiles16 < 2LL * a.num_sms)) return bits_small::launch(a, slot, parity, s);
     if (a.strip_segs == 10) return bits_ns10::launch(a, slot, parity, s);

@@ -321,6 +321,14 @@ static void set_skip_empty(pf_ctx* ctx) {
     ctx->args.skip_empty = 2.0 * band < 0.3 * ctx->cfg.height ? 1 : 0;
 }
 
+// Small sparse LEM grids run on the cluster-resident kernel (pf_cluster.cu).
+static void set_cluster(pf_ctx* ctx) {
+    uint32_t most = 0;
+    for (const auto& r : ctx->reps) most = std::max(most, r.n_agents);
+    ctx->args.cluster_cap = 0;
+    ctx->args.cluster = ctx->bits() ? pfk::plan_cluster_lem(ctx->args, most, &ctx->args.cluster_cap) : 0;
+}
+
 static int fill_consts(pf_ctx* ctx) {
     const pf_config& c = ctx->cfg;
     pfdev::StepConsts& k = ctx->args.k;
@@ -492,6 +500,7 @@ int pf_create(const pf_config* cfg, pf_ctx** out) {
     ctx->args.rows_owned = ctx->rows_owned;
     ctx->args.rows_buf = ctx->rows_buf;
     ctx->args.replicas = cfg->replicas;
+    set_cluster(ctx);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup(fail(PF_ERR_CUDA, "init failed"));
     if (ctx->plane() * 4 >= Stager::kChunk &&
         (ctx->stage[0].ready() != cudaSuccess || ctx->stage[1].ready() != cudaSuccess))
@@ -523,6 +532,7 @@ int pf_set_replicas(pf_ctx* ctx, const int32_t* agents_per_side, const uint64_t*
     ctx->reps.swap(reps);
     ctx->rep_aps.swap(aps);
     set_skip_empty(ctx);
+    set_cluster(ctx);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);  // they captured the old StepArgs
     ctx->graphs.clear();
     ctx->graph_launches.clear();

@@ -174,17 +174,20 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
 // and at least one slot is open. Returns the chosen goal-relative slot.
 // Inlined into the draw loops (A/B: C4 x64 -9%, C5 LEM -6%); the rarely
 // divergent AS241 tail stays out of line.
-static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ k, uint32_t open, uint64_t seed,
-                                       uint32_t step, uint32_t id) {
+// tab.score(i), tab.mu(), tab.sigma() return lem_score[i], sel_mu and
+// sel_sigma (the step constants, from global memory or a shared-memory copy).
+template <class Tab>
+__device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, uint64_t seed, uint32_t step,
+                                               uint32_t id) {
     // C_max = the largest open score (src/lem.cpp:28-30). With d0 > 1
     // (validate) the distance table grows with the slot index (d_F < d_FL <
     // d_L < d_B < d_BL) and dmin/d_i shrinks, so that is the first open
     // slot's score (host-checked in fill_consts).
-    const double cmax = __ldg(&k->lem_score[__ffs(open) - 1]);
+    const double cmax = tab.score(__ffs(open) - 1);
     // normal(key, mu_sel*C_max, sigma_sel*C_max) (src/lem.cpp:34, src/rng.cpp:152-156)
     const uint64_t bits = philox_bits(seed, step, kPhaseLemSelect, id, 0);
     const double u = __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
-    const double mu = __dmul_rn(__ldg(&k->sel_mu), cmax), sg = __dmul_rn(__ldg(&k->sel_sigma), cmax);
+    const double mu = __dmul_rn(tab.mu(), cmax), sg = __dmul_rn(tab.sigma(), cmax);
     double r = __dadd_rn(mu, __dmul_rn(sg, inverse_normal_cdf(u)));
     r = (r < 0.0) ? 0.0 : ((cmax < r) ? cmax : r); // std::clamp(r, 0, C_max)
     // The open slot(s) nearest r (src/lem.cpp:38-52). The reference's scan
@@ -195,7 +198,7 @@ static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ 
     double best = CUDART_INF;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        gap[i] = (open >> i & 1u) ? fabs(__dsub_rn(__ldg(&k->lem_score[i]), r)) : CUDART_INF;
+        gap[i] = (open >> i & 1u) ? fabs(__dsub_rn(tab.score(i), r)) : CUDART_INF;
         best = (gap[i] < best) ? gap[i] : best;
     }
     uint32_t tied = 0u;
@@ -209,6 +212,17 @@ static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ 
         for (int t = 0; t < j; ++t) tied &= tied - 1u;  // drop the j lowest
     }
     return __ffs(tied) - 1;
+}
+
+static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ k, uint32_t open, uint64_t seed,
+                                       uint32_t step, uint32_t id) {
+    struct Tab {
+        const StepConsts* k;
+        __device__ double score(int i) const { return __ldg(&k->lem_score[i]); }
+        __device__ double mu() const { return __ldg(&k->sel_mu); }
+        __device__ double sigma() const { return __ldg(&k->sel_sigma); }
+    };
+    return lem_choose_with(Tab{k}, open, seed, step, id);
 }
 
 // Slow path of aco_select (src/aco.cpp:64-92) given the numerators of the

@@ -87,12 +87,22 @@ struct StepArgs {
     // LEM: look for windows without agents and skip their S1/S2 (the
     // starting bands of every replica cover < 30% of the rows).
     int skip_empty;
+    // LEM, small unlinked grids: CTAs per thread-block cluster of the
+    // cluster-resident multi-step kernel (pf_cluster.cu), 0 = not used.
+    // Planned once per context (plan_cluster_lem).
+    int cluster;
+    int cluster_cap;        // its work-list capacity (entries)
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
 // Returns the number of kernel launches issued.
 int launch_step_bits(const StepArgs& a, int slot, int parity, cudaStream_t s);   // PF_KERNEL_FUSED
 int configure_step_bits();
+// Cluster-resident LEM kernel (pf_cluster.cu): the cluster size for these
+// args and the largest replica's agent count (0 = not applicable), and a
+// launch of a.nsteps steps with it.
+int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap);
+int launch_cluster_lem(const StepArgs& a, int slot, int parity, cudaStream_t s);
 int bits_strip_segments(int width, int model, bool tau_f32);  // strip width in segments (8 or 10)
 // Occupancy planes of rows [0, rows) from cell words (W columns; padding
 // segments untouched); written to occ0 and, if non-null, occ1.

@@ -16,6 +16,9 @@ steps, skip = int(sys.argv[1]), int(sys.argv[2])
 for name in sys.argv[3:]:
     cfg, reps, desc = bench.scenario(name)
     e = p.Ensemble(cfg, replicas=reps); e.run(5 + skip)
+    e.ctx.prepare_steps(steps)  # graph capture outside the timed region (as bench.py)
+    e.time_steps(steps)  # warm
+    e.ctx.prepare_steps(steps)
     tot, _ = e.time_steps(steps)
     print(f"{name} {tot/steps*1e3:.2f}", flush=True); e.close()
 '''
