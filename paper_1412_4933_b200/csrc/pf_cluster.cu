@@ -1,5 +1,5 @@
-// Cluster-resident multi-step kernel for small LEM scenarios (single 480^2
-// runs: C1, C3; PF_KERNEL_FUSED).
+// Cluster-resident multi-step kernel for small sparse LEM scenarios (single
+// 480^2 runs such as C1; PF_KERNEL_FUSED).
 //
 // A single small scenario is latency-bound on the persistent bit-plane kernel
 // (pf_bitstep.cuh): every step is a dependent chain of launch, TMA window
@@ -9,38 +9,41 @@
 // for all the steps of a launch: the grid is loaded once, every step runs
 // on-chip between two cluster barriers, and the result is written back once.
 // A LEM cell is its 32-bit word (id | crossed | group, 0 = empty) plus one
-// claim byte.
+// claim byte. Only sparse grids take this path (kMaxDensity): 16 SMs issue
+// every proposal, so dense grids keep the whole GPU.
 //
 // Layout: CTA q of a replica's cluster owns the column slice
 // [q * cpc, (q + 1) * cpc) of every row, so the crowds' horizontal bands
-// spread evenly over the CTAs and, with warp = row (strided) and lane =
-// column, over the threads. Its words are held with one ghost column on each
-// side (copies of the neighbours' edge columns, kWall at the arena's edges)
-// and a wall row above and below, so every proposal reads shared memory
-// only. Cross-slice traffic is stores: claims into a neighbour's claim bytes
-// (DSMEM atomics) and the commit's mirror writes into the neighbours' ghost
-// columns (DSMEM stores), all before the barrier that publishes them.
+// spread evenly over the CTAs. Its words are held with one ghost column on
+// each side (copies of the neighbours' edge columns, kWall at the arena's
+// edges) and a wall row above and below, so every proposal reads local
+// shared memory only. The work of a step is listed, not scanned: the slice's
+// agents (u16 entries row << 5 | column) and its claimed cells.
 //
 // One step (StepEngine::step, src/engine.cpp:53-193):
-//   S1  per agent: the LEM proposal (score_phase + intention_phase,
+//   S1  per listed agent: the LEM proposal (score_phase + intention_phase,
 //       src/engine.cpp:64-90, src/lem.cpp:20-60: the same forward priority
-//       and lem_choose_with as every other kernel, its table in shared
+//       and lem_choose_with as the other kernels, its tables in shared
 //       memory); a proposing agent ORs its claim bit (the row-major code of
-//       its cell seen from the destination) into the destination's claim byte
-//       (OR commutes: the result is order-independent).
+//       its cell seen from the destination) into the destination's claim
+//       byte, local or in a neighbour's slice (DSMEM atomics; OR commutes, so
+//       the result is order-independent), and the first claimer of a cell
+//       lists it with the cell's owner.
 //   --- cluster barrier
-//   S2  per claimed cell (empty at step start by construction): the keyed
-//       resolution on the global cell index (src/engine.cpp:101-122,
+//   S2  per listed claimed cell (empty at step start by construction): the
+//       keyed resolution on the global cell index (src/engine.cpp:101-122,
 //       pfdev::resolve), then the commit (src/engine.cpp:137-175): the
 //       winner's word moves in (crossed bit and counters, src/metrics.cpp:13-16)
-//       and its source is cleared, with the ghost copies. Each source is read
-//       and cleared only by the one destination it won, and destinations were
-//       empty at step start, so no two threads touch the same word.
+//       and its source is cleared, with the ghost copies (DSMEM stores). Each
+//       source is read and cleared only by the one destination it won, and
+//       destinations were empty at step start, so no two threads touch the
+//       same word.
 //   --- cluster barrier
-// Counters go to the report ring as in the other kernels.
+// Counters go to the report ring once per launch.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "pf_internal.h"
@@ -54,7 +57,8 @@ using namespace pfdev;
 
 constexpr int NT = 1024;
 constexpr int NW = NT / 32;
-constexpr size_t kSmemMax = 227 * 1024 - 256;  // dynamic shared memory per CTA
+constexpr size_t kSmemMax = 227 * 1024 - 4096;  // dynamic shared memory per CTA (static: counters, tables)
+constexpr int kMaxSteps = 256;                  // steps per launch (the context's graph batch)
 constexpr double kMaxDensity = 0.10;            // agents per cell (tools/cluster_sweep.py: faster up to ~12%)
 
 struct Geometry {
@@ -65,7 +69,7 @@ struct Geometry {
 };
 
 // Words: (H + 2) rows of cpc + 2 columns; claims: H rows of cpc rounded up
-// to whole u32 words (4 cells each); then three work lists of cap entries
+// to whole u32 words (4 cells each); then three u16 work lists of cap entries
 // (agents at step start, twice for ping-pong, and claimed cells).
 __host__ __device__ inline int word_pitch(int cpc) { return cpc + 2; }
 __host__ __device__ inline int claim_pitch(int cpc) { return (cpc + 3) / 4 * 4; }
@@ -81,6 +85,17 @@ __host__ __device__ inline size_t smem_bytes(int H, int cpc, int cap) {
 // grids of at most 2047 rows).
 constexpr int kColBits = 5;
 __device__ __forceinline__ uint16_t entry(int r, int lc) { return uint16_t(r << kColBits | lc); }
+__device__ __forceinline__ int entry_row(uint32_t e) { return int(e >> kColBits); }
+__device__ __forceinline__ int entry_col(uint32_t e) { return int(e & ((1u << kColBits) - 1u)); }
+
+// kDR / kDC / kSlotCodeTop as immediates (lanes index them divergently; the
+// constant bank would serialise the distinct addresses).
+__device__ __forceinline__ int dr_of(int c) { return int((0xA940u >> (2 * c)) & 3u) - 1; }
+__device__ __forceinline__ int dc_of(int c) { return int((0x9224u >> (2 * c)) & 3u) - 1; }
+__device__ __forceinline__ int slot_code(int slot, bool bottom) {
+    const int c = int((0x40C7EEu >> (3 * slot)) & 7u);
+    return bottom ? 7 - c : c;
+}
 
 // Append the calling lanes' entries (pred) to a shared-memory list: one
 // counter atomic per warp. Every lane of the warp must call it.
@@ -94,12 +109,34 @@ __device__ __forceinline__ void append(uint16_t* list, uint32_t* count, bool pre
     if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = e;
 }
 
+// glibc's log table (the AS241 tail) and the LEM constants in shared memory:
+// global loads after a cluster barrier (which invalidates L1) would each be
+// an L2 round trip.
+struct SharedLogTab {
+    const double* t;  // kLogTab row-major, then kLogPoly
+    __device__ double tab(int i, int j) const { return t[2 * i + j]; }
+    __device__ double poly(int i) const { return t[256 + i]; }
+};
+static __device__ __noinline__ double inverse_normal_cdf_shared(double p, const double* t) {
+    return inverse_normal_cdf_with(SharedLogTab{t}, p);
+}
+struct SharedLemTab {
+    const double* tab;
+    const double* logt;
+    double m, sg;
+    __device__ double score(int i) const { return tab[i]; }
+    __device__ double mu() const { return m; }
+    __device__ double sigma() const { return sg; }
+    __device__ double normal(double u) const { return inverse_normal_cdf_shared(u, logt); }
+};
+
 __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, int slot_idx, int parity, int cpc,
                                                             int cap) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t cnt[2][3];
+    __shared__ uint32_t cnt[kMaxSteps][3];       // per-step counters, flushed once at the end
     __shared__ uint32_t nagents[2], nclaims[2];  // list lengths, by step parity
     __shared__ double score_tab[8];
+    __shared__ double log_tab[2 * 128 + 5];
     cg::cluster_group cluster = cg::this_cluster();
     const int q = int(cluster.block_rank()), cl = int(cluster.num_blocks());
     const int rep = int(blockIdx.x) / cl;
@@ -124,9 +161,11 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
     uint32_t* const nclaims_l = q > 0 ? cluster.map_shared_rank(&nclaims[0], q - 1) : nullptr;
     uint32_t* const nclaims_r = q + 1 < cl ? cluster.map_shared_rank(&nclaims[0], q + 1) : nullptr;
 
-    if (threadIdx.x < 6) (&cnt[0][0])[threadIdx.x] = 0u;
+    for (int i = threadIdx.x; i < 3 * kMaxSteps; i += NT) (&cnt[0][0])[i] = 0u;
     if (threadIdx.x < 2) nagents[threadIdx.x] = nclaims[threadIdx.x] = 0u;
     if (threadIdx.x < 8) score_tab[threadIdx.x] = a.k.lem_score[threadIdx.x];
+    if (threadIdx.x < 256) log_tab[threadIdx.x] = kLogTab[threadIdx.x >> 1][threadIdx.x & 1];
+    if (threadIdx.x < 5) log_tab[256 + threadIdx.x] = kLogPoly[threadIdx.x];
     for (int i = threadIdx.x; i < H * CP / 4; i += NT) claim32[i] = 0u;
     for (int i = threadIdx.x; i < P; i += NT) {  // wall rows
         word[at(-1, i - 1)] = kWall;
@@ -160,14 +199,7 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
     }
     cluster.sync();
 
-    struct Tab {  // the LEM constants in shared memory / registers
-        const double* tab;
-        double m, sg;
-        __device__ double score(int i) const { return tab[i]; }
-        __device__ double mu() const { return m; }
-        __device__ double sigma() const { return sg; }
-    };
-    const Tab tab{score_tab, a.k.sel_mu, a.k.sel_sigma};
+    const SharedLemTab tab{score_tab, log_tab, a.k.sel_mu, a.k.sel_sigma};
     const int n = a.nsteps;
     uint32_t moved = 0, ntop = 0, nbot = 0;
     for (int s = 0; s < n; ++s) {
@@ -175,55 +207,40 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
         const int cur = s & 1;
         const uint16_t* const agents_in = agents0 + size_t(cur) * cap;
         uint16_t* const agents_out = agents0 + size_t(cur ^ 1) * cap;
-        // Counters of the previous step (its last barrier has passed).
-        if (threadIdx.x == 0 && s > 0) {
-            uint32_t* const c = cnt[cur ^ 1];
-            uint32_t* const slot = a.reports + (size_t(rep) * a.report_cap + (step - 1u) % uint32_t(a.report_cap)) * 4;
-            if (q == 0) slot[0] = step - 1u;
-            if (c[0]) atomicAdd(&slot[1], c[0]);
-            if (c[1]) atomicAdd(&slot[2], c[1]);
-            if (c[2]) atomicAdd(&slot[3], c[2]);
-            c[0] = c[1] = c[2] = 0u;
-        }
+#ifdef PF_CLUSTER_TRACE  // dev: per-warp phase clocks of one step (tools/cluster_trace.py)
+        long long tr[5];
+        tr[0] = clock64();
+#endif
         // ---- S1: the slice's agents (listed at the previous step's start or
         // arrived since; those that left are empty now): proposals and claims.
         const uint32_t na = nagents[cur];
         for (uint32_t base = 0; base < na; base += NT) {
             const uint32_t e = base + threadIdx.x;
-            uint16_t ent = 0;
-            uint32_t w = 0;
-            if (e < na) {
-                ent = agents_in[e];
-                w = word[at(int(ent >> kColBits), int(ent & ((1u << kColBits) - 1u)))];
-            }
+            const uint16_t ent = e < na ? agents_in[e] : uint16_t(0);
+            const int r = entry_row(ent), lc = entry_col(ent);
+            const uint32_t w = e < na ? word[at(r, lc)] : 0u;
             append(agents_out, &nagents[cur ^ 1], w != 0u, ent);  // the next step's list
-            int r = int(ent >> kColBits), lc = int(ent & ((1u << kColBits) - 1u));
-            uint8_t ic = kNone;
+            int ic = -1;
             if (w != 0u) {
                 const bool bottom = (w >> 30) == 2u;
                 // Forward priority: no draw (src/lem.cpp:23-26).
-                ic = bottom ? uint8_t(7 - kSlotCodeTop[0]) : kSlotCodeTop[0];
-                if (word[at(r + kDR[ic], lc + kDC[ic])] != 0u) {
+                ic = slot_code(0, bottom);
+                if (word[at(r + dr_of(ic), lc + dc_of(ic))] != 0u) {
                     uint32_t open = 0;
 #pragma unroll
                     for (int i = 1; i < 8; ++i) {
-                        const uint8_t c = bottom ? uint8_t(7 - kSlotCodeTop[i]) : kSlotCodeTop[i];
-                        open |= uint32_t(word[at(r + kDR[c], lc + kDC[c])] == 0u) << i;
+                        const int c = slot_code(i, bottom);
+                        open |= uint32_t(word[at(r + dr_of(c), lc + dc_of(c))] == 0u) << i;
                     }
-                    if (open == 0u) {
-                        ic = kNone;  // boxed in: stay
-                    } else {
-                        const int slot = lem_choose_with(tab, open, seed, step, w & kIdMask);
-                        ic = bottom ? uint8_t(7 - kSlotCodeTop[slot]) : kSlotCodeTop[slot];
-                    }
+                    ic = open == 0u ? -1 : slot_code(lem_choose_with(tab, open, seed, step, w & kIdMask), bottom);
                 }
             }
             // Claim: OR the bit into the destination's byte; the first
             // claimer of a cell lists it with the cell's owner.
             bool first_local = false;
             uint16_t dest = 0;
-            if (ic != kNone) {
-                const int rd = r + kDR[ic], ld = lc + kDC[ic];
+            if (ic >= 0) {
+                const int rd = r + dr_of(ic), ld = lc + dc_of(ic);
                 const uint32_t bitv = 1u << (7 - ic);
                 if (ld < 0) {
                     const int sh = 8 * ((cpc - 1) & 3);
@@ -240,7 +257,13 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
             }
             append(claimed, &nclaims[cur], first_local, dest);
         }
+#ifdef PF_CLUSTER_TRACE
+        tr[1] = clock64();
+#endif
         cluster.sync();
+#ifdef PF_CLUSTER_TRACE
+        tr[2] = clock64();
+#endif
         // ---- S2: resolution and commit at the claimed cells
         if (threadIdx.x == 0) {  // the lists of the next step: no reader or writer until the barrier
             nagents[cur] = 0u;
@@ -253,13 +276,13 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
             uint16_t ent = 0;
             if (e < nc) {
                 ent = claimed[e];
-                const int r = int(ent >> kColBits), lc = int(ent & ((1u << kColBits) - 1u));
+                const int r = entry_row(ent), lc = entry_col(ent);
                 const uint32_t cl8 = claim8[r * CP + lc];
                 claim8[r * CP + lc] = 0u;
                 const int grow = a.row_begin + r;
                 const uint64_t gidx = uint64_t(grow) * uint64_t(W) + uint64_t(c_lo + lc);
                 const int j = resolve(cl8, seed, step, gidx);
-                const int rs = r + kDR[j], ls = lc + kDC[j];
+                const int rs = r + dr_of(j), ls = lc + dc_of(j);
                 const uint32_t sw = word[at(rs, ls)];
                 // Clear the source, its owner's copy and the ghost copies.
                 word[at(rs, ls)] = 0u;
@@ -290,22 +313,32 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
         ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);
         nbot = __reduce_add_sync(0xFFFFFFFFu, nbot);
         if (lane == 0 && (moved | ntop | nbot)) {
-            atomicAdd(&cnt[cur][0], moved);
-            atomicAdd(&cnt[cur][1], ntop);
-            atomicAdd(&cnt[cur][2], nbot);
+            atomicAdd(&cnt[s][0], moved);
+            atomicAdd(&cnt[s][1], ntop);
+            atomicAdd(&cnt[s][2], nbot);
         }
         moved = ntop = nbot = 0u;
+#ifdef PF_CLUSTER_TRACE
+        tr[3] = clock64();
+#endif
         cluster.sync();
+#ifdef PF_CLUSTER_TRACE
+        tr[4] = clock64();
+        if (s == n / 2 && (q == 0 || q == 7) && lane == 0)
+            printf("TRACE step %u cta %d warp %d na %u nc %u  S1 %lld  bar1 %lld  S2 %lld  bar2 %lld\n", step, q, warp,
+                   nagents[cur ^ 1], nc, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3]);
+#endif
     }
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
-    if (threadIdx.x == 0 && n > 0) {
-        const uint32_t step = step0 + uint32_t(n - 1);
-        uint32_t* const c = cnt[(n - 1) & 1];
+    // The launch's counters go to the report ring (no global memory traffic
+    // inside the step loop: a cluster barrier's release would wait for it).
+    for (int t = threadIdx.x; t < n; t += NT) {
+        const uint32_t step = step0 + uint32_t(t);
         uint32_t* const slot = a.reports + (size_t(rep) * a.report_cap + step % uint32_t(a.report_cap)) * 4;
         if (q == 0) slot[0] = step;
-        if (c[0]) atomicAdd(&slot[1], c[0]);
-        if (c[1]) atomicAdd(&slot[2], c[1]);
-        if (c[2]) atomicAdd(&slot[3], c[2]);
+        if (cnt[t][0]) atomicAdd(&slot[1], cnt[t][0]);
+        if (cnt[t][1]) atomicAdd(&slot[2], cnt[t][1]);
+        if (cnt[t][2]) atomicAdd(&slot[3], cnt[t][2]);
     }
     // Write back the words (0 where empty) and the occupancy planes of the
     // final parity, 32-column segments spread over the cluster's CTAs (a
@@ -399,6 +432,7 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
 // a.nsteps steps as one cluster-resident launch; returns the launches issued.
 int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     using namespace cluster_lem;
+    if (a.nsteps > kMaxSteps) return 0;
     Geometry g = geometry(a, a.cluster, 0);
     g.cap = a.cluster_cap;
     g.bytes = smem_bytes(a.rows_owned, g.cpc, g.cap);

@@ -106,7 +106,14 @@ __device__ __forceinline__ double horner8(const double (&c)[8], double r) {
 static __device__ const double kLogTab[128][2] = PF_LOG_TAB_INIT;
 static __device__ const double kLogPoly[5] = PF_LOG_POLY_INIT;
 
-__device__ __forceinline__ double glibc_log(double x) {
+// lt.tab(i, j) / lt.poly(i): kLogTab / kLogPoly (global memory, or a copy).
+struct GlobalLogTab {
+    __device__ double tab(int i, int j) const { return __ldg(&kLogTab[i][j]); }
+    __device__ double poly(int i) const { return __ldg(&kLogPoly[i]); }
+};
+
+template <class LT>
+__device__ __forceinline__ double glibc_log_with(const LT& lt, double x) {
     const uint64_t ix = uint64_t(__double_as_longlong(x));
     const uint64_t top = ix >> 48;
     if (ix - 0x3fee000000000000ull < 0x3ff1090000000000ull - 0x3fee000000000000ull || top - 0x0010u >= 0x7ff0u - 0x0010u)
@@ -116,22 +123,25 @@ __device__ __forceinline__ double glibc_log(double x) {
     const int k = int(int64_t(tmp) >> 52);
     const double z = __longlong_as_double((long long)(ix - (tmp & (0xfffull << 52))));
     const double kd = double(k);
-    const double w = __fma_rn(kd, PF_LOG_LN2HI, __ldg(&kLogTab[i][1]));
-    const double r = __fma_rn(z, __ldg(&kLogTab[i][0]), -1.0);
-    const double p21 = __fma_rn(r, __ldg(&kLogPoly[2]), __ldg(&kLogPoly[1]));
+    const double w = __fma_rn(kd, PF_LOG_LN2HI, lt.tab(i, 1));
+    const double r = __fma_rn(z, lt.tab(i, 0), -1.0);
+    const double p21 = __fma_rn(r, lt.poly(2), lt.poly(1));
     const double hi = __dadd_rn(r, w);
     const double r2 = __dmul_rn(r, r);
     double lo = __dadd_rn(__dsub_rn(w, hi), r);
     lo = __fma_rn(kd, PF_LOG_LN2LO, lo);
     const double r3 = __dmul_rn(r, r2);
-    double p43 = __fma_rn(r, __ldg(&kLogPoly[4]), __ldg(&kLogPoly[3]));
-    lo = __fma_rn(r2, __ldg(&kLogPoly[0]), lo);
+    double p43 = __fma_rn(r, lt.poly(4), lt.poly(3));
+    lo = __fma_rn(r2, lt.poly(0), lo);
     p43 = __fma_rn(p43, r2, p21);
     return __dadd_rn(__fma_rn(r3, p43, lo), hi);
 }
 
+__device__ __forceinline__ double glibc_log(double x) { return glibc_log_with(GlobalLogTab{}, x); }
+
 // Wichura AS241 PPND16 (src/rng.cpp:61-150), same coefficients and order.
-static __device__ __noinline__ double inverse_normal_cdf(double p) {
+template <class LT>
+__device__ __forceinline__ double inverse_normal_cdf_with(const LT& lt, double p) {
     const double q = __dsub_rn(p, 0.5);
     if (fabs(q) <= 0.425) {
         constexpr double num[8] = {2.5090809287301226727e3, 3.3430575583588128105e4, 6.7265770927008700853e4,
@@ -144,7 +154,7 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
         return __ddiv_rn(__dmul_rn(q, horner8(num, r)), horner8(den, r));
     }
     double r = (q < 0.0) ? p : __dsub_rn(1.0, p);
-    r = __dsqrt_rn(-glibc_log(r));
+    r = __dsqrt_rn(-glibc_log_with(lt, r));
     double val;
     if (r <= 5.0) {
         constexpr double num[8] = {7.74545014278341407640e-4, 2.27238449892691845833e-2, 2.41780725177450611770e-1,
@@ -168,6 +178,9 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
     return (q < 0.0) ? -val : val;
 }
 
+static __device__ __noinline__ double inverse_normal_cdf(double p) { return inverse_normal_cdf_with(GlobalLogTab{}, p); }
+
+
 // ----------------------------------------------------------- proposals
 
 // Slow path of lem_select (src/lem.cpp:28-60): the forward slot is blocked
@@ -175,7 +188,8 @@ static __device__ __noinline__ double inverse_normal_cdf(double p) {
 // Inlined into the draw loops (A/B: C4 x64 -9%, C5 LEM -6%); the rarely
 // divergent AS241 tail stays out of line.
 // tab.score(i), tab.mu(), tab.sigma() return lem_score[i], sel_mu and
-// sel_sigma (the step constants, from global memory or a shared-memory copy).
+// sel_sigma (the step constants, from global memory or a shared-memory copy);
+// tab.normal(u) is inverse_normal_cdf(u).
 template <class Tab>
 __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, uint64_t seed, uint32_t step,
                                                uint32_t id) {
@@ -188,7 +202,7 @@ __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, ui
     const uint64_t bits = philox_bits(seed, step, kPhaseLemSelect, id, 0);
     const double u = __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
     const double mu = __dmul_rn(tab.mu(), cmax), sg = __dmul_rn(tab.sigma(), cmax);
-    double r = __dadd_rn(mu, __dmul_rn(sg, inverse_normal_cdf(u)));
+    double r = __dadd_rn(mu, __dmul_rn(sg, tab.normal(u)));
     r = (r < 0.0) ? 0.0 : ((cmax < r) ? cmax : r); // std::clamp(r, 0, C_max)
     // The open slot(s) nearest r (src/lem.cpp:38-52). The reference's scan
     // (reset on a strictly smaller gap, append on an equal one) ends with
@@ -214,15 +228,18 @@ __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, ui
     return __ffs(tied) - 1;
 }
 
+// The step constants in global memory (read-only path).
+struct GlobalLemTab {
+    const StepConsts* k;
+    __device__ double score(int i) const { return __ldg(&k->lem_score[i]); }
+    __device__ double mu() const { return __ldg(&k->sel_mu); }
+    __device__ double sigma() const { return __ldg(&k->sel_sigma); }
+    __device__ double normal(double u) const { return inverse_normal_cdf(u); }
+};
+
 static __device__ __forceinline__ int lem_choose(const StepConsts* __restrict__ k, uint32_t open, uint64_t seed,
                                        uint32_t step, uint32_t id) {
-    struct Tab {
-        const StepConsts* k;
-        __device__ double score(int i) const { return __ldg(&k->lem_score[i]); }
-        __device__ double mu() const { return __ldg(&k->sel_mu); }
-        __device__ double sigma() const { return __ldg(&k->sel_sigma); }
-    };
-    return lem_choose_with(Tab{k}, open, seed, step, id);
+    return lem_choose_with(GlobalLemTab{k}, open, seed, step, id);
 }
 
 // Slow path of aco_select (src/aco.cpp:64-92) given the numerators of the
