@@ -287,6 +287,20 @@ def run_reference_arm(args):
 
 # ------------------------------------------------------------------ GPU arm
 
+def _with_env(env, fn):
+    """fn() with the given environment variables set (read at context creation)."""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 def secondary_runs(steps):
     """Device timings beside the headline:
 
@@ -311,10 +325,17 @@ def secondary_runs(steps):
 
     peak, _ = measured_peak()
     out = {}
-    for name in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem", "c2_aco_x64", "c1_lem_x64",
-                 "c2_aco_1280", "c1_lem_1280", "c5_lem"):
+    for key in ("c4_aco_x64", "c3_lem_x64", "c4_aco", "c3_lem", "c2_aco", "c1_lem", "c1_lem@bitplane", "c2_aco_x64",
+                "c1_lem_x64", "c2_aco_1280", "c1_lem_1280", "c5_lem"):
+        # name@bitplane: the same workload on the bit-plane kernel
+        # (PEDFLOW_CLUSTER=0), beside the cluster-resident LEM path that sparse
+        # single grids take by default.
+        name, _, variant = key.partition("@")
         cfg, reps, desc = scenario(name)
-        ens = p.Ensemble(cfg, replicas=reps)
+        ens = _with_env({"PEDFLOW_CLUSTER": "0"} if variant else {}, lambda: p.Ensemble(cfg, replicas=reps))
+        if variant:
+            desc += " (bit-plane kernel, PEDFLOW_CLUSTER=0)"
+            name = name + "_bitplane"
         ens.run(5)
         n = min(steps if not name.startswith("c5") else 300, 1024)
         ens.ctx.prepare_steps(n)
@@ -404,6 +425,8 @@ def secondary_runs(steps):
     out["c5_aco_linked_shards_one_gpu"] = shard
     # SPEC acceptance #6: ACO <= 1.4x LEM time at 480x480, 20,480
     # agents, 500 steps (single scenario, and as a 64-seed batch).
+    # The single LEM run (8.9% density) takes the cluster-resident path by
+    # default; the ratio on one kernel for both models is beside it.
     spec6 = {}
     for reps in (1, 64):
         t = {}
@@ -413,6 +436,12 @@ def secondary_runs(steps):
             t[model.name.lower()], _ = ens.time_steps(500)
             ens.close()
         spec6[f"x{reps}"] = {"lem_ms": t["lem"], "aco_ms": t["aco"], "aco_over_lem": t["aco"] / t["lem"]}
+        if reps == 1:
+            cfg = p.ScenarioConfig(width=480, height=480, agents_per_side=10_240, model=p.Model.Lem, seed=42)
+            ens = _with_env({"PEDFLOW_CLUSTER": "0"}, lambda: p.Ensemble(cfg, replicas=1))
+            lem_bits, _ = ens.time_steps(500)
+            ens.close()
+            spec6["x1"].update({"lem_ms_bitplane": lem_bits, "aco_over_lem_bitplane": t["aco"] / lem_bits})
     out["spec6_aco_vs_lem_480_20480_500steps"] = spec6
     return out
 

@@ -22,3 +22,10 @@ for w in c4_aco_x64 c3_lem_x64; do
   timeout 300 ncu --set full --import-source on --clock-control none -k regex:step_bits -s 1 -c 1 \
     -o gpurun_out/${TAG}_${w}_s150 python tools/profile_step.py $w 150 fused 10 > gpurun_out/${TAG}_$w.log 2>&1
 done
+# Single sparse LEM scenario (C1) on the cluster-resident kernel: the launch
+# of steps 5..104 (before the crowds meet) and of steps 505..604 (jammed at
+# the goal rows).
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:lem_cluster -s 1 -c 1 \
+  -o gpurun_out/${TAG}_c1_lem_s5 python tools/profile_step.py c1_lem 5 fused 100 > gpurun_out/${TAG}_c1_lem_s5.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:lem_cluster -s 2 -c 1 \
+  -o gpurun_out/${TAG}_c1_lem_s505 python tools/profile_step.py c1_lem 505 fused 100 > gpurun_out/${TAG}_c1_lem_s505.log 2>&1
