@@ -97,16 +97,21 @@ __device__ __forceinline__ int slot_code(int slot, bool bottom) {
     return bottom ? 7 - c : c;
 }
 
-// Append the calling lanes' entries (pred) to a shared-memory list: one
-// counter atomic per warp. Every lane of the warp must call it.
-__device__ __forceinline__ void append(uint16_t* list, uint32_t* count, bool pred, uint16_t e) {
+// Append the calling lanes' entries (pred) to a shared-memory list of cap
+// entries: one counter atomic per warp. Every lane of the warp must call it.
+// The capacities are proven bounds (geometry()); an overflow would be an
+// internal error: it is not written and sets bit 2 of *err.
+__device__ __forceinline__ void append(uint16_t* list, uint32_t* count, bool pred, uint16_t e, uint32_t cap,
+                                       uint32_t* err) {
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, pred);
     if (m == 0u) return;
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     uint32_t base = 0;
     if (lane == leader) base = atomicAdd(count, uint32_t(__popc(m)));
     base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = e;
+    const uint32_t i = base + __popc(m & ((1u << lane) - 1u));
+    if (pred && i < cap) list[i] = e;
+    if (pred && i >= cap) atomicOr(err, 4u);
 }
 
 // glibc's log table (the AS241 tail) and the LEM constants in shared memory:
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
                 w = (((p.x | p.y) >> (c & 31)) & 1u) ? cw[b * W + c] : 0u;
             }
             if (lc <= cpc) word[at(r, lc)] = w;
-            append(agents0, &nagents[0], lc >= 0 && lc < ncols && w != 0u, entry(r, lc));
+            append(agents0, &nagents[0], lc >= 0 && lc < ncols && w != 0u, entry(r, lc), cap, a.err);
         }
     }
     cluster.sync();
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
             const uint16_t ent = e < na ? agents_in[e] : uint16_t(0);
             const int r = entry_row(ent), lc = entry_col(ent);
             const uint32_t w = e < na ? word[at(r, lc)] : 0u;
-            append(agents_out, &nagents[cur ^ 1], w != 0u, ent);  // the next step's list
+            append(agents_out, &nagents[cur ^ 1], w != 0u, ent, cap, a.err);  // the next step's list
             int ic = -1;
             if (w != 0u) {
                 const bool bottom = (w >> 30) == 2u;
@@ -245,17 +250,19 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
                 if (ld < 0) {
                     const int sh = 8 * ((cpc - 1) & 3);
                     if (((atomicOr(&claim_l[(rd * CP + cpc - 1) >> 2], bitv << sh) >> sh) & 0xFFu) == 0u)
-                        claimed_l[atomicAdd(&nclaims_l[cur], 1u)] = entry(rd, cpc - 1);
+                        if (const uint32_t i = atomicAdd(&nclaims_l[cur], 1u); i < uint32_t(cap)) claimed_l[i] = entry(rd, cpc - 1);
+                        else atomicOr(a.err, 4u);
                 } else if (ld >= ncols) {
                     if ((atomicOr(&claim_r[(rd * CP) >> 2], bitv) & 0xFFu) == 0u)
-                        claimed_r[atomicAdd(&nclaims_r[cur], 1u)] = entry(rd, 0);
+                        if (const uint32_t i = atomicAdd(&nclaims_r[cur], 1u); i < uint32_t(cap)) claimed_r[i] = entry(rd, 0);
+                        else atomicOr(a.err, 4u);
                 } else {
                     const int sh = 8 * (ld & 3);
                     first_local = ((atomicOr(&claim32[(rd * CP + ld) >> 2], bitv << sh) >> sh) & 0xFFu) == 0u;
                     dest = entry(rd, ld);
                 }
             }
-            append(claimed, &nclaims[cur], first_local, dest);
+            append(claimed, &nclaims[cur], first_local, dest, cap, a.err);
         }
 #ifdef PF_CLUSTER_TRACE
         tr[1] = clock64();
@@ -307,7 +314,7 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
                 if (lc == ncols - 1 && word_r) word_r[at(r, -1)] = nw;
                 arrived = true;
             }
-            append(agents_out, &nagents[cur ^ 1], arrived, ent);
+            append(agents_out, &nagents[cur ^ 1], arrived, ent, cap, a.err);
         }
         moved = __reduce_add_sync(0xFFFFFFFFu, moved);
         ntop = __reduce_add_sync(0xFFFFFFFFu, ntop);

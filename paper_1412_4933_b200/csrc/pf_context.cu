@@ -994,6 +994,7 @@ static int check_halo(pf_ctx* ctx) {
     PF_CUDA(cudaMemcpy(&err, ctx->d_err, 4, cudaMemcpyDeviceToHost));
     if (err & 1u) return fail(PF_ERR_COMM, "fused halo exchange: a neighbour shard did not complete its step (timeout)");
     if (err & 2u) return fail(PF_ERR_CUDA, "multi-step launch: a tile dependency wait timed out (internal error)");
+    if (err & 4u) return fail(PF_ERR_CUDA, "cluster-resident LEM kernel: a work list overflowed (internal error)");
     return PF_OK;
 }
 

@@ -51,4 +51,19 @@ for model in (p.Model.Lem, p.Model.Aco):
             c.synchronize()
             c.close()
         print(f"ok {model.name} {w}x{h} n={n} x{reps}", flush=True)
+# The cluster-resident LEM kernel (pf_cluster.cu): sparse single grids take it
+# by default; a dense one forced onto it; two replicas (two clusters); 16- and
+# 8-CTA clusters (a 16-column grid needs 2-column slices: 8 CTAs).
+for (w, h, n, reps, dens) in ((480, 480, 1024, 1, None), (96, 96, 200, 2, None), (96, 96, 3000, 1, "1"),
+                              (16, 64, 16, 1, "1")):
+    if dens:
+        os.environ["PEDFLOW_CLUSTER_MAX_DENSITY"] = dens
+    cfg = C(width=w, height=h, agents_per_side=n, model=p.Model.Lem, seed=5)
+    e = p.Ensemble(cfg, replicas=reps)
+    e.run(steps)
+    e.state(0)
+    e.audit(0)
+    e.close()
+    os.environ.pop("PEDFLOW_CLUSTER_MAX_DENSITY", None)
+    print(f"ok cluster LEM {w}x{h} n={n} x{reps}", flush=True)
 print("sanitize_run done")
