@@ -59,11 +59,17 @@ constexpr int NT = 1024;
 constexpr int NW = NT / 32;
 constexpr size_t kSmemMax = 227 * 1024 - 4096;  // dynamic shared memory per CTA (static: counters, tables)
 constexpr int kMaxSteps = 256;                  // steps per launch (the context's graph batch)
+// Replica batches (one cluster per replica, in waves when they outnumber the
+// resident clusters): C1 x64 (0.9% density, 8-CTA clusters in waves)
+// 23.6 -> 22.1 us/step; denser batches keep the bit-plane kernel.
+constexpr long long kMaxWaves = 8;
+constexpr double kMaxDensityBatch = 0.02;
 constexpr double kMaxDensity = 0.10;            // agents per cell (tools/cluster_sweep.py: faster up to ~12%)
 
 struct Geometry {
     int cl;   // CTAs per cluster (one replica per cluster)
     int cpc;  // columns per CTA
+    int cb;   // list-entry column bits
     int cap;  // entries per work list: min(2 x agents of the largest replica, cells per slice)
     size_t bytes;
 };
@@ -81,12 +87,8 @@ __host__ __device__ inline size_t smem_bytes(int H, int cpc, int cap) {
     return words_bytes(H, cpc) + claims_bytes(H, cpc) + 3 * size_t(cap) * 2;
 }
 
-// List entry (u16): row << 5 | slice column (slices of at most 32 columns,
-// grids of at most 2047 rows).
-constexpr int kColBits = 5;
-__device__ __forceinline__ uint16_t entry(int r, int lc) { return uint16_t(r << kColBits | lc); }
-__device__ __forceinline__ int entry_row(uint32_t e) { return int(e >> kColBits); }
-__device__ __forceinline__ int entry_col(uint32_t e) { return int(e & ((1u << kColBits) - 1u)); }
+// List entry (u16): row << cb | slice column, cb = the column bits of the
+// slice width (geometry()).
 
 // kDR / kDC / kSlotCodeTop as immediates (lanes index them divergently; the
 // constant bank would serialise the distinct addresses).
@@ -136,7 +138,7 @@ struct SharedLemTab {
 };
 
 __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, int slot_idx, int parity, int cpc,
-                                                            int cap) {
+                                                            int cap, int cb) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t cnt[kMaxSteps][3];       // per-step counters, flushed once at the end
     __shared__ uint32_t nagents[2], nclaims[2];  // list lengths, by step parity
@@ -154,6 +156,9 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
     uint32_t* const claim32 = reinterpret_cast<uint32_t*>(claim8);
     uint16_t* const agents0 = reinterpret_cast<uint16_t*>(claim8 + claims_bytes(H, cpc));
     uint16_t* const claimed = agents0 + 2 * size_t(cap);
+    auto entry = [cb](int r, int lc) { return uint16_t(r << cb | lc); };
+    auto entry_row = [cb](uint32_t e) { return int(e >> cb); };
+    auto entry_col = [cb](uint32_t e) { return int(e & ((1u << cb) - 1u)); };
     // Word (r, lc), r in -1 .. H, lc in -1 .. cpc.
     auto at = [P](int r, int lc) { return (r + 1) * P + (lc + 1); };
     // The neighbours' arrays (same geometry).
@@ -381,7 +386,9 @@ static Geometry geometry(const StepArgs& a, int cl, uint32_t max_agents) {
     // A list holds distinct cells of the slice: the step-start agents (some of
     // which leave) plus the arrivals, so at most twice the agents.
     const int cap = int(std::min<long long>(2LL * max_agents, (long long)a.rows_owned * cpc));
-    return Geometry{cl, cpc, cap, smem_bytes(a.rows_owned, cpc, cap)};
+    int cb = 1;
+    while ((1 << cb) < cpc) ++cb;
+    return Geometry{cl, cpc, cb, cap, smem_bytes(a.rows_owned, cpc, cap)};
 }
 
 }  // namespace cluster_lem
@@ -401,12 +408,16 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
         cudaGetLastError();
         return 0;
     }
+    // Replicas beyond the resident clusters run in waves (one replica per
+    // cluster for the whole launch): take the cluster size with the fewest
+    // waves, 16 CTAs on a tie.
+    int best = 0;
+    long long best_waves = 0;
     for (int cl : {16, 8}) {
         const Geometry g = geometry(a, cl, max_agents);
         // Slices of at least 2 columns: a remote source clear then has exactly
         // one ghost copy (the clearing CTA's own).
-        if (g.bytes > kSmemMax || g.cpc < 2 || g.cpc > (1 << kColBits) || a.rows_owned >= (1 << (16 - kColBits)))
-            continue;
+        if (g.bytes > kSmemMax || g.cpc < 2 || a.rows_owned >= (1 << (16 - g.cb))) continue;
         if (cudaFuncSetAttribute(lem_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) !=
             cudaSuccess) {
             cudaGetLastError();
@@ -428,12 +439,19 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
             cudaGetLastError();
             continue;
         }
-        if (clusters >= a.replicas) {
+        if (clusters < 1) continue;
+        const long long waves = (a.replicas + clusters - 1) / clusters;
+        if (best == 0 || waves < best_waves) {
+            best = cl;
+            best_waves = waves;
             *cap = g.cap;
-            return cl;
         }
     }
-    return 0;
+    const double batch_density = dens ? max_density : kMaxDensityBatch;
+    if (a.replicas > 1 &&
+        (best_waves > kMaxWaves || double(max_agents) > batch_density * double(a.k.W) * double(a.k.H)))
+        return 0;
+    return best;
 }
 
 // a.nsteps steps as one cluster-resident launch; returns the launches issued.
@@ -443,6 +461,7 @@ int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t
     Geometry g = geometry(a, a.cluster, 0);
     g.cap = a.cluster_cap;
     g.bytes = smem_bytes(a.rows_owned, g.cpc, g.cap);
+    // (replicas beyond the resident clusters queue: waves)
     // The attribute is per function; another context may have planned a
     // smaller footprint since.
     if (cudaFuncSetAttribute(lem_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) != cudaSuccess)
@@ -461,7 +480,7 @@ int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, lem_cluster_kernel, a, slot_idx, parity, g.cpc, g.cap) != cudaSuccess) {
+    if (cudaLaunchKernelEx(&cfg, lem_cluster_kernel, a, slot_idx, parity, g.cpc, g.cap, g.cb) != cudaSuccess) {
         cudaGetLastError();
         return 0;  // the bit-plane kernel takes the step
     }

@@ -78,8 +78,9 @@ def test_cluster_replicas_match_single_runs():
 
     kw = dict(width=96, height=96, agents_per_side=900, model="lem", seed=100)
     ens = p.Ensemble(to_config(kw), replicas=5, seed=100)
+    l0 = ens.ctx.launches
     rep = ens.run(120)
-    assert ens.ctx.launches < 60
+    assert ens.ctx.launches - l0 < 10
     for i in range(5):
         ora = OracleState(to_scenario(dict(kw, seed=100 + i)))
         o = ora.run(120)
@@ -131,3 +132,24 @@ def test_default_density_cut(monkeypatch):
         kw = dict(width=480, height=480, agents_per_side=n, model="lem")
         _, _, launches = _run(kw, 100, {})
         assert (launches < 50) == cluster, (n, launches)
+
+
+def test_sparse_batch_in_waves_vs_oracle(monkeypatch):
+    """A sparse 64-replica C1 batch runs one cluster per replica in waves
+    (more replicas than resident clusters); replicas 0, 31 and 63 against the
+    oracle over 300 steps."""
+    import paper_1412_4933_b200 as p
+    from oracle.oracle import OracleState
+
+    monkeypatch.delenv("PEDFLOW_CLUSTER_MAX_DENSITY")
+    kw = dict(width=480, height=480, agents_per_side=1024, model="lem", seed=7)
+    ens = p.Ensemble(to_config(kw), replicas=64, seed=7)
+    l0 = ens.ctx.launches  # (after the setup kernels)
+    rep = ens.run(300)
+    assert ens.ctx.launches - l0 < 10  # batches of <= 256 steps, one launch each
+    for i in (0, 31, 63):
+        ora = OracleState(to_scenario(dict(kw, seed=7 + i)))
+        o = ora.run(300)
+        assert (rep[i]["moved"] == o["moved"]).all()
+        assert (rep[i]["newly_crossed_bottom"] == o["newly_crossed_bottom"]).all()
+        assert first_divergence(ens.state(i), ora) == "identical"
