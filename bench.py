@@ -512,23 +512,37 @@ def run_gpu_arm(args):
         time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
         eng.step(args.warmup)  # the W untimed warm-up steps (also keep the GPU busy for the sampler)
         eng.synchronize()
+        t_wait = time.perf_counter()
+        while len(clocks.lines) < 2 and time.perf_counter() - t_wait < 5.0:  # the sampler is producing
+            time.sleep(0.02)
         if world == 1:
             eng.ctx.prepare_steps(args.steps)  # graph capture stays outside the timed region
-        barrier()
-        torch.cuda.synchronize()
-        launches0 = eng.ctx.launches
-        clocks.mark("t0")
-        e0.record(stream)
-        if world == 1:
-            eng.ctx.step_async(args.steps)  # CUDA-graph batches
-        else:
-            eng.step(args.steps)
-        e1.record(stream)
-        e1.synchronize()
-        torch.cuda.synchronize()
-        clocks.mark("t1")
-        time.sleep(0.06)  # nvidia-smi's last samples of the region
-        launches = eng.ctx.launches - launches0
+        # A timed region shorter than nvidia-smi's sampling can miss every
+        # sample: it is then timed again (the next K steps; at most 3 times,
+        # the same on every rank) and the attempt with clock samples reported.
+        for attempt in range(3):
+            barrier()
+            torch.cuda.synchronize()
+            launches0 = eng.ctx.launches
+            clocks.mark("t0")
+            e0.record(stream)
+            if world == 1:
+                eng.ctx.step_async(args.steps)  # CUDA-graph batches
+            else:
+                eng.step(args.steps)
+            e1.record(stream)
+            e1.synchronize()
+            torch.cuda.synchronize()
+            clocks.mark("t1")
+            time.sleep(0.06)  # nvidia-smi's last samples of the region
+            launches = eng.ctx.launches - launches0
+            sampled = torch.tensor([clocks.summary()["samples"]], device=f"cuda:{local}")
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(sampled, op=dist.ReduceOp.MIN)
+            if int(sampled.item()) > 0:
+                break
+        timed_attempts = attempt + 1
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     rep = eng.reports(min(args.steps, 1024))
@@ -591,7 +605,7 @@ def run_gpu_arm(args):
                                   "alg_bytes_per_launch": rl["bitplane"]["alg_bytes_per_launch"],
                                   "alg_bytes_model": BITPLANE_MODEL, "movers_per_step": movers},
             "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": dict(clocks.summary(), timed_attempts=timed_attempts),
             "setup_s": setup_s,
             "setup_warm_s": setup_warm_s,
             "cuda_context_s": cuda_context_s,
