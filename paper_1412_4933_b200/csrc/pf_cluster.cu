@@ -413,7 +413,9 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
     // waves, 16 CTAs on a tie.
     int best = 0;
     long long best_waves = 0;
+    const char* csz = std::getenv("PEDFLOW_CLUSTER_SIZE");  // dev: 16 or 8 only
     for (int cl : {16, 8}) {
+        if (csz && std::atoi(csz) != cl) continue;
         const Geometry g = geometry(a, cl, max_agents);
         // Slices of at least 2 columns: a remote source clear then has exactly
         // one ghost copy (the clearing CTA's own).
