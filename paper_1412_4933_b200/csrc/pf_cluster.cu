@@ -55,8 +55,11 @@ namespace cluster_lem {
 
 using namespace pfdev;
 
-constexpr int NT = 1024;
-constexpr int NW = NT / 32;
+// Threads per CTA: 512 when a CTA's slice holds at most one agent per thread
+// on average (C1: 128), else 1,024 (kernel template parameter; picked in
+// plan_cluster_lem). A/B on C1: 512 threads 2.2 / 4.1 us per step before /
+// after the crowds meet, 1,024 threads 2.5 / 4.4 us (fewer idle warps at the
+// cluster barriers); at 10,240 agents per side 1,024 threads are 5% faster.
 constexpr size_t kSmemMax = 227 * 1024 - 4096;  // dynamic shared memory per CTA (static: counters, tables)
 constexpr int kMaxSteps = 256;                  // steps per launch (the context's graph batch)
 // Replica batches (one cluster per replica, in waves when they outnumber the
@@ -137,8 +140,10 @@ struct SharedLemTab {
     __device__ double normal(double u) const { return inverse_normal_cdf_shared(u, logt); }
 };
 
+template <int NT>
 __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, int slot_idx, int parity, int cpc,
                                                             int cap, int cb) {
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t cnt[kMaxSteps][3];       // per-step counters, flushed once at the end
     __shared__ uint32_t nagents[2], nclaims[2];  // list lengths, by step parity
@@ -393,7 +398,10 @@ static Geometry geometry(const StepArgs& a, int cl, uint32_t max_agents) {
 
 }  // namespace cluster_lem
 
-int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
+// The kernel instantiation for a thread count.
+static auto kernel_for(int nt) { return nt == 512 ? cluster_lem::lem_cluster_kernel<512> : cluster_lem::lem_cluster_kernel<1024>; }
+
+int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap, int* nt) {
     using namespace cluster_lem;
     if (a.k.model != 0 || a.small_tiles == 1) return 0;
     if (a.row_begin != 0 || a.rows_owned != a.k.H) return 0;
@@ -404,10 +412,11 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
     const char* dens = std::getenv("PEDFLOW_CLUSTER_MAX_DENSITY");  // dev override
     const double max_density = dens ? std::atof(dens) : kMaxDensity;
     if (double(max_agents) > max_density * double(a.k.W) * double(a.k.H)) return 0;
-    if (cudaFuncSetAttribute(lem_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
+    for (int t : {512, 1024})
+        if (cudaFuncSetAttribute(kernel_for(t), cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
     // Replicas beyond the resident clusters run in waves (one replica per
     // cluster for the whole launch): take the cluster size with the fewest
     // waves, 16 CTAs on a tie.
@@ -420,14 +429,16 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
         // Slices of at least 2 columns: a remote source clear then has exactly
         // one ghost copy (the clearing CTA's own).
         if (g.bytes > kSmemMax || g.cpc < 2 || a.rows_owned >= (1 << (16 - g.cb))) continue;
-        if (cudaFuncSetAttribute(lem_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) !=
+        const int threads = max_agents <= 512u * uint32_t(cl) ? 512 : 1024;
+        const auto kernel = kernel_for(threads);
+        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) !=
             cudaSuccess) {
             cudaGetLastError();
             continue;
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(cl * a.replicas));
-        cfg.blockDim = dim3(NT);
+        cfg.blockDim = dim3(unsigned(threads));
         cfg.dynamicSmemBytes = g.bytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -437,7 +448,7 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, lem_cluster_kernel, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg) != cudaSuccess) {
             cudaGetLastError();
             continue;
         }
@@ -447,6 +458,7 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap) {
             best = cl;
             best_waves = waves;
             *cap = g.cap;
+            *nt = threads;
         }
     }
     const double batch_density = dens ? max_density : kMaxDensityBatch;
@@ -466,11 +478,12 @@ int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t
     // (replicas beyond the resident clusters queue: waves)
     // The attribute is per function; another context may have planned a
     // smaller footprint since.
-    if (cudaFuncSetAttribute(lem_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) != cudaSuccess)
+    const auto kernel = kernel_for(a.cluster_nt);
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bytes)) != cudaSuccess)
         return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(g.cl * a.replicas));
-    cfg.blockDim = dim3(NT);
+    cfg.blockDim = dim3(unsigned(a.cluster_nt));
     cfg.dynamicSmemBytes = g.bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -482,7 +495,7 @@ int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, lem_cluster_kernel, a, slot_idx, parity, g.cpc, g.cap, g.cb) != cudaSuccess) {
+    if (cudaLaunchKernelEx(&cfg, kernel, a, slot_idx, parity, g.cpc, g.cap, g.cb) != cudaSuccess) {
         cudaGetLastError();
         return 0;  // the bit-plane kernel takes the step
     }

@@ -326,7 +326,9 @@ static void set_cluster(pf_ctx* ctx) {
     uint32_t most = 0;
     for (const auto& r : ctx->reps) most = std::max(most, r.n_agents);
     ctx->args.cluster_cap = 0;
-    ctx->args.cluster = ctx->bits() ? pfk::plan_cluster_lem(ctx->args, most, &ctx->args.cluster_cap) : 0;
+    ctx->args.cluster_nt = 1024;
+    ctx->args.cluster =
+        ctx->bits() ? pfk::plan_cluster_lem(ctx->args, most, &ctx->args.cluster_cap, &ctx->args.cluster_nt) : 0;
 }
 
 static int fill_consts(pf_ctx* ctx) {

@@ -92,6 +92,7 @@ struct StepArgs {
     // Planned once per context (plan_cluster_lem).
     int cluster;
     int cluster_cap;        // its work-list capacity (entries)
+    int cluster_nt;         // its threads per CTA (512 or 1024)
 };
 
 // Launch one step (batch slot `slot`, reading parity `parity`) on `s`.
@@ -101,7 +102,7 @@ int configure_step_bits();
 // Cluster-resident LEM kernel (pf_cluster.cu): the cluster size for these
 // args and the largest replica's agent count (0 = not applicable), and a
 // launch of a.nsteps steps with it.
-int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap);
+int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap, int* nt);
 int launch_cluster_lem(const StepArgs& a, int slot, int parity, cudaStream_t s);
 int bits_strip_segments(int width, int model, bool tau_f32);  // strip width in segments (8 or 10)
 // Occupancy planes of rows [0, rows) from cell words (W columns; padding
