@@ -18,7 +18,8 @@
 // each side (copies of the neighbours' edge columns, kWall at the arena's
 // edges) and a wall row above and below, so every proposal reads local
 // shared memory only. The work of a step is listed, not scanned: the slice's
-// agents (u16 entries row << 5 | column) and its claimed cells.
+// agents (u16 entries row << cb | column) and its claimed cells. Sparse
+// replica batches run one cluster per replica, in waves.
 //
 // One step (StepEngine::step, src/engine.cpp:53-193):
 //   S1  per listed agent: the LEM proposal (score_phase + intention_phase,
