@@ -64,7 +64,7 @@ using namespace pfdev;
 constexpr size_t kSmemMax = 227 * 1024 - 4096;  // dynamic shared memory per CTA (static: counters, tables)
 constexpr int kMaxSteps = 256;                  // steps per launch (the context's graph batch)
 // Replica batches (one cluster per replica, in waves when they outnumber the
-// resident clusters): C1 x64 (0.9% density, 8-CTA clusters in waves)
+// resident clusters): C1 x64 (0.9% density, clusters in waves)
 // 23.4 -> 16.4 us/step; denser batches keep the bit-plane kernel.
 constexpr long long kMaxWaves = 8;
 constexpr double kMaxDensityBatch = 0.02;
