@@ -132,6 +132,7 @@ static __device__ __noinline__ double inverse_normal_cdf_shared(double p, const 
     return inverse_normal_cdf_with(SharedLogTab{t}, p);
 }
 struct SharedLemTab {
+    static constexpr bool kEagerTie = true;  // (the draw chain is this kernel's critical path)
     const double* tab;
     const double* logt;
     double m, sg;

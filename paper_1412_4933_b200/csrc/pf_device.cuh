@@ -198,6 +198,10 @@ __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, ui
     // d_L < d_B < d_BL) and dmin/d_i shrinks, so that is the first open
     // slot's score (host-checked in fill_consts).
     const double cmax = tab.score(__ffs(open) - 1);
+    // Tab::kEagerTie: the tie-break bits drawn up front, independent of (and
+    // interleaved with) the selection draw, instead of after the gap scan.
+    [[maybe_unused]] uint64_t tie_bits;
+    if constexpr (Tab::kEagerTie) tie_bits = philox_bits(seed, step, kPhaseTieBreak, id, 0);
     // normal(key, mu_sel*C_max, sigma_sel*C_max) (src/lem.cpp:34, src/rng.cpp:152-156)
     const uint64_t bits = philox_bits(seed, step, kPhaseLemSelect, id, 0);
     const double u = __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
@@ -220,7 +224,9 @@ __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, ui
     for (int i = 0; i < 8; ++i) tied |= uint32_t((open >> i & 1u) != 0u && gap[i] == best) << i;
     const int ntied = __popc(tied);
     if (ntied > 1) {  // tie break: uniform(key.with_phase(TieBreak)) (src/lem.cpp:54-58)
-        const double tu = uniform_from_bits(philox_bits(seed, step, kPhaseTieBreak, id, 0));
+        double tu;
+        if constexpr (Tab::kEagerTie) tu = uniform_from_bits(tie_bits);
+        else tu = uniform_from_bits(philox_bits(seed, step, kPhaseTieBreak, id, 0));
         int j = __double2int_rz(__dmul_rn(tu, double(ntied)));
         j = j < ntied - 1 ? j : ntied - 1;
         for (int t = 0; t < j; ++t) tied &= tied - 1u;  // drop the j lowest
@@ -230,6 +236,7 @@ __device__ __forceinline__ int lem_choose_with(const Tab& tab, uint32_t open, ui
 
 // The step constants in global memory (read-only path).
 struct GlobalLemTab {
+    static constexpr bool kEagerTie = false;
     const StepConsts* k;
     __device__ double score(int i) const { return __ldg(&k->lem_score[i]); }
     __device__ double mu() const { return __ldg(&k->sel_mu); }
