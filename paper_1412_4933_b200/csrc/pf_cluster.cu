@@ -261,13 +261,17 @@ __global__ void __launch_bounds__(NT, 1) lem_cluster_kernel(const StepArgs a, in
                 const uint32_t bitv = 1u << (7 - ic);
                 if (ld < 0) {
                     const int sh = 8 * ((cpc - 1) & 3);
-                    if (((atomicOr(&claim_l[(rd * CP + cpc - 1) >> 2], bitv << sh) >> sh) & 0xFFu) == 0u)
-                        if (const uint32_t i = atomicAdd(&nclaims_l[cur], 1u); i < uint32_t(cap)) claimed_l[i] = entry(rd, cpc - 1);
+                    if (((atomicOr(&claim_l[(rd * CP + cpc - 1) >> 2], bitv << sh) >> sh) & 0xFFu) == 0u) {
+                        const uint32_t i = atomicAdd(&nclaims_l[cur], 1u);
+                        if (i < uint32_t(cap)) claimed_l[i] = entry(rd, cpc - 1);
                         else atomicOr(a.err, 4u);
+                    }
                 } else if (ld >= ncols) {
-                    if ((atomicOr(&claim_r[(rd * CP) >> 2], bitv) & 0xFFu) == 0u)
-                        if (const uint32_t i = atomicAdd(&nclaims_r[cur], 1u); i < uint32_t(cap)) claimed_r[i] = entry(rd, 0);
+                    if ((atomicOr(&claim_r[(rd * CP) >> 2], bitv) & 0xFFu) == 0u) {
+                        const uint32_t i = atomicAdd(&nclaims_r[cur], 1u);
+                        if (i < uint32_t(cap)) claimed_r[i] = entry(rd, 0);
                         else atomicOr(a.err, 4u);
+                    }
                 } else {
                     const int sh = 8 * (ld & 3);
                     first_local = ((atomicOr(&claim32[(rd * CP + ld) >> 2], bitv << sh) >> sh) & 0xFFu) == 0u;
