@@ -128,9 +128,6 @@ struct SharedLogTab {
     __device__ double tab(int i, int j) const { return t[2 * i + j]; }
     __device__ double poly(int i) const { return t[256 + i]; }
 };
-static __device__ __noinline__ double inverse_normal_cdf_shared(double p, const double* t) {
-    return inverse_normal_cdf_with(SharedLogTab{t}, p);
-}
 struct SharedLemTab {
     static constexpr bool kEagerTie = true;  // (the draw chain is this kernel's critical path)
     const double* tab;
@@ -139,7 +136,9 @@ struct SharedLemTab {
     __device__ double score(int i) const { return tab[i]; }
     __device__ double mu() const { return m; }
     __device__ double sigma() const { return sg; }
-    __device__ double normal(double u) const { return inverse_normal_cdf_shared(u, logt); }
+    // Inlined here (the other kernels call it out of line): no call/return and
+    // register save around it on the draw chain (jammed C1 4.05 -> 3.94 us).
+    __device__ double normal(double u) const { return inverse_normal_cdf_with(SharedLogTab{logt}, u); }
 };
 
 template <int NT>
