@@ -63,6 +63,10 @@ using namespace pfdev;
 // cluster barriers); at 10,240 agents per side 1,024 threads are 5% faster.
 constexpr size_t kSmemMax = 227 * 1024 - 4096;  // dynamic shared memory per CTA (static: counters, tables)
 constexpr int kMaxSteps = 256;                  // steps per launch (the context's graph batch)
+// Shorter launches take the bit-plane kernel: loading and writing back the
+// replica costs ~24 us per launch (C1 one step per launch: 27 us against
+// 8.2 us on the bit-plane kernel), so the cluster kernel pays from ~5 steps on.
+constexpr int kMinSteps = 8;
 // Replica batches (one cluster per replica, in waves when they outnumber the
 // resident clusters): C1 x64 (0.9% density, clusters in waves)
 // 23.4 -> 16.4 us/step; denser batches keep the bit-plane kernel.
@@ -476,7 +480,7 @@ int plan_cluster_lem(const StepArgs& a, uint32_t max_agents, int* cap, int* nt) 
 // a.nsteps steps as one cluster-resident launch; returns the launches issued.
 int launch_cluster_lem(const StepArgs& a, int slot_idx, int parity, cudaStream_t s) {
     using namespace cluster_lem;
-    if (a.nsteps > kMaxSteps) return 0;
+    if (a.nsteps > kMaxSteps || a.nsteps < kMinSteps) return 0;
     Geometry g = geometry(a, a.cluster, 0);
     g.cap = a.cluster_cap;
     g.bytes = smem_bytes(a.rows_owned, g.cpc, g.cap);

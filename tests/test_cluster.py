@@ -93,7 +93,9 @@ def test_cluster_replicas_match_single_runs():
 def test_cluster_odd_shapes_vs_oracle(shape):
     """Widths that are multiples of 16 but not of 32 (partial plane
     segments and claim words), few rows, and batches split at odd step
-    counts (one launch per call: 1, 7, 13, ... steps)."""
+    counts (one launch per call: 1, 7, 13, ... steps; the 1- and 7-step
+    calls run on the bit-plane kernel, so the two kernels alternate on one
+    state)."""
     import paper_1412_4933_b200 as p
     from oracle.oracle import OracleState
 
@@ -114,8 +116,9 @@ def test_cluster_odd_shapes_vs_oracle(shape):
 
 
 def test_cluster_one_launch_per_step_matches_batches():
-    """PEDFLOW_MULTISTEP=0 (one single-step cluster launch per step) against
-    the default batched launch, C3 over 150 steps."""
+    """PEDFLOW_MULTISTEP=0 (one launch per step: the bit-plane kernel, as
+    every launch of fewer than 8 steps) against the default batched cluster
+    launch, C3 over 150 steps."""
     kw = dict(width=480, height=480, agents_per_side=51200, model="lem")
     s1, r1, l1 = _run(kw, 150, {"PEDFLOW_MULTISTEP": "0"})
     s2, r2, l2 = _run(kw, 150, {"PEDFLOW_MULTISTEP": "1"})
